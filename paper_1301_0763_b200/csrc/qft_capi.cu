@@ -1,0 +1,417 @@
+// qft_capi.cu -- the C ABI declared in include/qft_b200.h: plans (constant
+// tables built with the reference's two-tier recipe), dispatch to the
+// per-size transform kernels (qft_inst.cu), layout conversion for the
+// reference's (N, batch) layout, the pipelined host path, and the seeded
+// device input generator used by the benchmarks.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/qft_b200.h"
+#include "qft_launch.cuh"
+
+using namespace qft;
+
+// ============================================================== errors
+static thread_local std::string g_last_error;
+static int fail(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+#define CUDA_TRY(expr)                                                                  \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            return fail(QFT_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+// ============================================================== constants
+// Two-tier recipe of counting.py:116-140.  float64: cos in x87 long double with
+// a 50-digit pi, 1/(2c) in long double, rounded once.  float32: in double,
+// rounded once.  Depends only on the reduced fraction m/N (exact here).
+static const long double kWidePi = 3.14159265358979323846264338327950288419716939937510L;
+
+static void natural_table_f64(int N, std::vector<double> &T) {
+    T.assign(N / 4, 0.0);
+    T[0] = (double)cosl(2.0L * kWidePi * (1.0L / 8.0L));
+    for (int m = 1; m < N / 4; ++m) {
+        long double c = cosl(2.0L * kWidePi * ((long double)m / (long double)N));
+        T[m] = (double)(1.0L / (2.0L * c));
+    }
+}
+static void natural_table_f32(int N, std::vector<float> &T) {
+    T.assign(N / 4, 0.0f);
+    T[0] = (float)cos(2.0 * M_PI * (1.0 / 8.0));
+    for (int m = 1; m < N / 4; ++m) {
+        double c = cos(2.0 * M_PI * ((double)m / (double)N));
+        T[m] = (float)(1.0 / (2.0 * c));
+    }
+}
+// level table U (qft_lee.cuh): U[0] = cos8, U[S/2+i] = T[(2i+1) N/(4S)]
+template <typename T>
+static void level_table(int N, const std::vector<T> &Tn, std::vector<T> &U) {
+    U.assign(N / 4 >= 2 ? N / 4 : 2, (T)0);
+    if (N < 8) return;
+    U[0] = Tn[0];
+    for (int S = 2; S <= N / 4; S *= 2)
+        for (int i = 0; i < S / 2; ++i) U[S / 2 + i] = Tn[(size_t)(2 * i + 1) * (N / (4 * S))];
+}
+
+// (N, batch) <-> (batch, N) for complex elements: tiled transpose through smem.
+// dst[b*N + n] = src[n*B + b]  (to_batch_major)   /   dst[n*B + b] = src[b*N + n]
+template <typename T>
+__global__ void qft_transpose(const vec2<T> *__restrict__ src, vec2<T> *__restrict__ dst, long long rows,
+                              long long cols) {
+    // src is rows x cols (row-major), dst is cols x rows
+    __shared__ vec2<T> tile[32][33];
+    long long c0 = (long long)blockIdx.x * 32, r0 = (long long)blockIdx.y * 32;
+    int tx = threadIdx.x, ty = threadIdx.y;
+    for (int i = ty; i < 32; i += 8) {
+        long long r = r0 + i, c = c0 + tx;
+        if (r < rows && c < cols) tile[i][tx] = src[r * cols + c];
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+        long long c = c0 + i, r = r0 + tx;
+        if (r < rows && c < cols) dst[c * rows + r] = tile[tx][i];
+    }
+}
+
+// general strided gather / scatter (rare layouts)
+template <typename T>
+__global__ void qft_strided_copy(const vec2<T> *__restrict__ src, vec2<T> *__restrict__ dst, long long batch,
+                                 int N, long long sbs, long long ses, long long dbs, long long des) {
+    long long total = batch * N;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        long long b = idx / N, n = idx % N;
+        dst[b * dbs + n * des] = src[b * sbs + n * ses];
+    }
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+template <typename T>
+__global__ void qft_fill_normal_kernel(vec2<T> *out, long long batch, int N, long long first, uint64_t seed) {
+    long long total = batch * N;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        long long b = idx / N, n = idx % N;
+        uint64_t key = splitmix64(seed ^ splitmix64((uint64_t)(first + b) * 0x100000001B3ull + (uint64_t)n));
+        uint64_t k2 = splitmix64(key);
+        double u1 = ((key >> 11) + 1) * (1.0 / 9007199254740993.0);  // (0, 1]
+        double u2 = (k2 >> 11) * (1.0 / 9007199254740992.0);         // [0, 1)
+        double r = sqrt(-2.0 * log(u1));
+        double s, c;
+        sincospi(2.0 * u2, &s, &c);
+        out[idx] = {(T)(r * c), (T)(r * s)};
+    }
+}
+
+// ============================================================== plan
+struct qft_plan {
+    int log2n = 0, N = 0, prec = 0, algo = 0, device = 0;
+    int num_sms = 0;
+    void *d_U = nullptr;
+    size_t u_bytes = 0;
+    std::vector<double> t64;
+    std::vector<float> t32;
+    // scratch for layout conversion / host path
+    void *d_scratch = nullptr;
+    size_t scratch_bytes = 0;
+    cudaStream_t streams[2] = {nullptr, nullptr};
+    std::mutex mu;
+};
+
+// per-instance launchers, one translation unit each (qft_inst.cu)
+#define QFT_DECL(P, L) int qft_inst_launch_##P##_##L(const LaunchArgs *);
+#define QFT_DECL_ALL(P) \
+    QFT_DECL(P, 1) QFT_DECL(P, 2) QFT_DECL(P, 3) QFT_DECL(P, 4) QFT_DECL(P, 5) QFT_DECL(P, 6) QFT_DECL(P, 7) \
+    QFT_DECL(P, 8) QFT_DECL(P, 9) QFT_DECL(P, 10) QFT_DECL(P, 11) QFT_DECL(P, 12)
+QFT_DECL_ALL(32)
+QFT_DECL_ALL(64)
+typedef int (*launch_fn)(const LaunchArgs *);
+#define QFT_ROW(P)                                                                                              \
+    {nullptr, qft_inst_launch_##P##_1, qft_inst_launch_##P##_2, qft_inst_launch_##P##_3, qft_inst_launch_##P##_4, \
+     qft_inst_launch_##P##_5, qft_inst_launch_##P##_6, qft_inst_launch_##P##_7, qft_inst_launch_##P##_8,         \
+     qft_inst_launch_##P##_9, qft_inst_launch_##P##_10, qft_inst_launch_##P##_11, qft_inst_launch_##P##_12}
+static const launch_fn kLaunch[2][13] = {QFT_ROW(32), QFT_ROW(64)};
+static constexpr int kMaxLog2N = 12;
+
+static int launch_contig(const qft_plan *p, const void *in, void *out, long long batch, cudaStream_t st) {
+    if (p->log2n < 1 || p->log2n > kMaxLog2N)
+        return fail(QFT_EUNSUPPORTED, "periodization 2^" + std::to_string(p->log2n) + " not built yet");
+    LaunchArgs a{in, out, batch, p->d_U, p->num_sms, st};
+    int e = kLaunch[p->prec == QFT_PREC_F32 ? 0 : 1][p->log2n](&a);
+    if (e != 0) return fail(QFT_ECUDA, std::string("kernel launch: ") + cudaGetErrorString((cudaError_t)e));
+    return 0;
+}
+
+static bool size_supported(int log2n) { return log2n >= 1 && log2n <= kMaxLog2N; }
+
+// Exported functions inherit C linkage from their extern "C" declarations in qft_b200.h.
+
+int qft_version(void) { return 100; }
+
+const char *qft_last_error(void) { return g_last_error.c_str(); }
+
+int qft_plan_create(qft_plan **out, int log2n, int prec, int algo, int device) {
+    if (!out) return fail(QFT_EINVAL, "plan pointer is NULL");
+    *out = nullptr;
+    if (log2n < 1 || log2n > 30) return fail(QFT_EINVAL, "periodization must be a power of two >= 2");
+    if (prec != QFT_PREC_F32 && prec != QFT_PREC_F64) return fail(QFT_EINVAL, "prec must be 32 or 64");
+    if (algo != QFT_ALGO_IMPROVED) return fail(QFT_EUNSUPPORTED, "only the improved algorithm is built on the GPU");
+    if (!size_supported(log2n))
+        return fail(QFT_EUNSUPPORTED, "periodization 2^" + std::to_string(log2n) + " not built yet");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(QFT_EINVAL, "bad device ordinal");
+    CUDA_TRY(cudaSetDevice(device));
+    qft_plan *p = new qft_plan();
+    p->log2n = log2n;
+    p->N = 1 << log2n;
+    p->prec = prec;
+    p->algo = algo;
+    p->device = device;
+    cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
+    int rc = 0;
+    if (prec == QFT_PREC_F64) {
+        std::vector<double> U;
+        if (p->N >= 8) natural_table_f64(p->N, p->t64);
+        level_table(p->N, p->t64, U);
+        p->u_bytes = U.size() * sizeof(double);
+        if (cudaMalloc(&p->d_U, p->u_bytes) != cudaSuccess ||
+            cudaMemcpy(p->d_U, U.data(), p->u_bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+            rc = fail(QFT_ECUDA, "table upload failed");
+    } else {
+        std::vector<float> U;
+        if (p->N >= 8) natural_table_f32(p->N, p->t32);
+        level_table(p->N, p->t32, U);
+        p->u_bytes = U.size() * sizeof(float);
+        if (cudaMalloc(&p->d_U, p->u_bytes) != cudaSuccess ||
+            cudaMemcpy(p->d_U, U.data(), p->u_bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+            rc = fail(QFT_ECUDA, "table upload failed");
+    }
+    if (rc) {
+        qft_plan_destroy(p);
+        return rc;
+    }
+    *out = p;
+    return 0;
+}
+
+int qft_plan_destroy(qft_plan *p) {
+    if (!p) return 0;
+    cudaSetDevice(p->device);
+    if (p->d_U) cudaFree(p->d_U);
+    if (p->d_scratch) cudaFree(p->d_scratch);
+    for (auto &s : p->streams)
+        if (s) cudaStreamDestroy(s);
+    delete p;
+    return 0;
+}
+
+int qft_plan_get_info(const qft_plan *p, qft_plan_info_t *info) {
+    if (!p || !info) return fail(QFT_EINVAL, "NULL argument");
+    memset(info, 0, sizeof(*info));
+    info->log2n = p->log2n;
+    info->prec = p->prec;
+    info->algo = p->algo;
+    info->passes = 1;
+    info->kernel_launches = 1;
+    info->smem_bytes = smem_bytes_for(p->log2n, p->prec);
+    info->threads_per_cta = p->log2n >= 6 ? kSmemWarps * 32 : 128;
+    info->ctas_per_sm = 0;
+    info->scratch_bytes = (int64_t)p->scratch_bytes;
+    return 0;
+}
+
+int qft_plan_table(const qft_plan *p, void *h_out) {
+    if (!p || !h_out) return fail(QFT_EINVAL, "NULL argument");
+    if (p->N < 8) return 0;
+    if (p->prec == QFT_PREC_F64) memcpy(h_out, p->t64.data(), p->t64.size() * sizeof(double));
+    else memcpy(h_out, p->t32.data(), p->t32.size() * sizeof(float));
+    return 0;
+}
+
+int qft_plan_set_table(qft_plan *p, const void *h_table) {
+    if (!p || !h_table) return fail(QFT_EINVAL, "NULL argument");
+    if (p->N < 8) return 0;
+    std::lock_guard<std::mutex> lk(p->mu);
+    CUDA_TRY(cudaSetDevice(p->device));
+    if (p->prec == QFT_PREC_F64) {
+        const double *t = (const double *)h_table;
+        p->t64.assign(t, t + p->N / 4);
+        std::vector<double> U;
+        level_table(p->N, p->t64, U);
+        CUDA_TRY(cudaMemcpy(p->d_U, U.data(), U.size() * sizeof(double), cudaMemcpyHostToDevice));
+    } else {
+        const float *t = (const float *)h_table;
+        p->t32.assign(t, t + p->N / 4);
+        std::vector<float> U;
+        level_table(p->N, p->t32, U);
+        CUDA_TRY(cudaMemcpy(p->d_U, U.data(), U.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    return 0;
+}
+
+static int ensure_scratch(qft_plan *p, size_t bytes) {
+    if (p->scratch_bytes >= bytes) return 0;
+    if (p->d_scratch) cudaFree(p->d_scratch);
+    p->d_scratch = nullptr;
+    p->scratch_bytes = 0;
+    CUDA_TRY(cudaMalloc(&p->d_scratch, bytes));
+    p->scratch_bytes = bytes;
+    return 0;
+}
+
+template <typename T>
+static int layout_copy(const void *src, void *dst, long long batch, int N, long long sbs, long long ses,
+                       long long dbs, long long des, cudaStream_t st, int num_sms) {
+    if (sbs == N && ses == 1 && dbs == N && des == 1) {
+        CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)batch * N * sizeof(vec2<T>), cudaMemcpyDeviceToDevice, st));
+        return 0;
+    }
+    if (ses == batch && sbs == 1 && dbs == N && des == 1) {  // (N, B) -> (B, N)
+        dim3 grid((unsigned)((batch + 31) / 32), (unsigned)((N + 31) / 32));
+        qft_transpose<T><<<grid, dim3(32, 8), 0, st>>>((const vec2<T> *)src, (vec2<T> *)dst, N, batch);
+    } else if (sbs == N && ses == 1 && des == batch && dbs == 1) {  // (B, N) -> (N, B)
+        dim3 grid((unsigned)((N + 31) / 32), (unsigned)((batch + 31) / 32));
+        qft_transpose<T><<<grid, dim3(32, 8), 0, st>>>((const vec2<T> *)src, (vec2<T> *)dst, batch, N);
+    } else {
+        qft_strided_copy<T><<<num_sms * 8, 256, 0, st>>>((const vec2<T> *)src, (vec2<T> *)dst, batch, N, sbs, ses,
+                                                          dbs, des);
+    }
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+// scratch: NULL -> the plan's own (grown on demand); else >= 2*batch*N elements
+static int exec_impl(qft_plan *p, const void *d_in, void *d_out, int64_t batch, int64_t ibs, int64_t ies,
+                     int64_t obs, int64_t oes, cudaStream_t st, void *scratch = nullptr) {
+    if (batch == 0) return 0;
+    const int N = p->N;
+    const bool in_c = (ibs == N && ies == 1), out_c = (obs == N && oes == 1);
+    const size_t esz = p->prec == QFT_PREC_F32 ? 8 : 16;
+    const size_t bytes = (size_t)batch * N * esz;
+    const void *src = d_in;
+    void *dst = d_out;
+    if ((!in_c || !out_c) && !scratch) {
+        int rc = ensure_scratch(p, (in_c ? 0 : bytes) + (out_c ? 0 : bytes));
+        if (rc) return rc;
+        scratch = p->d_scratch;
+    }
+    char *scr = (char *)scratch;
+    if (!in_c) {
+        int rc = p->prec == QFT_PREC_F32
+                     ? layout_copy<float>(d_in, scr, batch, N, ibs, ies, N, 1, st, p->num_sms)
+                     : layout_copy<double>(d_in, scr, batch, N, ibs, ies, N, 1, st, p->num_sms);
+        if (rc) return rc;
+        src = scr;
+        scr += bytes;
+    }
+    if (!out_c) dst = scr;
+    int rc = launch_contig(p, src, dst, batch, st);
+    if (rc) return rc;
+    if (!out_c) {
+        rc = p->prec == QFT_PREC_F32 ? layout_copy<float>(dst, d_out, batch, N, N, 1, obs, oes, st, p->num_sms)
+                                     : layout_copy<double>(dst, d_out, batch, N, N, 1, obs, oes, st, p->num_sms);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
+int qft_exec_cdft(const qft_plan *cp, const void *d_in, void *d_out, int64_t batch, int64_t ibs, int64_t ies,
+                  int64_t obs, int64_t oes, void *stream) {
+    qft_plan *p = const_cast<qft_plan *>(cp);
+    if (!p || (!d_in && batch) || (!d_out && batch)) return fail(QFT_EINVAL, "NULL argument");
+    if (batch < 0) return fail(QFT_EINVAL, "negative batch");
+    if (d_in == d_out && batch) return fail(QFT_EINVAL, "transform is out-of-place: d_in must differ from d_out");
+    CUDA_TRY(cudaSetDevice(p->device));
+    std::lock_guard<std::mutex> lk(p->mu);
+    return exec_impl(p, d_in, d_out, batch, ibs, ies, obs, oes, (cudaStream_t)stream);
+}
+
+int qft_exec_cdft_host(qft_plan *p, const void *h_in, void *h_out, int64_t batch, int64_t ibs, int64_t ies,
+                       int64_t obs, int64_t oes) {
+    if (!p || (batch && (!h_in || !h_out))) return fail(QFT_EINVAL, "NULL argument");
+    if (batch <= 0) return batch == 0 ? 0 : fail(QFT_EINVAL, "negative batch");
+    CUDA_TRY(cudaSetDevice(p->device));
+    std::lock_guard<std::mutex> lk(p->mu);
+    const int N = p->N;
+    const size_t esz = p->prec == QFT_PREC_F32 ? 8 : 16;
+    const bool batch_major_in = (ibs == N && ies == 1), batch_major_out = (obs == N && oes == 1);
+    const bool ref_in = (ies == batch && ibs == 1), ref_out = (oes == batch && obs == 1);
+    if (!(batch_major_in || ref_in) || !(batch_major_out || ref_out))
+        return fail(QFT_EINVAL, "host path supports batch-major or (N, batch) layouts only");
+    for (auto &s : p->streams)
+        if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    // chunk the batch so copies of one chunk overlap the transform of the other
+    const size_t target = (size_t)64 << 20;  // bytes per chunk
+    long long chunk = (long long)(target / ((size_t)N * esz));
+    if (chunk < 1) chunk = 1;
+    if (chunk > batch) chunk = batch;
+    const size_t cbytes = (size_t)chunk * N * esz;
+    // per stream: in buffer, out buffer, (transpose scratch is inside exec_impl's scratch -> use own)
+    void *bufs = nullptr;
+    CUDA_TRY(cudaMalloc(&bufs, cbytes * 8));  // per stream: in, out, 2x layout scratch
+    int rc = 0;
+    for (long long b0 = 0, it = 0; b0 < batch && !rc; b0 += chunk, ++it) {
+        const long long nb = (batch - b0) < chunk ? (batch - b0) : chunk;
+        cudaStream_t st = p->streams[it & 1];
+        char *din = (char *)bufs + (it & 1) * 4 * cbytes, *dout = din + cbytes, *dscr = din + 2 * cbytes;
+        cudaError_t e;
+        if (batch_major_in)
+            e = cudaMemcpyAsync(din, (const char *)h_in + (size_t)b0 * N * esz, (size_t)nb * N * esz,
+                                cudaMemcpyHostToDevice, st);
+        else  // columns [b0, b0+nb) of the (N, batch) array -> (N, nb) pitched
+            e = cudaMemcpy2DAsync(din, (size_t)nb * esz, (const char *)h_in + (size_t)b0 * esz, (size_t)batch * esz,
+                                  (size_t)nb * esz, (size_t)N, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) {
+            rc = fail(QFT_ECUDA, std::string("H2D: ") + cudaGetErrorString(e));
+            break;
+        }
+        // device layout of the chunk: batch-major (nb, N) or (N, nb)
+        rc = exec_impl(p, din, dout, nb, batch_major_in ? N : 1, batch_major_in ? 1 : nb, batch_major_out ? N : 1,
+                       batch_major_out ? 1 : nb, st, dscr);
+        if (rc) break;
+        if (batch_major_out)
+            e = cudaMemcpyAsync((char *)h_out + (size_t)b0 * N * esz, dout, (size_t)nb * N * esz,
+                                cudaMemcpyDeviceToHost, st);
+        else
+            e = cudaMemcpy2DAsync((char *)h_out + (size_t)b0 * esz, (size_t)batch * esz, dout, (size_t)nb * esz,
+                                  (size_t)nb * esz, (size_t)N, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) rc = fail(QFT_ECUDA, std::string("D2H: ") + cudaGetErrorString(e));
+    }
+    for (auto &s : p->streams) {
+        cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess && !rc) rc = fail(QFT_ECUDA, std::string("sync: ") + cudaGetErrorString(e));
+    }
+    cudaFree(bufs);
+    return rc;
+}
+
+int qft_fill_normal(const qft_plan *p, void *d_out, int64_t batch, int64_t first_index, uint64_t seed, void *stream) {
+    if (!p || (!d_out && batch)) return fail(QFT_EINVAL, "NULL argument");
+    if (batch <= 0) return 0;
+    CUDA_TRY(cudaSetDevice(p->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (p->prec == QFT_PREC_F32)
+        qft_fill_normal_kernel<float><<<p->num_sms * 16, 256, 0, st>>>((vec2<float> *)d_out, batch, p->N, first_index,
+                                                                        seed);
+    else
+        qft_fill_normal_kernel<double><<<p->num_sms * 16, 256, 0, st>>>((vec2<double> *)d_out, batch, p->N,
+                                                                         first_index, seed);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+

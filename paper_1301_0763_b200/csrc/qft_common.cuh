@@ -1,0 +1,113 @@
+// qft_common.cuh -- arithmetic contract and small helpers shared by every
+// improved-QFT kernel.
+//
+// The arithmetic contract is the reference's counted primitives
+// (/root/reference/pkg/src/quickfourier/counting.py:40-81): every value is one
+// IEEE round-to-nearest add, sub or mul of two operands.  On the device we use
+// the explicit __fadd_rn/__fmul_rn/__dadd_rn/__dmul_rn intrinsics, which the
+// compiler never contracts into FMA (the build also passes -fmad=false).
+// Functions are __host__ __device__ so the test-only host emulator
+// (tests/emu/) can execute the exact same index logic on the CPU.
+#pragma once
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define QFT_HD __host__ __device__ __forceinline__
+#define QFT_DEV __device__ __forceinline__
+#else
+#define QFT_HD inline
+#define QFT_DEV inline
+#endif
+
+namespace qft {
+
+// One complex sample, or -- inside the real-factor recursion -- the pair
+// (value of the Re-part signal, value of the Im-part signal).  Both halves
+// follow the identical operation DAG (shared.py:56-57), so the kernels run
+// them as one 2-vector stream.
+template <typename T>
+struct alignas(2 * sizeof(T)) vec2 {
+    T x, y;
+};
+
+QFT_HD float radd(float a, float b) {
+#if defined(__CUDA_ARCH__)
+    return __fadd_rn(a, b);
+#else
+    return a + b;
+#endif
+}
+QFT_HD float rsub(float a, float b) {
+#if defined(__CUDA_ARCH__)
+    return __fsub_rn(a, b);
+#else
+    return a - b;
+#endif
+}
+QFT_HD float rmul(float a, float b) {
+#if defined(__CUDA_ARCH__)
+    return __fmul_rn(a, b);
+#else
+    return a * b;
+#endif
+}
+QFT_HD double radd(double a, double b) {
+#if defined(__CUDA_ARCH__)
+    return __dadd_rn(a, b);
+#else
+    return a + b;
+#endif
+}
+QFT_HD double rsub(double a, double b) {
+#if defined(__CUDA_ARCH__)
+    return __dsub_rn(a, b);
+#else
+    return a - b;
+#endif
+}
+QFT_HD double rmul(double a, double b) {
+#if defined(__CUDA_ARCH__)
+    return __dmul_rn(a, b);
+#else
+    return a * b;
+#endif
+}
+
+template <typename T>
+QFT_HD vec2<T> vadd(vec2<T> a, vec2<T> b) { return {radd(a.x, b.x), radd(a.y, b.y)}; }
+template <typename T>
+QFT_HD vec2<T> vsub(vec2<T> a, vec2<T> b) { return {rsub(a.x, b.x), rsub(a.y, b.y)}; }
+template <typename T>
+QFT_HD vec2<T> vmul(vec2<T> a, T c) { return {rmul(a.x, c), rmul(a.y, c)}; }
+template <typename T>
+QFT_HD vec2<T> vsel(bool p, vec2<T> a, vec2<T> b) { return p ? a : b; }
+
+QFT_HD int ctz32(uint32_t v) {
+#if defined(__CUDA_ARCH__)
+    return __ffs((int)v) - 1;
+#else
+    return __builtin_ctz(v);
+#endif
+}
+
+// Position of element `t` of input slot `s` of an r-level reflection group
+// of a Lee block of size L is c + sg*t.  Restates the fold pairing of
+// elaborations.py:364-377 (element i with L-1-i) applied r times; every slot
+// is a contiguous (possibly reversed) run, and the runs tile the block.
+QFT_HD void run_of(int r, int L, int s, int &c, int &sg) {
+    int A = 0, B = 1;
+    while (r > 0) {
+        int H = 1 << (r - 1);
+        if (s >= H) {
+            s = (1 << r) - 1 - s;
+            A += B * (L - 1);
+            B = -B;
+        }
+        L >>= 1;
+        --r;
+    }
+    c = A;
+    sg = B;
+}
+
+}  // namespace qft

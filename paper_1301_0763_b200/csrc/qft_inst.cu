@@ -1,0 +1,26 @@
+// qft_inst.cu -- one (precision, N) instance of the transform kernels.
+// Compiled once per instance with -DQFT_INST_PREC={32,64} -DQFT_INST_LOG2N={1..12}.
+#include "qft_launch.cuh"
+
+#if !defined(QFT_INST_PREC) || !defined(QFT_INST_LOG2N)
+#error "compile with -DQFT_INST_PREC=<32|64> -DQFT_INST_LOG2N=<1..12>"
+#endif
+
+#define QFT_CAT3(a, b, c) a##_##b##_##c
+#define QFT_NAME(P, L) QFT_CAT3(qft_inst_launch, P, L)
+
+namespace {
+#if QFT_INST_PREC == 32
+using Real = float;
+#else
+using Real = double;
+#endif
+}  // namespace
+
+int QFT_NAME(QFT_INST_PREC, QFT_INST_LOG2N)(const qft::LaunchArgs *a) {
+#if QFT_INST_LOG2N <= 5
+    return (int)qft::launch_reg<(1 << QFT_INST_LOG2N), Real>(*a);
+#else
+    return (int)qft::launch_smem<QFT_INST_LOG2N, Real>(*a);
+#endif
+}

@@ -1,0 +1,115 @@
+// tests/emu/kernel_emu.cpp -- TEST-ONLY host emulation of the device phase
+// functions in paper_1301_0763_b200/csrc/qft_smem.cuh.
+//
+// It runs the exact index/arithmetic code of the shared-memory kernel on the
+// CPU (one "thread" at a time, the B-phase split into load / __syncwarp /
+// store exactly like the kernel) so that the layout logic can be checked
+// bit-for-bit against the oracle without a GPU.  It is never used by the
+// product path, which fails loudly without its CUDA extension.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../paper_1301_0763_b200/csrc/qft_smem.cuh"
+
+using namespace qft;
+
+template <typename T>
+static void build_U(int N, const T *Tnat, std::vector<T> &U) {
+    // Tnat = natural table T[m] = halfsec(m/N), T[0] = cos8; U[S/2+i] = T[(2i+1) N/(4S)]
+    U.assign(N / 4 > 1 ? N / 4 : 2, (T)0);
+    U[0] = Tnat[0];
+    for (int S = 2; S <= N / 4; S *= 2)
+        for (int i = 0; i < S / 2; ++i) U[S / 2 + i] = Tnat[(2 * i + 1) * (N / (4 * S))];
+}
+
+template <int LOG2N, typename T, int J>
+static void emu_f(vec2<T> *w, const T *U) {
+    using P = SPlan<LOG2N>;
+    if constexpr (J < P::JF) {
+        for (int t = 0; t < 32; ++t) f_unit<LOG2N, J, false, T>(w, U, t);
+        for (int t = 0; t < 32; ++t) f_unit<LOG2N, J, true, T>(w, U, t);
+        emu_f<LOG2N, T, J + 1>(w, U);
+    }
+}
+
+template <int LOG2N, typename T, int J, bool DST>
+static void emu_c_side(vec2<T> *w) {
+    std::vector<BUnit<LOG2N, J, DST, T>> lanes(32);
+    for (int i = 0; i < 32; ++i) lanes[i].load(w, i);
+    for (int i = 0; i < 32; ++i) lanes[i].store(w, i);
+}
+
+template <int LOG2N, typename T, int J>
+static void emu_c(vec2<T> *w) {
+    using P = SPlan<LOG2N>;
+    if constexpr (J < P::JF) {
+        emu_c_side<LOG2N, T, J, false>(w);
+        emu_c_side<LOG2N, T, J, true>(w);
+        emu_c<LOG2N, T, J + 1>(w);
+    }
+}
+
+template <int LOG2N, typename T>
+static void emu_one(const vec2<T> *x, vec2<T> *y, const T *U) {
+    using P = SPlan<LOG2N>;
+    std::vector<vec2<T>> W(P::W_PADDED);
+    vec2<T> *w = W.data();
+    for (int n = 0; n <= P::m; ++n) a0_item<LOG2N, T>(x, w, n);
+    emu_f<LOG2N, T, 0>(w, U);
+    for (int u = 0; u < P::NB_UNITS; ++u) b_unit<LOG2N, T>(w, U, u);
+    emu_c<LOG2N, T, 0>(w);
+    for (int t = 0; t <= P::MRC; ++t) Chain<LOG2N, T>::unit(w, y, t);
+}
+
+template <int NN, typename T>
+static void emu_reg(const vec2<T> *x, vec2<T> *y, const T *U) {
+    cdft_reg<NN, T>(x, y, U);
+}
+
+template <typename T>
+static int emu_dispatch(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
+    switch (log2n) {
+        case 1: emu_reg<2, T>(x, y, U); return 0;
+        case 2: emu_reg<4, T>(x, y, U); return 0;
+        case 3: emu_reg<8, T>(x, y, U); return 0;
+        case 4: emu_reg<16, T>(x, y, U); return 0;
+        case 5: emu_reg<32, T>(x, y, U); return 0;
+        case 6: emu_one<6, T>(x, y, U); return 0;
+        case 7: emu_one<7, T>(x, y, U); return 0;
+        case 8: emu_one<8, T>(x, y, U); return 0;
+        case 9: emu_one<9, T>(x, y, U); return 0;
+        case 10: emu_one<10, T>(x, y, U); return 0;
+        case 11: emu_one<11, T>(x, y, U); return 0;
+        case 12: emu_one<12, T>(x, y, U); return 0;
+        default: return -1;
+    }
+}
+
+extern "C" {
+// x, y: batch-major interleaved complex; Tnat: natural table for N (N >= 8)
+int emu_cdft_f64(int log2n, const double *x, double *y, long batch, const double *Tnat) {
+    const int N = 1 << log2n;
+    std::vector<double> U;
+    double dummy[2] = {0, 0};
+    if (N >= 8) build_U(N, Tnat, U); else U.assign(dummy, dummy + 2);
+    for (long b = 0; b < batch; ++b) {
+        int rc = emu_dispatch<double>(log2n, (const vec2<double> *)(x + 2L * N * b),
+                                      (vec2<double> *)(y + 2L * N * b), U.data());
+        if (rc) return rc;
+    }
+    return 0;
+}
+int emu_cdft_f32(int log2n, const float *x, float *y, long batch, const float *Tnat) {
+    const int N = 1 << log2n;
+    std::vector<float> U;
+    float dummy[2] = {0, 0};
+    if (N >= 8) build_U(N, Tnat, U); else U.assign(dummy, dummy + 2);
+    for (long b = 0; b < batch; ++b) {
+        int rc = emu_dispatch<float>(log2n, (const vec2<float> *)(x + 2L * N * b),
+                                     (vec2<float> *)(y + 2L * N * b), U.data());
+        if (rc) return rc;
+    }
+    return 0;
+}
+}

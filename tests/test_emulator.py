@@ -1,0 +1,46 @@
+"""Host emulation of the device phase functions (tests/emu/, test-only) must be
+bit-identical to the oracle: validates the kernel's layout/index logic on CPU."""
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, bit_equal
+
+EMU_DIR = os.path.join(ROOT, "tests", "emu")
+EMU_LIB = os.path.join(EMU_DIR, "libkernel_emu.so")
+
+
+@pytest.fixture(scope="module")
+def emu():
+    src = os.path.join(EMU_DIR, "kernel_emu.cpp")
+    hdrs = [os.path.join(ROOT, "paper_1301_0763_b200", "csrc", f) for f in
+            ("qft_common.cuh", "qft_lee.cuh", "qft_smem.cuh")]
+    newest = max(os.path.getmtime(p) for p in [src] + hdrs)
+    if not os.path.exists(EMU_LIB) or os.path.getmtime(EMU_LIB) < newest:
+        cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+        subprocess.check_call([cxx, "-O1", "-std=c++17", "-fPIC", "-shared", "-ffp-contract=off",
+                               "-o", EMU_LIB, src])
+    lib = ctypes.CDLL(EMU_LIB)
+    for name in ("emu_cdft_f64", "emu_cdft_f32"):
+        getattr(lib, name).argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_long,
+                                       ctypes.c_void_p]
+    return lib
+
+
+@pytest.mark.parametrize("dt", [np.complex128, np.complex64])
+@pytest.mark.parametrize("lg", list(range(1, 13)))
+def test_emulated_kernel_bitwise(emu, oracle_mod, dt, lg):
+    N = 1 << lg
+    rt = np.float32 if dt == np.complex64 else np.float64
+    rng = np.random.default_rng(100 + lg)
+    B = 2
+    z = (rng.standard_normal((B, N)) + 1j * rng.standard_normal((B, N))).astype(dt)
+    y = np.empty_like(z)
+    T = oracle_mod.table(N, rt) if N >= 8 else np.zeros(2, rt)
+    fn = emu.emu_cdft_f32 if dt == np.complex64 else emu.emu_cdft_f64
+    assert fn(lg, z.ctypes.data, y.ctypes.data, B, T.ctypes.data) == 0
+    assert bit_equal(y, oracle_mod.cdft_rows(z))

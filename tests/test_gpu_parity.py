@@ -1,0 +1,213 @@
+"""Parity of the sm_100a kernels with the oracle (bit-identical), through the
+C ABI and the drop-in API.  Run on a B200 with -m gpu."""
+
+import numpy as np
+import pytest
+
+from conftest import bit_equal, config1_input, golden_input, sha
+
+pytestmark = pytest.mark.gpu
+
+ALL_LG = list(range(1, 13))
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+def _rows(torch, z):
+    from paper_1301_0763_b200 import improved
+    return improved.cdft_rows(torch.from_numpy(np.ascontiguousarray(z)).cuda()).cpu().numpy()
+
+
+@pytest.mark.parametrize("dt", [np.complex64, np.complex128])
+@pytest.mark.parametrize("lg", ALL_LG)
+def test_rows_bitwise_vs_oracle(torch_cuda, oracle_mod, dt, lg):
+    N = 1 << lg
+    B = 37 if lg <= 10 else 9
+    rng = np.random.default_rng(10 * lg + (dt == np.complex64))
+    z = (rng.standard_normal((B, N)) + 1j * rng.standard_normal((B, N))).astype(dt)
+    assert bit_equal(_rows(torch_cuda, z), oracle_mod.cdft_rows(z))
+
+
+@pytest.mark.parametrize("tag,dt", [("c128", np.complex128), ("c64", np.complex64)])
+def test_golden_raw(golden, torch_cuda, tag, dt):
+    from paper_1301_0763_b200 import improved
+    arrays, _ = golden
+    for lg in range(1, 11):
+        N = 1 << lg
+        got = improved.cdft(arrays[f"in_{tag}_{N}"])
+        assert bit_equal(got, arrays[f"improved_{tag}_{N}"]), N
+
+
+@pytest.mark.parametrize("tag,dt", [("c128", np.complex128), ("c64", np.complex64)])
+def test_golden_digests(golden, torch_cuda, tag, dt):
+    from paper_1301_0763_b200 import improved
+    _, meta = golden
+    for lg in (11, 12):
+        N = 1 << lg
+        e = meta["cdft_sha256"][f"improved_{tag}_{N}"]
+        z = golden_input(N, e["batch"], dt, e["seed"])
+        assert sha(improved.cdft(z)) == e["sha256"], N
+
+
+def test_known_answer_vectors(golden, torch_cuda):
+    from paper_1301_0763_b200 import improved
+    arrays, _ = golden
+    z8 = arrays["kat_cdft8_in"]
+    got = improved.cdft(z8)
+    assert bit_equal(got, arrays["kat_cdft8_improved"])
+    np.testing.assert_allclose(got, arrays["kat_cdft8_frozen"], rtol=0, atol=1e-13)
+    assert bit_equal(improved.cdft(z8.astype(np.complex64)), arrays["kat_cdft8_improved_c64"])
+    assert bit_equal(improved.cdft(np.array([1, 1j, -1, -1j])), arrays["kat_rot4_improved"])
+    imp = np.zeros(16, dtype=np.complex128)
+    imp[0] = 1
+    assert bit_equal(improved.cdft(imp), arrays["kat_impulse16_improved"])
+
+
+def test_config1_full_batch(golden, torch_cuda):
+    """BASELINE config 1: c128, N=2^10, batch 64, U[-1,1) seed 0 -- bit-identical."""
+    from paper_1301_0763_b200 import improved
+    _, meta = golden
+    z = config1_input()
+    assert sha(z) == meta["config1"]["input_sha256"]
+    assert sha(improved.cdft(z)) == meta["config1"]["improved_sha256"]
+
+
+def test_plan_table_bit_parity(golden, torch_cuda):
+    from paper_1301_0763_b200 import _native
+    arrays, meta = golden
+    for prec, tag in ((64, "f64"), (32, "f32")):
+        for lg in range(3, 13):
+            T = _native.plan(lg, prec).table()
+            assert T.tobytes() == arrays[f"table_{tag}_{1 << lg}"].tobytes()
+            assert sha(T) == meta["table_sha256"][f"{tag}_{1 << lg}"]
+
+
+@pytest.mark.parametrize("shape", [(64,), (64, 1), (64, 5), (128, 2, 3), (16, 4, 1, 2)])
+def test_reference_layouts(torch_cuda, oracle_mod, shape):
+    from paper_1301_0763_b200 import improved
+    rng = np.random.default_rng(len(shape))
+    z = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    got = improved.cdft(z)
+    assert got.shape == z.shape and got.dtype == np.complex128
+    assert bit_equal(got, oracle_mod.cdft(z))
+    # non-contiguous input views
+    zt = np.asfortranarray(z)
+    assert bit_equal(improved.cdft(zt), oracle_mod.cdft(z))
+
+
+def test_dtype_rules(torch_cuda, oracle_mod):
+    from paper_1301_0763_b200 import improved
+    x = np.random.default_rng(1).standard_normal(32).astype(np.float32)
+    out = improved.cdft(x)  # real float32 -> complex128 path (improved.py:142-143)
+    assert out.dtype == np.complex128
+    assert bit_equal(out, oracle_mod.cdft(x.astype(np.complex128)))
+    z = x.astype(np.complex64)
+    assert improved.cdft(z).dtype == np.complex64
+    assert improved.cdft(list(x)).dtype == np.complex128
+
+
+def test_input_not_mutated(torch_cuda):
+    from paper_1301_0763_b200 import improved
+    z = golden_input(256, 4, np.complex64, 5)
+    keep = z.copy()
+    improved.cdft(z)
+    assert bit_equal(z, keep)
+
+
+def test_counter_and_table(torch_cuda, oracle_mod):
+    from paper_1301_0763_b200 import improved
+    from paper_1301_0763_b200.counting import OpCounter, TrigTable, build_trig_table
+    z = golden_input(64, 7, np.complex128, 9)
+    c = OpCounter()
+    improved.cdft(z, counter=c)
+    assert (c.adds, c.muls) == (6748, 1372)  # N=64 x 7
+    t = build_trig_table("improved", 64, np.float64)
+    improved.cdft(z, table=t, counter=OpCounter())
+    assert t.touched_count() == 16
+    with pytest.raises(ValueError, match="does not match"):
+        improved.cdft(z, table=TrigTable(dtype=np.float32))
+    # a single-tier table changes the constants the kernel uses
+    st = TrigTable(dtype=np.float64, pipeline="single_tier")
+    got = improved.cdft(golden_input(4096, 2, np.complex128, 3), table=st)
+    from paper_1301_0763_b200.counting import natural_constants
+    want = oracle_mod.cdft(golden_input(4096, 2, np.complex128, 3),
+                           T=natural_constants(TrigTable(np.float64, "single_tier"), 4096))
+    assert bit_equal(got, want)
+    # and the default table is restored afterwards
+    z2 = golden_input(4096, 2, np.complex128, 4)
+    assert bit_equal(improved.cdft(z2), oracle_mod.cdft(z2))
+
+
+def test_reference_table_objects_accepted(torch_cuda, oracle_mod):
+    """A TrigTable from the reference package (duck-typed) drives the kernel."""
+    import sys
+    import os
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference not present on this host")
+    sys.path.insert(0, ref)
+    from quickfourier.counting import build_trig_table as ref_build
+    from paper_1301_0763_b200 import improved
+    t = ref_build("improved", 256, np.float64)
+    z = golden_input(256, 3, np.complex128, 2)
+    assert bit_equal(improved.cdft(z, table=t), oracle_mod.cdft(z))
+    assert t.touched_count() == 64
+
+
+def test_torch_device_path_reference_layout(torch_cuda, oracle_mod):
+    from paper_1301_0763_b200 import improved
+    torch = torch_cuda
+    z = golden_input(512, 6, np.complex64, 11)
+    t = torch.from_numpy(z).cuda()
+    out = improved.cdft(t)
+    assert out.is_cuda and out.shape == t.shape
+    assert bit_equal(out.cpu().numpy(), oracle_mod.cdft(z))
+
+
+def test_batched_equals_single_and_empty(torch_cuda, oracle_mod):
+    from paper_1301_0763_b200 import improved
+    torch = torch_cuda
+    z = golden_input(4096, 1, np.complex64, 12)[:, 0]
+    one = improved.cdft(z)
+    zz = np.stack([z] * 300)
+    many = improved.cdft_rows(torch.from_numpy(zz).cuda()).cpu().numpy()
+    assert all(bit_equal(many[i], one) for i in (0, 150, 299))
+    empty = improved.cdft_rows(torch.empty((0, 64), dtype=torch.complex64, device="cuda"))
+    assert empty.shape == (0, 64)
+
+
+def test_special_values(torch_cuda, oracle_mod):
+    """zeros (signed-zero bookkeeping), huge, tiny/denormal inputs: still bit-identical."""
+    for dt in (np.complex64, np.complex128):
+        N = 1024
+        cases = [np.zeros((2, N)), -np.zeros((2, N)), np.full((2, N), 1e30), np.full((2, N), 1e-39)]
+        rng = np.random.default_rng(0)
+        m = rng.standard_normal((2, N))
+        m[:, ::3] = 0.0
+        cases.append(m)
+        for c in cases:
+            z = (c + 1j * c[::-1]).astype(dt)
+            assert bit_equal(_rows(torch_cuda, z), oracle_mod.cdft_rows(z))
+
+
+def test_large_batch_properties(torch_cuda):
+    """Config-2 sized batch: linearity and Parseval (size-independent checks)."""
+    torch = torch_cuda
+    from paper_1301_0763_b200 import improved
+    N, B = 4096, 16384
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn((B, N), dtype=torch.complex64, device="cuda", generator=g)
+    y = improved.cdft_rows(x)
+    # Parseval: sum |X|^2 = N sum |x|^2 per row
+    ex = (x.abs() ** 2).double().sum(1) * N
+    ey = (y.abs() ** 2).double().sum(1)
+    assert torch.allclose(ey, ex, rtol=1e-4)
+    # agreement with torch.fft (fp32 accuracy of the reference algorithm)
+    ref = torch.fft.fft(x.to(torch.complex128), dim=1)
+    rel = ((y.to(torch.complex128) - ref).abs().pow(2).sum(1).sqrt() / ref.abs().pow(2).sum(1).sqrt()).max()
+    assert rel.item() < 1e-6 * 12
