@@ -48,7 +48,8 @@ typedef struct {
     int32_t kernel_launches; /* kernel launches per qft_exec_cdft call          */
     int32_t smem_bytes;      /* dynamic shared memory per CTA of the main kernel */
     int32_t threads_per_cta;
-    int32_t ctas_per_sm;     /* occupancy of the main kernel                     */
+    int32_t ctas_per_sm;     /* resident CTAs per SM of the main kernel          */
+    int32_t signals_per_cta; /* signals a CTA transforms per iteration           */
     int64_t scratch_bytes;   /* device scratch owned by the plan                 */
 } qft_plan_info_t;
 

@@ -32,6 +32,7 @@ class PlanInfo(ctypes.Structure):
         ("smem_bytes", ctypes.c_int32),
         ("threads_per_cta", ctypes.c_int32),
         ("ctas_per_sm", ctypes.c_int32),
+        ("signals_per_cta", ctypes.c_int32),
         ("scratch_bytes", ctypes.c_int64),
     ]
 

@@ -86,8 +86,9 @@ def ptxas_report():
     """(kernel, registers, spill bytes) from the cached build logs."""
     import re
     rows = []
+    dig = _headers_digest()
     for f in sorted(os.listdir(BUILD)):
-        if not f.endswith(".log"):
+        if not f.endswith(f"_{dig}.o.log"):
             continue
         fn = None
         for line in open(os.path.join(BUILD, f)):

@@ -133,7 +133,7 @@ struct qft_plan {
 };
 
 // per-instance launchers, one translation unit each (qft_inst.cu)
-#define QFT_DECL(P, L) int qft_inst_launch_##P##_##L(const LaunchArgs *);
+#define QFT_DECL(P, L) int qft_inst_launch_##P##_##L(const LaunchArgs *); void qft_inst_cfg_##P##_##L(int *);
 #define QFT_DECL_ALL(P) \
     QFT_DECL(P, 1) QFT_DECL(P, 2) QFT_DECL(P, 3) QFT_DECL(P, 4) QFT_DECL(P, 5) QFT_DECL(P, 6) QFT_DECL(P, 7) \
     QFT_DECL(P, 8) QFT_DECL(P, 9) QFT_DECL(P, 10) QFT_DECL(P, 11) QFT_DECL(P, 12)
@@ -145,6 +145,12 @@ typedef int (*launch_fn)(const LaunchArgs *);
      qft_inst_launch_##P##_5, qft_inst_launch_##P##_6, qft_inst_launch_##P##_7, qft_inst_launch_##P##_8,         \
      qft_inst_launch_##P##_9, qft_inst_launch_##P##_10, qft_inst_launch_##P##_11, qft_inst_launch_##P##_12}
 static const launch_fn kLaunch[2][13] = {QFT_ROW(32), QFT_ROW(64)};
+typedef void (*cfg_fn)(int *);
+#define QFT_CROW(P)                                                                                   \
+    {nullptr, qft_inst_cfg_##P##_1, qft_inst_cfg_##P##_2, qft_inst_cfg_##P##_3, qft_inst_cfg_##P##_4,   \
+     qft_inst_cfg_##P##_5, qft_inst_cfg_##P##_6, qft_inst_cfg_##P##_7, qft_inst_cfg_##P##_8,             \
+     qft_inst_cfg_##P##_9, qft_inst_cfg_##P##_10, qft_inst_cfg_##P##_11, qft_inst_cfg_##P##_12}
+static const cfg_fn kCfg[2][13] = {QFT_CROW(32), QFT_CROW(64)};
 static constexpr int kMaxLog2N = 12;
 
 static int launch_contig(const qft_plan *p, const void *in, void *out, long long batch, cudaStream_t st) {
@@ -228,9 +234,12 @@ int qft_plan_get_info(const qft_plan *p, qft_plan_info_t *info) {
     info->algo = p->algo;
     info->passes = 1;
     info->kernel_launches = 1;
-    info->smem_bytes = smem_bytes_for(p->log2n, p->prec);
-    info->threads_per_cta = p->log2n >= 6 ? kSmemWarps * 32 : 128;
-    info->ctas_per_sm = 0;
+    int cfg[3] = {0, 0, 0};
+    if (p->log2n >= 1 && p->log2n <= kMaxLog2N) kCfg[p->prec == QFT_PREC_F32 ? 0 : 1][p->log2n](cfg);
+    info->smem_bytes = cfg[0];
+    info->threads_per_cta = cfg[1];
+    info->ctas_per_sm = p->log2n >= 6 ? 1 : 0;
+    info->signals_per_cta = cfg[2];
     info->scratch_bytes = (int64_t)p->scratch_bytes;
     return 0;
 }

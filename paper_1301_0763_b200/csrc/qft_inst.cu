@@ -17,6 +17,22 @@ using Real = double;
 #endif
 }  // namespace
 
+#define QFT_CFGNAME(P, L) QFT_CAT3(qft_inst_cfg, P, L)
+
+// cfg[0] dynamic smem bytes, cfg[1] threads per CTA, cfg[2] signals per CTA iteration
+void QFT_CFGNAME(QFT_INST_PREC, QFT_INST_LOG2N)(int *cfg) {
+#if QFT_INST_LOG2N <= 5
+    cfg[0] = 0;
+    cfg[1] = 128;
+    cfg[2] = 1;
+#else
+    using K = qft::KCfg<QFT_INST_LOG2N, Real>;
+    cfg[0] = K::SMEM;
+    cfg[1] = K::NT;
+    cfg[2] = K::TT;
+#endif
+}
+
 int QFT_NAME(QFT_INST_PREC, QFT_INST_LOG2N)(const qft::LaunchArgs *a) {
 #if QFT_INST_LOG2N <= 5
     return (int)qft::launch_reg<(1 << QFT_INST_LOG2N), Real>(*a);

@@ -1,7 +1,9 @@
 // qft_launch.cuh -- the batched transform kernels and their launchers.
 //   qft_cdft_reg   N <= 32     : one thread per signal, whole transform in registers
-//   qft_cdft_smem  N = 64..4096: one signal per CTA iteration, persistent grid,
-//                                shared-memory working set, phases of qft_smem.cuh
+//   qft_cdft_smem  N = 64..4096: persistent CTAs (1 per SM); each CTA transforms
+//                                TT signals per iteration through the phases of
+//                                qft_smem.cuh while a TMA bulk copy prefetches the
+//                                next TT signals into a staging buffer
 // Each (precision, N) instance is compiled in its own translation unit
 // (qft_inst.cu) so the build parallelises.
 #pragma once
@@ -20,6 +22,60 @@ struct LaunchArgs {
     cudaStream_t stream;
 };
 
+// ------------------------------------------------------------ TMA / mbarrier
+QFT_DEV uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+QFT_DEV void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+QFT_DEV void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// one thread: order earlier generic-proxy accesses of the buffer, arm the
+// barrier with the byte count and issue the bulk copy global -> shared
+QFT_DEV void tma_bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// ------------------------------------------------------------ configuration
+template <int LOG2N, typename T>
+struct KCfg {
+    using P = SPlan<LOG2N>;
+    static constexpr int VB = (int)sizeof(vec2<T>);
+    static constexpr int PER = P::N * VB + P::PADDED * VB;  // staging + working per signal
+    static constexpr int UB = P::UCELLS * (int)sizeof(T);
+    static constexpr int BUDGET = 200 * 1024 - UB - 64;
+    static constexpr int TT0 = BUDGET / PER;
+    static constexpr int TT = TT0 < 1 ? 1 : (TT0 > 64 ? 64 : TT0);  // signals per CTA iteration
+    static constexpr int rup32(int x) { return (x + 31) / 32 * 32; }
+    static constexpr int NB32 = rup32(TT * P::NL32);                 // phase-B Lee-32 lanes per side
+    static constexpr int W_B = (2 * NB32 + rup32(2 * TT)) / 32;
+    static constexpr int W_D = (TT * P::MRC + 31) / 32;
+    static constexpr int W_AC = TT * P::NWU;
+    static constexpr int mx(int a, int b) { return a > b ? a : b; }
+    static constexpr int NW0 = mx(mx(W_B, W_D), W_AC);
+    static constexpr int NWMAX = sizeof(T) == 8 ? 12 : 16;  // keep >= 168 registers for fp64
+    static constexpr int NW = NW0 < 4 ? 4 : (NW0 > NWMAX ? NWMAX : NW0);
+    static constexpr int NT = NW * 32;
+    static constexpr int STAGE_OFF = 0;
+    static constexpr int W_OFF = TT * P::N * VB;
+    static constexpr int U_OFF = W_OFF + TT * P::PADDED * VB;
+    static constexpr int BAR_OFF = (U_OFF + UB + 15) / 16 * 16;
+    static constexpr int SMEM = BAR_OFF + 16;
+};
+
+// ------------------------------------------------------------ small N
 template <int NN, typename T>
 __global__ void __launch_bounds__(128) qft_cdft_reg(const vec2<T> *__restrict__ in, vec2<T> *__restrict__ out,
                                                     long long batch, const T *__restrict__ U) {
@@ -37,102 +93,198 @@ __global__ void __launch_bounds__(128) qft_cdft_reg(const vec2<T> *__restrict__ 
     }
 }
 
+// ------------------------------------------------------------ phase drivers
 template <int LOG2N, typename T, int J>
-__device__ __forceinline__ void run_phase_a(vec2<T> *w, const T *U, int unit, int lane) {
+QFT_DEV void run_f_blocks(vec2<T> *w, const T *U, bool dst, int lane) {
+    // blocks J, J+1, ... < JF of one side, sequentially (combined warp unit)
     if constexpr (J < SPlan<LOG2N>::JF) {
-        if (unit == 2 * J) f_unit<LOG2N, J, false, T>(w, U, lane);
-        else if (unit == 2 * J + 1) f_unit<LOG2N, J, true, T>(w, U, lane);
-        else run_phase_a<LOG2N, T, J + 1>(w, U, unit, lane);
+        if (dst) {
+            FBlock<LOG2N, J, true, T> f;
+            f.load(w, U, lane);
+            __syncwarp();
+            f.store(w, lane);
+        } else {
+            FBlock<LOG2N, J, false, T> f;
+            f.load(w, U, lane);
+            __syncwarp();
+            f.store(w, lane);
+        }
+        __syncwarp();
+        run_f_blocks<LOG2N, T, J + 1>(w, U, dst, lane);
     }
+}
+
+template <typename T>
+QFT_DEV vec2<T> shfl_vec(vec2<T> v, bool down) {
+    vec2<T> r;
+    if (down) {
+        r.x = __shfl_down_sync(0xffffffffu, v.x, 1);
+        r.y = __shfl_down_sync(0xffffffffu, v.y, 1);
+    } else {
+        r.x = __shfl_up_sync(0xffffffffu, v.x, 1);
+        r.y = __shfl_up_sync(0xffffffffu, v.y, 1);
+    }
+    return r;
 }
 
 template <int LOG2N, typename T, int J, bool DST>
-__device__ __forceinline__ void run_c_side(vec2<T> *w, int lane) {
-    BUnit<LOG2N, J, DST, T> b;
-    b.load(w, lane);
+QFT_DEV void run_c_block(vec2<T> *w, int lane) {
+    CBlock<LOG2N, J, DST, T> c;
+    c.load(w, lane);
+    constexpr int G = CBlock<LOG2N, J, DST, T>::G;
+    vec2<T> out[G];
+    auto halo = [&](int p) { return shfl_vec(c.own[p], !DST); };
+    c.compute(lane, halo, out);
     __syncwarp();
-    b.store(w, lane);
+    c.store(w, lane, out);
+    __syncwarp();
 }
 
 template <int LOG2N, typename T, int J>
-__device__ __forceinline__ void run_phase_c(vec2<T> *w, int unit, int lane) {
+QFT_DEV void run_c_blocks(vec2<T> *w, bool dst, int lane) {
     if constexpr (J < SPlan<LOG2N>::JF) {
-        if (unit == 2 * J) run_c_side<LOG2N, T, J, false>(w, lane);
-        else if (unit == 2 * J + 1) run_c_side<LOG2N, T, J, true>(w, lane);
-        else run_phase_c<LOG2N, T, J + 1>(w, unit, lane);
+        if (dst) run_c_block<LOG2N, T, J, true>(w, lane);
+        else run_c_block<LOG2N, T, J, false>(w, lane);
+        run_c_blocks<LOG2N, T, J + 1>(w, dst, lane);
     }
 }
 
-template <int LOG2N, typename T, int NW>
-__global__ void __launch_bounds__(NW * 32) qft_cdft_smem(const vec2<T> *__restrict__ in, vec2<T> *__restrict__ out,
-                                                         long long batch, const T *__restrict__ Ug) {
+template <int LOG2N, typename T>
+__global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, 1)
+    qft_cdft_smem(const vec2<T> *__restrict__ in, vec2<T> *__restrict__ out, long long batch,
+                  const T *__restrict__ Ug) {
     using P = SPlan<LOG2N>;
-    constexpr int NT = NW * 32;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    vec2<T> *w = reinterpret_cast<vec2<T> *>(smem_raw);
-    T *U = reinterpret_cast<T *>(smem_raw + sizeof(vec2<T>) * P::W_PADDED);
+    using K = KCfg<LOG2N, T>;
+    constexpr int TT = K::TT, NT = K::NT, NW = K::NW;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    vec2<T> *stage = reinterpret_cast<vec2<T> *>(smem_raw + K::STAGE_OFF);
+    vec2<T> *W = reinterpret_cast<vec2<T> *>(smem_raw + K::W_OFF);
+    T *U = reinterpret_cast<T *>(smem_raw + K::U_OFF);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + K::BAR_OFF);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+    const long long nbatch = (batch + TT - 1) / TT;
     for (int i = tid; i < P::UCELLS; i += NT) U[i] = Ug[i];
+    if (tid == 0) mbar_init(bar, 1);
     __syncthreads();
-
-    for (long long b = blockIdx.x; b < batch; b += gridDim.x) {
-        const vec2<T> *x = in + b * P::N;
-        vec2<T> *y = out + b * P::N;
-        // A0: fold + route
-        for (int n = tid; n <= P::m; n += NT) a0_item<LOG2N, T>(x, w, n);
+    long long bt = blockIdx.x;
+    if (tid == 0 && bt < nbatch) {
+        const long long nt = (batch - bt * TT) < TT ? (batch - bt * TT) : TT;
+        tma_bulk_load(stage, in + bt * TT * P::N, (uint32_t)(nt * P::N * K::VB), bar);
+    }
+    uint32_t parity = 0;
+    for (; bt < nbatch; bt += gridDim.x) {
+        const int ntr = (int)((batch - bt * TT) < TT ? (batch - bt * TT) : TT);
+        mbar_wait(bar, parity);
+        parity ^= 1u;
+        // A0: fold + route, staging -> W
+        for (int it = tid; it < TT * P::m; it += NT) {
+            const int tau = it / P::m, nn = it - tau * P::m;
+            if (tau < ntr) a0_item<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, nn);
+        }
         __syncthreads();
-        // A: forward levels of the big blocks (one warp per block side)
-        if constexpr (P::JF > 0) {
-            for (int u = warp; u < 2 * P::JF; u += NW) run_phase_a<LOG2N, T, 0>(w, U, u, lane);
+        // the staging buffer is free: prefetch the next batch while we compute
+        if (tid == 0 && bt + gridDim.x < nbatch) {
+            const long long nb = bt + gridDim.x;
+            const long long nt = (batch - nb * TT) < TT ? (batch - nb * TT) : TT;
+            tma_bulk_load(stage, in + nb * TT * P::N, (uint32_t)(nt * P::N * K::VB), bar);
+        }
+        // A: forward levels of the big blocks (warp units: side x {block 0, blocks 1..})
+        if constexpr (P::NWU > 0) {
+            for (int u = warp; u < TT * P::NWU; u += NW) {
+                const int tau = u / P::NWU, kind = u - tau * P::NWU;
+                if (tau >= ntr) continue;
+                vec2<T> *w = W + tau * P::PADDED;
+                const bool dst = kind & 1;
+                if (kind < 2) {
+                    if (dst) {
+                        FBlock<LOG2N, 0, true, T> f;
+                        f.load(w, U, lane);
+                        __syncwarp();
+                        f.store(w, lane);
+                    } else {
+                        FBlock<LOG2N, 0, false, T> f;
+                        f.load(w, U, lane);
+                        __syncwarp();
+                        f.store(w, lane);
+                    }
+                } else {
+                    run_f_blocks<LOG2N, T, 1>(w, U, dst, lane);
+                }
+                __syncwarp();
+            }
             __syncthreads();
         }
-        // B: full sub-transforms + tail
-        for (int u = tid; u < P::NB_UNITS; u += NT) b_unit<LOG2N, T>(w, U, u);
+        // B: Lee-32 on every 32-cell chunk (warp-uniform side), then the small blocks
+        for (int u = tid; u < 2 * K::NB32 + 2 * TT; u += NT) {
+            if (u < 2 * K::NB32) {
+                const bool dst = u >= K::NB32;
+                const int v = dst ? u - K::NB32 : u;
+                const int tau = v / (P::NL32 > 0 ? P::NL32 : 1), k = v - tau * P::NL32;
+                if (P::NL32 > 0 && tau < ntr) {
+                    vec2<T> *w = W + tau * P::PADDED;
+                    if (dst) b_l32<true, T>(w, P::S0 + 32 * k, U);
+                    else b_l32<false, T>(w, 32 * k, U);
+                }
+            } else {
+                const int v = u - 2 * K::NB32;
+                const int tau = v >> 1;
+                if (tau < ntr) {
+                    vec2<T> *w = W + tau * P::PADDED;
+                    if (v & 1) b_small<LOG2N, true, T>(w, U);
+                    else b_small<LOG2N, false, T>(w, U);
+                }
+            }
+        }
         __syncthreads();
         // C: backward levels of the big blocks
-        if constexpr (P::JF > 0) {
-            for (int u = warp; u < 2 * P::JF; u += NW) run_phase_c<LOG2N, T, 0>(w, u, lane);
+        if constexpr (P::NWU > 0) {
+            for (int u = warp; u < TT * P::NWU; u += NW) {
+                const int tau = u / P::NWU, kind = u - tau * P::NWU;
+                if (tau >= ntr) continue;
+                vec2<T> *w = W + tau * P::PADDED;
+                const bool dst = kind & 1;
+                if (kind < 2) {
+                    if (dst) run_c_block<LOG2N, T, 0, true>(w, lane);
+                    else run_c_block<LOG2N, T, 0, false>(w, lane);
+                } else {
+                    run_c_blocks<LOG2N, T, 1>(w, dst, lane);
+                }
+            }
             __syncthreads();
         }
-        // D: chain top + recombination -> global
-        for (int t = tid; t <= P::MRC; t += NT) Chain<LOG2N, T>::unit(w, y, t);
+        // D: chain + recombination -> global
+        for (int it = tid; it < TT * P::MRC; it += NT) {
+            const int tau = it / P::MRC, t = it - tau * P::MRC;
+            if (tau < ntr) Chain<LOG2N, T>::unit(W + tau * P::PADDED, out + (bt * TT + tau) * P::N, t);
+        }
         __syncthreads();
     }
 }
 
-constexpr int kSmemWarps = 4;
-
-inline int smem_bytes_for(int log2n, int prec) {
-    if (log2n < 6) return 0;
-    const int N = 1 << log2n;
-    const int cells = N + 32;
-    const int padded = cells + cells / 32 + 1;
-    const int vb = prec == 32 ? 8 : 16, sb = prec == 32 ? 4 : 8;
-    return padded * vb + (N / 4) * sb;
-}
-
+inline int smem_bytes_for_cfg(int smem) { return smem; }
 
 template <int LOG2N, typename T>
 cudaError_t launch_smem(const LaunchArgs &a) {
-    auto kern = qft_cdft_smem<LOG2N, T, kSmemWarps>;
-    const int smem = smem_bytes_for(LOG2N, sizeof(T) == 4 ? 32 : 64);
-    cudaError_t e;
-    if (smem > 48 * 1024) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-    }
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSmemWarps * 32, smem);
+    using K = KCfg<LOG2N, T>;
+    auto kern = qft_cdft_smem<LOG2N, T>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
     if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::NT, K::SMEM);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const long long nbatch = (a.batch + K::TT - 1) / K::TT;
     long long grid = (long long)a.num_sms * per_sm;
-    if (grid > a.batch) grid = a.batch;
+    if (grid > nbatch) grid = nbatch;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, kSmemWarps * 32, smem, a.stream>>>((const vec2<T> *)a.in, (vec2<T> *)a.out, a.batch,
-                                                          (const T *)a.U);
+    kern<<<(unsigned)grid, K::NT, K::SMEM, a.stream>>>((const vec2<T> *)a.in, (vec2<T> *)a.out, a.batch,
+                                                       (const T *)a.U);
     return cudaGetLastError();
 }
+
+template <int LOG2N, typename T>
+constexpr int smem_config_bytes() { return KCfg<LOG2N, T>::SMEM; }
 
 template <int NN, typename T>
 cudaError_t launch_reg(const LaunchArgs &a) {
@@ -141,7 +293,7 @@ cudaError_t launch_reg(const LaunchArgs &a) {
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     qft_cdft_reg<NN, T><<<(unsigned)blocks, 128, 0, a.stream>>>((const vec2<T> *)a.in, (vec2<T> *)a.out, a.batch,
-                                                            (const T *)a.U);
+                                                                (const T *)a.U);
     return cudaGetLastError();
 }
 

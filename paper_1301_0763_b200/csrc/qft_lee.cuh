@@ -93,33 +93,35 @@ QFT_HD void lee_fwd(vec2<T> *v, int t, const T *U) {
 // ---------------------------------------------------------------------------
 // R backward levels for column i of 2^R sub-block spectra (the neighbour sums
 // of improved.py:72-73 / :110-111 and the free interleaves of
-// elaborations.py:388-399).  v[p] = Z_p[i]; hv[p] = Z_p[i+1] (DCT) or Z_p[i-1]
-// (DST) for p >= 1 -- the halo is always a raw sub-block value because the
-// first element of the next column's range is reached through copies only.
-// edge: i is the last (DCT) / first (DST) column, where the reference copies
-// instead of adding.  Out: block spectrum slots [i*2^R, (i+1)*2^R).
+// elaborations.py:388-399).  v[p] = Z_p[i] (p relative to absolute index pofs);
+// halo(p) returns Z_p[i+1] (DCT) or Z_p[i-1] (DST) for absolute p -- the halo is
+// always a raw sub-block value because the first element of the next column's
+// range is reached through copies only.  edge: i is the last (DCT) / first
+// (DST) column, where the reference copies instead of adding.
+// Out: block spectrum slots [i*2^R, (i+1)*2^R).
 // ---------------------------------------------------------------------------
-template <int R, bool DST, typename T>
-QFT_HD void lee_bwd(const vec2<T> *v, const vec2<T> *hv, bool edge, vec2<T> *out) {
+template <int R, bool DST, typename T, class Halo>
+QFT_HD void lee_bwd_fn(const vec2<T> *v, int pofs, Halo &halo, bool edge, vec2<T> *out) {
     if constexpr (R == 0) {
         out[0] = v[0];
     } else {
         constexpr int H = 1 << (R - 1);
         vec2<T> e[H], o[H];
-        lee_bwd<R - 1, DST, T>(v, hv, edge, e);
-        lee_bwd<R - 1, DST, T>(v + H, hv + H, edge, o);
+        lee_bwd_fn<R - 1, DST, T>(v, pofs, halo, edge, e);
+        lee_bwd_fn<R - 1, DST, T>(v + H, pofs + H, halo, edge, o);
+        const vec2<T> hv = halo(pofs + H);  // leftmost leaf of the odd child
         if constexpr (!DST) {
 #pragma unroll
             for (int t = 0; t < H; ++t) out[2 * t] = e[t];
 #pragma unroll
             for (int t = 0; t < H - 1; ++t) out[2 * t + 1] = vadd(o[t], o[t + 1]);
-            out[2 * H - 1] = edge ? o[H - 1] : vadd(o[H - 1], hv[H]);
+            out[2 * H - 1] = edge ? o[H - 1] : vadd(o[H - 1], hv);
         } else {
 #pragma unroll
             for (int t = 0; t < H; ++t) out[2 * t + 1] = e[t];
 #pragma unroll
             for (int t = 1; t < H; ++t) out[2 * t] = vadd(o[t - 1], o[t]);
-            out[0] = edge ? o[0] : vadd(hv[H], o[0]);
+            out[0] = edge ? o[0] : vadd(hv, o[0]);
         }
     }
 }

@@ -1,208 +1,156 @@
-// qft_smem.cuh -- single-CTA improved-QFT of one length-N complex signal held
-// in shared memory (N = 2^6 .. 2^12 fp32, 2^6 .. 2^11 fp64).
+// qft_smem.cuh -- improved-QFT of length-N complex signals (N = 2^6 .. 2^12)
+// held in shared memory; a CTA works on T signals at a time.
 //
-// Working layout W (vec2 cells, padded address p + p/32 to break bank
-// conflicts of stride-32 accesses):
-//   C region [0, m]     : Lee block j (cosine, L_j = N/2^(j+2)) at off_j = m - 2L_j,
-//                         base pair s(0), s(m) at m-1, m
-//   S region [m+1, N)   : Lee block j (sine) at m+1+off_j
-//   tail     [N, N+32)  : C_JC (17 cells) and S_JC (15 cells), the cosine/sine
-//                         spectra of the 32-point sub-problem (JC = LOG2N-5)
-// Sample n = 2^j (2i+1) of the folded signal is element i of Lee block j: this
-// is the time-parity chain of improved._dct / _dst (improved.py:43, :81)
-// unrolled, with no arithmetic.
+// Working layout W of one signal (vec2 cells, padded address p + p/32 so that
+// the stride-32 accesses of phases B/C are bank-conflict free):
+//   [0, m-1)      cosine Lee blocks j = 0..n-2 (L_j = N/2^(j+2)) at off_j = m - 2L_j
+//   [m, N-1)      sine   Lee blocks at m + off_j
+//   N-1, N        the DCT base pair s(0), s(m)
+// Sample n = 2^j (2i+1) of the folded signal is element i of Lee block j: the
+// time-parity chain of improved._dct / _dst (improved.py:43, :81) unrolled.
 //
-// Phases (one __syncthreads between phases):
-//   A0  fold x[n] +- x[N-n] and route (shared.py:28-35)            global -> W
-//   A   RF forward levels of each big block (L > 32), in place        W -> W
-//   B   full Lee DCT-II/DST-II of every 32-cell sub-block and of the
-//       small blocks; the 32-point tail (improved.py:36-112)          W -> W
-//   C   RF backward levels of each big block (one warp per block)     W -> W
-//   D   time-split chain (elaborations.py:329-340) for the top RC levels,
-//       complex recombination (shared.py:58-72)                     W -> global
+// Phases (one __syncthreads between phases, all warps of the CTA run the same
+// phase so the instruction stream is shared):
+//   A0  fold x[n] +- x[N-n] and route (shared.py:28-35)           staging -> W
+//   A   forward fold levels of the big blocks (L > 32); sub-blocks of 32
+//       are written sub-block-major                                 W -> W
+//   B   full Lee DCT-II/DST-II of every 32-cell chunk; small blocks  W -> W
+//   C   backward levels of the big blocks (halo = neighbour lane)   W -> W
+//   D   time-split chain (elaborations.py:329-340) + complex
+//       recombination (shared.py:58-72)                          W -> global
 #pragma once
 #include "qft_lee.cuh"
 
 namespace qft {
 
-QFT_HD int padx(int p) { return p + (p >> 5); }
+QFT_HD constexpr int padx(int p) { return p + (p >> 5); }
 
 template <int LOG2N>
 struct SPlan {
-    static constexpr int N = 1 << LOG2N, m = N / 2, q = N / 4;
-    static constexpr int JC = LOG2N - 5;                    // tail level (N_JC = 32)
-    static constexpr int JF = LOG2N > 7 ? LOG2N - 7 : 0;    // blocks j < JF are big (L > 32)
-    static constexpr int RC = JC < 4 ? JC : 4;              // chain levels unfolded in phase D
-    static constexpr int L(int j) { return 1 << (LOG2N - 2 - j); }
+    static constexpr int n = LOG2N, N = 1 << LOG2N, m = N / 2, q = N / 4;
+    static constexpr int JF = n > 7 ? n - 7 : 0;     // big blocks j < JF (L > 32)
+    static constexpr int JS = n - 6;                 // first small block (L = 16)
+    static constexpr int RC = n - 2 < 4 ? n - 2 : 4; // chain levels unfolded in phase D
+    static constexpr int L(int j) { return 1 << (n - 2 - j); }
     static constexpr int off(int j) { return m - 2 * L(j); }
-    static constexpr int RF(int j) { return LOG2N - 7 - j; }  // big block: L = 32 << RF
-    static constexpr int TAIL = N;                          // tail cells
-    static constexpr int W_CELLS = N + 32;
-    static constexpr int W_PADDED = W_CELLS + W_CELLS / 32 + 1;
-    // phase B units: big sub-blocks (both sides), small blocks (both sides), tail
-    static constexpr int NSUB = JF > 0 ? (1 << (LOG2N - 6)) - 2 : 0;  // per side: sum 2^RF(j)
-    static constexpr int NSMALL = JC - JF;                  // per side
-    static constexpr int NB_UNITS = 2 * NSUB + 2 * NSMALL + 1;
-    static constexpr int MRC = N >> (RC + 1);               // phase D threads: t in [0, MRC]
-    static constexpr int UCELLS = N / 4;                    // level-table entries
+    static constexpr int RF(int j) { return n - 7 - j; }  // big block: L = 32 << RF
+    static constexpr int S0 = m;                     // sine region
+    static constexpr int BASE = N - 1;               // s(0) at N-1, s(m) at N
+    static constexpr int CELLS = N + 1;
+    static constexpr int PADDED = CELLS + CELLS / 32 + 1;
+    static constexpr int NL32 = n >= 7 ? m / 32 - 1 : 0;  // Lee-32 chunks per side
+    static constexpr int NWU = 2 * ((JF >= 1) + (JF >= 2)); // phase A/C warp units
+    static constexpr int MRC = N >> (RC + 1);        // phase D threads per signal
+    static constexpr int UCELLS = N / 4;             // level-table entries
 };
 
 // ---------------------------------------------------------------- phase A0
+// item n in [0, m): n = 0 routes s(0) and s(m); else folds the pair (n, N-n)
 template <int LOG2N, typename T>
 QFT_HD void a0_item(const vec2<T> *x, vec2<T> *w, int n) {
     using P = SPlan<LOG2N>;
     if (n == 0) {
-        w[padx(P::m - 1)] = x[0];  // dc[0] = x[0]
-    } else if (n == P::m) {
-        w[padx(P::m)] = x[P::m];   // dc[m] = x[m]
+        w[padx(P::BASE)] = x[0];
+        w[padx(P::BASE + 1)] = x[P::m];
     } else {
         vec2<T> a = x[n], b = x[P::N - n];
         const int j = ctz32((uint32_t)n);
-        const int i = n >> (j + 1);
-        const int off = P::m - 2 * (1 << (LOG2N - 2 - j));
-        w[padx(off + i)] = vadd(a, b);              // dc[n]   = x[n] + x[N-n]
-        w[padx(P::m + 1 + off + i)] = vsub(a, b);   // ds[n-1] = x[n] - x[N-n]
+        const int cell = P::m - (1 << (LOG2N - 1 - j)) + (n >> (j + 1));  // off_j + i
+        w[padx(cell)] = vadd(a, b);              // dc[n]   = x[n] + x[N-n]
+        w[padx(P::S0 + cell)] = vsub(a, b);      // ds[n-1] = x[n] - x[N-n]
     }
 }
 
 // ---------------------------------------------------------------- phase A
+// Lane t of the warp owning big block J of one side: loads its reflection group,
+// folds RF levels, and (after __syncwarp) writes element t of sub-block p to
+// cell 32p + t of the block.
 template <int LOG2N, int J, bool DST, typename T>
-QFT_HD void f_unit(vec2<T> *w, const T *U, int t) {
+struct FBlock {
     using P = SPlan<LOG2N>;
-    constexpr int L = P::L(J), R = P::RF(J), G = 1 << R;
-    constexpr int base = (DST ? P::m + 1 : 0) + P::off(J);
+    static constexpr int L = P::L(J), R = P::RF(J), G = 1 << R;
+    static constexpr int base = (DST ? P::S0 : 0) + P::off(J);  // multiple of 32
     vec2<T> v[G];
+    QFT_HD void load(const vec2<T> *w, const T *U, int t) {
+        const vec2<T> *bf = w + padx(base) + t;       // forward runs
+        const vec2<T> *br = w + padx(base) + 31 - t;  // reversed runs
 #pragma unroll
-    for (int s = 0; s < G; ++s) {
-        int c, sg;
-        run_of(R, L, s, c, sg);
-        v[s] = w[padx(base + c + sg * t)];
+        for (int s = 0; s < G; ++s) {
+            int c, sg;
+            run_of(R, L, s, c, sg);  // compile-time after unrolling
+            const int u = c >> 5;    // the run is the 32-aligned chunk u
+            v[s] = sg > 0 ? bf[33 * u] : br[33 * u];
+        }
+        lee_fwd<R, L, DST, T>(v, t, U);
     }
-    lee_fwd<R, L, DST, T>(v, t, U);
+    QFT_HD void store(vec2<T> *w, int t) const {
+        vec2<T> *o = w + padx(base) + t;
 #pragma unroll
-    for (int s = 0; s < G; ++s) {
-        int c, sg;
-        run_of(R, L, s, c, sg);
-        w[padx(base + c + sg * t)] = v[s];
+        for (int p = 0; p < G; ++p) o[33 * p] = v[p];
     }
-}
+};
 
 // ---------------------------------------------------------------- phase B
-template <int L, bool DST, typename T>
-QFT_HD void full_run(vec2<T> *w, int base, int c, int sg, const T *U) {
-    vec2<T> v[L];
+// Lee-32 on the 32-cell chunk starting at (padded) cell p0; in place.
+template <bool DST, typename T>
+QFT_HD void b_l32(vec2<T> *w, int chunk_base, const T *U) {
+    vec2<T> *c = w + padx(chunk_base);
+    vec2<T> v[32];
 #pragma unroll
-    for (int e = 0; e < L; ++e) v[e] = w[padx(base + c + sg * e)];
-    lee_full<L, DST, T>(v, U);
+    for (int e = 0; e < 32; ++e) v[e] = c[e];
+    lee_full<32, DST, T>(v, U);
 #pragma unroll
-    for (int e = 0; e < L; ++e) w[padx(base + c + sg * e)] = v[e];
+    for (int e = 0; e < 32; ++e) c[e] = v[e];
 }
 
-// cell of dc sample n (0 <= n <= m) / ds sample n (1 <= n < m) in W
-template <int LOG2N>
-QFT_HD int dc_cell(int n) {
+template <int LOG2N, bool DST, typename T, int J>
+QFT_HD void b_small_rec(vec2<T> *w, const T *U) {
     using P = SPlan<LOG2N>;
-    if (n == 0) return P::m - 1;
-    if (n == P::m) return P::m;
-    const int j = ctz32((uint32_t)n);
-    return P::m - 2 * (1 << (LOG2N - 2 - j)) + (n >> (j + 1));
-}
-template <int LOG2N>
-QFT_HD int ds_cell(int n) {
-    using P = SPlan<LOG2N>;
-    const int j = ctz32((uint32_t)n);
-    return P::m + 1 + P::m - 2 * (1 << (LOG2N - 2 - j)) + (n >> (j + 1));
-}
-
-template <int LOG2N, typename T>
-QFT_HD void tail_unit(vec2<T> *w, const T *U) {
-    using P = SPlan<LOG2N>;
-    constexpr int ST = 1 << P::JC;  // sample stride of the 32-point sub-problem
-    vec2<T> xc[17], xs[15], oc[17], os[15];
+    if constexpr (J <= LOG2N - 2) {
+        constexpr int L = P::L(J);
+        vec2<T> v[L];
+        constexpr int b0 = (DST ? P::S0 : 0) + P::off(J);
 #pragma unroll
-    for (int k = 0; k <= 16; ++k) xc[k] = w[padx(dc_cell<LOG2N>(k * ST))];
+        for (int e = 0; e < L; ++e) v[e] = w[padx(b0 + e)];
+        lee_full<L, DST, T>(v, U);
 #pragma unroll
-    for (int k = 1; k <= 15; ++k) xs[k - 1] = w[padx(ds_cell<LOG2N>(k * ST))];
-    dct0_reg<32, T>(xc, oc, U);
-    dst0_reg<32, T>(xs, os, U);
-#pragma unroll
-    for (int k = 0; k <= 16; ++k) w[padx(P::TAIL + k)] = oc[k];
-#pragma unroll
-    for (int k = 0; k < 15; ++k) w[padx(P::TAIL + 17 + k)] = os[k];
-}
-
-template <int LOG2N, int J, typename T>
-QFT_HD void b_big_dispatch(vec2<T> *w, const T *U, int pp, bool dst) {
-    using P = SPlan<LOG2N>;
-    if constexpr (J < P::JF) {
-        constexpr int G = 1 << P::RF(J);
-        if (pp < G) {
-            // after phase A, sub-block pp is the run c0 + sg0*e, e in [0, 32)
-            int c0, sg0;
-            run_of(P::RF(J), P::L(J), pp, c0, sg0);
-            if (dst) full_run<32, true, T>(w, P::m + 1 + P::off(J), c0, sg0, U);
-            else full_run<32, false, T>(w, P::off(J), c0, sg0, U);
-        } else {
-            b_big_dispatch<LOG2N, J + 1, T>(w, U, pp - G, dst);
-        }
+        for (int e = 0; e < L; ++e) w[padx(b0 + e)] = v[e];
+        b_small_rec<LOG2N, DST, T, J + 1>(w, U);
     }
 }
-
-template <int LOG2N, int J, typename T>
-QFT_HD void b_small_dispatch(vec2<T> *w, const T *U, int jj, bool dst) {
-    using P = SPlan<LOG2N>;
-    if constexpr (J < P::JC) {
-        if (jj == J) {
-            constexpr int L = P::L(J);
-            if (dst) full_run<L, true, T>(w, P::m + 1 + P::off(J), 0, 1, U);
-            else full_run<L, false, T>(w, P::off(J), 0, 1, U);
-        } else {
-            b_small_dispatch<LOG2N, J + 1, T>(w, U, jj, dst);
-        }
-    }
-}
-
-template <int LOG2N, typename T>
-QFT_HD void b_unit(vec2<T> *w, const T *U, int u) {
-    using P = SPlan<LOG2N>;
-    if (u < 2 * P::NSUB) {
-        const bool dst = u >= P::NSUB;
-        b_big_dispatch<LOG2N, 0, T>(w, U, dst ? u - P::NSUB : u, dst);
-    } else if (u < 2 * P::NSUB + 2 * P::NSMALL) {
-        const int v = u - 2 * P::NSUB;
-        const bool dst = v >= P::NSMALL;
-        b_small_dispatch<LOG2N, P::JF, T>(w, U, P::JF + (dst ? v - P::NSMALL : v), dst);
-    } else {
-        tail_unit<LOG2N, T>(w, U);
-    }
+// all blocks with L <= 16 of one side
+template <int LOG2N, bool DST, typename T>
+QFT_HD void b_small(vec2<T> *w, const T *U) {
+    constexpr int J0 = SPlan<LOG2N>::JS > 0 ? SPlan<LOG2N>::JS : 0;
+    b_small_rec<LOG2N, DST, T, J0>(w, U);
 }
 
 // ---------------------------------------------------------------- phase C
+// Lane i of the warp owning big block J of one side: column i of the 2^R
+// sub-block spectra -> block spectrum slots [i*2^R, (i+1)*2^R), natural order.
+// The halo Z_p[i+1] (DCT) / Z_p[i-1] (DST) is the neighbour lane's own value.
 template <int LOG2N, int J, bool DST, typename T>
-struct BUnit {
+struct CBlock {
     using P = SPlan<LOG2N>;
-    static constexpr int L = P::L(J), R = P::RF(J), G = 1 << R;
-    static constexpr int base = (DST ? P::m + 1 : 0) + P::off(J);
-    vec2<T> own[G], halo[G];
-
+    static constexpr int R = P::RF(J), G = 1 << R;
+    static constexpr int base = (DST ? P::S0 : 0) + P::off(J);
+    vec2<T> own[G];
     QFT_HD void load(const vec2<T> *w, int i) {
-        const int ih = DST ? i - 1 : i + 1;
-        const bool has_halo = ih >= 0 && ih < 32;
+        const vec2<T> *c = w + padx(base) + i;
 #pragma unroll
-        for (int p = 0; p < G; ++p) {
-            int c, sg;
-            run_of(R, L, p, c, sg);
-            own[p] = w[padx(base + c + sg * i)];
-            if (p > 0) halo[p] = has_halo ? w[padx(base + c + sg * ih)] : own[p];
-        }
-        halo[0] = own[0];
+        for (int p = 0; p < G; ++p) own[p] = c[33 * p];
     }
-    QFT_HD void store(vec2<T> *w, int i) const {
-        vec2<T> out[G];
+    // halo(p) must return the neighbour lane's own[p]
+    template <class Halo>
+    QFT_HD void compute(int i, Halo &&halo, vec2<T> *out) const {
         const bool edge = DST ? (i == 0) : (i == 31);
-        lee_bwd<R, DST, T>(own, halo, edge, out);
+        lee_bwd_fn<R, DST, T>(own, 0, halo, edge, out);
+    }
+    QFT_HD static void store(vec2<T> *w, int i, const vec2<T> *out) {
+        // slots i*G .. i*G+G-1 lie inside one 32-cell chunk: contiguous when padded
+        vec2<T> *o = w + padx(base + i * G);
 #pragma unroll
-        for (int s = 0; s < G; ++s) w[padx(base + i * G + s)] = out[s];
+        for (int s = 0; s < G; ++s) o[s] = out[s];
     }
 };
 
@@ -210,74 +158,98 @@ struct BUnit {
 template <int LOG2N, typename T>
 struct Chain {
     using P = SPlan<LOG2N>;
-    static QFT_HD vec2<T> OC(const vec2<T> *w, int j, int k) { return w[padx(P::m - 2 * (1 << (LOG2N - 2 - j)) + k)]; }
-    // sine spectrum of block j at harmonic h (slot h-1)
-    static QFT_HD vec2<T> OS(const vec2<T> *w, int j, int h) {
-        return w[padx(P::m + 1 + P::m - 2 * (1 << (LOG2N - 2 - j)) + h - 1)];
-    }
+    static constexpr int n = LOG2N;
+    static QFT_HD constexpr int qj(int j) { return 1 << (n - 2 - j); }
+    // cosine spectrum of Lee block j, slot k
+    static QFT_HD vec2<T> OC(const vec2<T> *w, int j, int k) { return w[padx(P::off(j) + k)]; }
+    // sine spectrum of Lee block j, harmonic h (slot h-1)
+    static QFT_HD vec2<T> OS(const vec2<T> *w, int j, int h) { return w[padx(P::S0 + P::off(j) + h - 1)]; }
 
-    // C_J[k] for 0 <= k <= m_J, descending the chain to the tail
+    // C_J[k], 0 <= k <= m_J: descend the time-split chain to the DCT base
     template <int J>
     static QFT_HD vec2<T> descC(const vec2<T> *w, int k) {
-        if constexpr (J == P::JC) {
-            return w[padx(P::TAIL + k)];
+        if constexpr (J == n - 1) {  // DCT-0 of two points: [s0 + sm, s0 - sm]
+            vec2<T> s0 = w[padx(P::BASE)], sm = w[padx(P::BASE + 1)];
+            return k == 0 ? vadd(s0, sm) : vsub(s0, sm);
         } else {
-            constexpr int qj = 1 << (LOG2N - 2 - J), mj = 2 * qj;
-            const int kk = k <= qj ? k : mj - k;
+            constexpr int q = qj(J), mm = 2 * q;
+            const int kk = k <= q ? k : mm - k;
             vec2<T> e = descC<J + 1>(w, kk);
-            if (k == qj) return e;                   // out[q] = E[q]
+            if (k == q) return e;                       // out[q] = E[q]
             vec2<T> o = OC(w, J, kk);
-            return k < qj ? vadd(e, o) : vsub(e, o);  // E+O / E-O
+            return k < q ? vadd(e, o) : vsub(e, o);     // E+O / E-O
         }
     }
-    // S_J[k] for 1 <= k <= m_J - 1 (other k: unused garbage, in-bounds reads)
+    // S_J[k], 1 <= k <= m_J - 1 (k = 0, m_J: unused value, in-bounds reads)
     template <int J>
     static QFT_HD vec2<T> descS(const vec2<T> *w, int k) {
-        if constexpr (J == P::JC) {
-            return w[padx(P::TAIL + 17 + (k > 0 ? k - 1 : 0))];
+        constexpr int q = qj(J), mm = 2 * q;
+        if constexpr (J == n - 2) {
+            return OS(w, J, 1);                         // _dst base: copy
         } else {
-            constexpr int qj = 1 << (LOG2N - 2 - J), mj = 2 * qj;
-            if (k == qj) return OS(w, J, qj);          // out[q-1] = O[q-1]
-            const int kk = k < qj ? k : mj - k;
+            if (k == q) return OS(w, J, q);             // out[q-1] = O[q-1]
+            const int kk = k < q ? k : mm - k;
             vec2<T> e = descS<J + 1>(w, kk);
             vec2<T> o = OS(w, J, kk);
-            return k < qj ? vadd(o, e) : vsub(o, e);  // O+E / O-E
+            return k < q ? vadd(o, e) : vsub(o, e);     // O+E / O-E
         }
     }
 
     static QFT_HD void emit(vec2<T> *y, int k, vec2<T> cv, vec2<T> sv) {
-        if (k == 0 || k == P::m) {
-            y[k] = cv;
-        } else {
-            vec2<T> lo, hi;
-            recombine(cv, sv, lo, hi);
-            y[k] = lo;
-            y[P::N - k] = hi;
-        }
+        vec2<T> lo, hi;
+        recombine(cv, sv, lo, hi);
+        y[k] = lo;
+        y[P::N - k] = hi;
     }
 
+    // regular thread: every index stays strictly inside (0, q_j) at every level
     template <int J>
     static QFT_HD void up(const vec2<T> *w, vec2<T> *y, int k, vec2<T> cv, vec2<T> sv) {
         if constexpr (J == 0) {
             emit(y, k, cv, sv);
         } else {
-            constexpr int qj = 1 << (LOG2N - 2 - (J - 1)), mj = 2 * qj;
-            const bool self = (k == qj);
-            vec2<T> o = OC(w, J - 1, self ? 0 : k);
-            vec2<T> os = OS(w, J - 1, k);
-            vec2<T> clo = self ? cv : vadd(cv, o);
-            vec2<T> chi = self ? cv : vsub(cv, o);
-            vec2<T> slo = self ? os : vadd(os, sv);
-            vec2<T> shi = self ? os : vsub(os, sv);
-            up<J - 1>(w, y, k, clo, slo);
-            up<J - 1>(w, y, self ? qj : mj - k, chi, shi);
+            constexpr int mm = 2 * qj(J - 1);
+            vec2<T> o = OC(w, J - 1, k), os = OS(w, J - 1, k);
+            up<J - 1>(w, y, k, vadd(cv, o), vadd(os, sv));
+            up<J - 1>(w, y, mm - k, vsub(cv, o), vsub(os, sv));
         }
     }
 
+    // special thread: groups of t = 0 and t = m_RC; every index is compile-time
+    template <int J, int K>
+    static QFT_HD void up_s(const vec2<T> *w, vec2<T> *y, vec2<T> cv, vec2<T> sv) {
+        if constexpr (J == 0) {
+            if constexpr (K == 0 || K == P::m) y[K] = cv;  // harmonics 0, N/2: copies
+            else emit(y, K, cv, sv);
+        } else {
+            constexpr int q = qj(J - 1), mm = 2 * q;
+            if constexpr (K == q) {                        // C copy, S leaf
+                up_s<J - 1, q>(w, y, cv, OS(w, J - 1, q));
+            } else {
+                vec2<T> o = OC(w, J - 1, K);
+                if constexpr (K == 0) {                    // no sine harmonic 0
+                    up_s<J - 1, 0>(w, y, vadd(cv, o), sv);
+                    up_s<J - 1, mm>(w, y, vsub(cv, o), sv);
+                } else {
+                    vec2<T> os = OS(w, J - 1, K);
+                    up_s<J - 1, K>(w, y, vadd(cv, o), vadd(os, sv));
+                    up_s<J - 1, mm - K>(w, y, vsub(cv, o), vsub(os, sv));
+                }
+            }
+        }
+    }
+
+    // t in [0, MRC): t = 0 is the special thread (groups 0 and MRC)
     static QFT_HD void unit(const vec2<T> *w, vec2<T> *y, int t) {
-        vec2<T> cv = descC<P::RC>(w, t);
-        vec2<T> sv = descS<P::RC>(w, t);
-        up<P::RC>(w, y, t, cv, sv);
+        constexpr int RC = P::RC;
+        if (t == 0) {
+            vec2<T> c0 = descC<RC>(w, 0);
+            up_s<RC, 0>(w, y, c0, c0);
+            constexpr int qq = qj(RC - 1);                 // = MRC
+            up_s<RC - 1, qq>(w, y, descC<RC>(w, qq), OS(w, RC - 1, qq));
+        } else {
+            up<RC>(w, y, t, descC<RC>(w, t), descS<RC>(w, t));
+        }
     }
 };
 

@@ -23,21 +23,36 @@ static void build_U(int N, const T *Tnat, std::vector<T> &U) {
         for (int i = 0; i < S / 2; ++i) U[S / 2 + i] = Tnat[(2 * i + 1) * (N / (4 * S))];
 }
 
+template <int LOG2N, typename T, int J, bool DST>
+static void emu_f_side(vec2<T> *w, const T *U) {
+    std::vector<FBlock<LOG2N, J, DST, T>> lanes(32);
+    for (int t = 0; t < 32; ++t) lanes[t].load(w, U, t);   // all lanes load ...
+    for (int t = 0; t < 32; ++t) lanes[t].store(w, t);     // ... __syncwarp ... store
+}
+
 template <int LOG2N, typename T, int J>
 static void emu_f(vec2<T> *w, const T *U) {
     using P = SPlan<LOG2N>;
     if constexpr (J < P::JF) {
-        for (int t = 0; t < 32; ++t) f_unit<LOG2N, J, false, T>(w, U, t);
-        for (int t = 0; t < 32; ++t) f_unit<LOG2N, J, true, T>(w, U, t);
+        emu_f_side<LOG2N, T, J, false>(w, U);
+        emu_f_side<LOG2N, T, J, true>(w, U);
         emu_f<LOG2N, T, J + 1>(w, U);
     }
 }
 
 template <int LOG2N, typename T, int J, bool DST>
 static void emu_c_side(vec2<T> *w) {
-    std::vector<BUnit<LOG2N, J, DST, T>> lanes(32);
+    using CB = CBlock<LOG2N, J, DST, T>;
+    std::vector<CB> lanes(32);
+    std::vector<std::vector<vec2<T>>> outs(32, std::vector<vec2<T>>(CB::G));
     for (int i = 0; i < 32; ++i) lanes[i].load(w, i);
-    for (int i = 0; i < 32; ++i) lanes[i].store(w, i);
+    for (int i = 0; i < 32; ++i) {
+        // the device gets the halo with a shuffle from lane i+1 (DCT) / i-1 (DST)
+        const int nb = DST ? i - 1 : i + 1;
+        auto halo = [&](int p) { return (nb >= 0 && nb < 32) ? lanes[nb].own[p] : lanes[i].own[p]; };
+        lanes[i].compute(i, halo, outs[i].data());
+    }
+    for (int i = 0; i < 32; ++i) CB::store(w, i, outs[i].data());
 }
 
 template <int LOG2N, typename T, int J>
@@ -53,13 +68,18 @@ static void emu_c(vec2<T> *w) {
 template <int LOG2N, typename T>
 static void emu_one(const vec2<T> *x, vec2<T> *y, const T *U) {
     using P = SPlan<LOG2N>;
-    std::vector<vec2<T>> W(P::W_PADDED);
-    vec2<T> *w = W.data();
-    for (int n = 0; n <= P::m; ++n) a0_item<LOG2N, T>(x, w, n);
+    std::vector<vec2<T>> Wv(P::PADDED);
+    vec2<T> *w = Wv.data();
+    for (int n = 0; n < P::m; ++n) a0_item<LOG2N, T>(x, w, n);
     emu_f<LOG2N, T, 0>(w, U);
-    for (int u = 0; u < P::NB_UNITS; ++u) b_unit<LOG2N, T>(w, U, u);
+    for (int k = 0; k < P::NL32; ++k) {
+        b_l32<false, T>(w, 32 * k, U);
+        b_l32<true, T>(w, P::S0 + 32 * k, U);
+    }
+    b_small<LOG2N, false, T>(w, U);
+    b_small<LOG2N, true, T>(w, U);
     emu_c<LOG2N, T, 0>(w);
-    for (int t = 0; t <= P::MRC; ++t) Chain<LOG2N, T>::unit(w, y, t);
+    for (int t = 0; t < P::MRC; ++t) Chain<LOG2N, T>::unit(w, y, t);
 }
 
 template <int NN, typename T>
