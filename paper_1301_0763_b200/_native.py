@@ -10,7 +10,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqftb200.so")
+LIB_PATH = os.environ.get("QFT_LIB") or os.path.join(_HERE, "libqftb200.so")  # QFT_LIB: A/B variants
 
 QFT_PREC_F32 = 32
 QFT_PREC_F64 = 64

@@ -56,15 +56,17 @@ def _compile(src, obj, defines):
     return obj
 
 
-def build(jobs=None, verbose=True):
-    """Compile all translation units (cached) and link libqftb200.so."""
+def build(jobs=None, verbose=True, defines=(), lib=None):
+    """Compile all translation units (cached) and link libqftb200.so.
+    ``defines``/``lib``: build an experimental variant (e.g. QFT_CTAS_PER_SM=3)."""
     os.makedirs(BUILD, exist_ok=True)
-    dig = _headers_digest()
-    units = [(os.path.join(CSRC, "qft_capi.cu"), os.path.join(BUILD, f"capi_{dig}.o"), [])]
+    dig = _headers_digest() + ("_" + hashlib.sha256(" ".join(defines).encode()).hexdigest()[:8] if defines else "")
+    target = lib or LIB
+    units = [(os.path.join(CSRC, "qft_capi.cu"), os.path.join(BUILD, f"capi_{dig}.o"), list(defines))]
     for p in PRECS:
         for l in LOG2NS:
             units.append((os.path.join(CSRC, "qft_inst.cu"), os.path.join(BUILD, f"inst_{p}_{l}_{dig}.o"),
-                          [f"QFT_INST_PREC={p}", f"QFT_INST_LOG2N={l}"]))
+                          [f"QFT_INST_PREC={p}", f"QFT_INST_LOG2N={l}"] + list(defines)))
     todo = [u for u in units if not os.path.exists(u[1])]
     if todo:
         jobs = jobs or max(2, os.cpu_count() or 2)
@@ -73,13 +75,13 @@ def build(jobs=None, verbose=True):
         with cf.ThreadPoolExecutor(jobs) as ex:
             list(ex.map(lambda u: _compile(*u), todo))
     objs = [u[1] for u in units]
-    tmp = LIB + ".tmp"
+    tmp = target + ".tmp"
     cmd = [nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart"]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
+    os.replace(tmp, target)
     if verbose:
-        print(f"[build] {LIB}", flush=True)
-    return LIB
+        print(f"[build] {target}", flush=True)
+    return target
 
 
 def ptxas_report():
@@ -105,4 +107,8 @@ def ptxas_report():
 
 
 if __name__ == "__main__":
-    build(jobs=int(sys.argv[1]) if len(sys.argv) > 1 else None)
+    # python -m paper_1301_0763_b200.build [out.so DEFINE=VAL ...]
+    if len(sys.argv) > 1:
+        build(lib=os.path.abspath(sys.argv[1]), defines=tuple(sys.argv[2:]))
+    else:
+        build()

@@ -79,6 +79,39 @@ template <typename T>
 QFT_HD vec2<T> vsub(vec2<T> a, vec2<T> b) { return {rsub(a.x, b.x), rsub(a.y, b.y)}; }
 template <typename T>
 QFT_HD vec2<T> vmul(vec2<T> a, T c) { return {rmul(a.x, c), rmul(a.y, c)}; }
+
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000 && !defined(QFT_NO_F32X2)
+// sm_100a packed fp32 adds: one FADD2 per (Re-part, Im-part) pair.  .rn is the
+// IEEE round-to-nearest single-precision op on each lane (denormals preserved),
+// i.e. bit-identical to two scalar __fadd_rn.  Multiplies stay scalar
+// (mul.rn.f32): ptxas 12.9 contracts mul.rn.f32x2 (and fma.rn.f32x2 with a -0
+// addend) followed by add.rn.f32x2 into FFMA2 even under --fmad=false, which
+// would change the rounding; scalar .rn multiplies are never contracted.
+// tests/test_sass.py checks the built kernels contain no FFMA/FFMA2/DFMA.
+QFT_DEV unsigned long long pk(vec2<float> a) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+QFT_DEV vec2<float> upk(unsigned long long r) {
+    vec2<float> a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+template <>
+QFT_DEV vec2<float> vadd<float>(vec2<float> a, vec2<float> b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+    return upk(r);
+}
+template <>
+QFT_DEV vec2<float> vsub<float>(vec2<float> a, vec2<float> b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+    return upk(r);
+}
+
+#endif
 template <typename T>
 QFT_HD vec2<T> vsel(bool p, vec2<T> a, vec2<T> b) { return p ? a : b; }
 

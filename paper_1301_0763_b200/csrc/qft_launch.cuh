@@ -11,6 +11,13 @@
 
 #include "qft_smem.cuh"
 
+#ifndef QFT_CTAS_PER_SM
+#define QFT_CTAS_PER_SM 1  // shared-memory budget split: CTAs resident per SM
+#endif
+#ifndef QFT_A0_UNIT8
+#define QFT_A0_UNIT8 0     // A0 with 8 pairs per thread (fewer instructions, more bank conflicts)
+#endif
+
 namespace qft {
 
 struct LaunchArgs {
@@ -55,14 +62,14 @@ struct KCfg {
     static constexpr int VB = (int)sizeof(vec2<T>);
     static constexpr int PER = P::N * VB + P::PADDED * VB;  // staging + working per signal
     static constexpr int UB = P::UCELLS * (int)sizeof(T);
-    static constexpr int BUDGET = 200 * 1024 - UB - 64;
+    static constexpr int BUDGET = (226 * 1024) / QFT_CTAS_PER_SM - UB - 64;
     static constexpr int TT0 = BUDGET / PER;
     static constexpr int TT = TT0 < 1 ? 1 : (TT0 > 64 ? 64 : TT0);  // signals per CTA iteration
     static constexpr int rup32(int x) { return (x + 31) / 32 * 32; }
     static constexpr int NB32 = rup32(TT * P::NL32);                 // phase-B Lee-32 lanes per side
     static constexpr int W_B = (2 * NB32 + rup32(2 * TT)) / 32;
     static constexpr int W_D = (TT * P::MRC + 31) / 32;
-    static constexpr int W_AC = TT * P::NWU;
+    static constexpr int W_AC = TT * P::NWU + QFT_CHAIN_MID;  // + the chain-mid warp
     static constexpr int mx(int a, int b) { return a > b ? a : b; }
     static constexpr int NW0 = mx(mx(W_B, W_D), W_AC);
     static constexpr int NWMAX = sizeof(T) == 8 ? 12 : 16;  // keep >= 168 registers for fp64
@@ -149,8 +156,38 @@ QFT_DEV void run_c_blocks(vec2<T> *w, bool dst, int lane) {
     }
 }
 
+// chain-mid: one warp computes C_JM / S_JM of all signals, level by level
+template <int LOG2N, typename T, int TT>
+QFT_DEV void run_chain_mid(vec2<T> *W, int ntr, int lane) {
+    using P = SPlan<LOG2N>;
+    using C = Chain<LOG2N, T>;
+    for (int it = lane; it < ntr; it += 32) C::mid_base(W + it * P::PADDED);
+    __syncwarp();
+    constexpr int RK = (P::MJM + 1 + 31) / 32;  // rounds of 32 lanes per signal and level
+    for (int j = P::n - 2; j >= P::JM; --j) {
+        const int cnt = 2 * C::qj(j) + 1;  // k in [0, m_j]
+        vec2<T> cv[TT][RK], sv[TT][RK];
+#pragma unroll
+        for (int tau = 0; tau < TT; ++tau)
+#pragma unroll
+            for (int r = 0; r < RK; ++r) {
+                const int k = lane + 32 * r;
+                if (tau < ntr && k < cnt) C::mid_level_load(W + tau * P::PADDED, j, k, cv[tau][r], sv[tau][r]);
+            }
+        __syncwarp();
+#pragma unroll
+        for (int tau = 0; tau < TT; ++tau)
+#pragma unroll
+            for (int r = 0; r < RK; ++r) {
+                const int k = lane + 32 * r;
+                if (tau < ntr && k < cnt) C::mid_level_store(W + tau * P::PADDED, j, k, cv[tau][r], sv[tau][r]);
+            }
+        __syncwarp();
+    }
+}
+
 template <int LOG2N, typename T>
-__global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, 1)
+__global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
     qft_cdft_smem(const vec2<T> *__restrict__ in, vec2<T> *__restrict__ out, long long batch,
                   const T *__restrict__ Ug) {
     using P = SPlan<LOG2N>;
@@ -178,10 +215,17 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, 1)
         mbar_wait(bar, parity);
         parity ^= 1u;
         // A0: fold + route, staging -> W
-        for (int it = tid; it < TT * P::m; it += NT) {
-            const int tau = it / P::m, nn = it - tau * P::m;
-            if (tau < ntr) a0_item<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, nn);
+#if QFT_A0_UNIT8
+        for (int it = tid; it < TT * (P::m / 8); it += NT) {
+            const int tau = it / (P::m / 8), k = it - tau * (P::m / 8);
+            if (tau < ntr) a0_unit8<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, k);
         }
+#else
+        for (int tau = 0; tau < TT; ++tau) {
+            if (tau >= ntr) break;
+            for (int nn = tid; nn < P::m; nn += NT) a0_item<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, nn);
+        }
+#endif
         __syncthreads();
         // the staging buffer is free: prefetch the next batch while we compute
         if (tid == 0 && bt + gridDim.x < nbatch) {
@@ -237,18 +281,25 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, 1)
             }
         }
         __syncthreads();
-        // C: backward levels of the big blocks
-        if constexpr (P::NWU > 0) {
-            for (int u = warp; u < TT * P::NWU; u += NW) {
-                const int tau = u / P::NWU, kind = u - tau * P::NWU;
-                if (tau >= ntr) continue;
-                vec2<T> *w = W + tau * P::PADDED;
-                const bool dst = kind & 1;
-                if (kind < 2) {
-                    if (dst) run_c_block<LOG2N, T, 0, true>(w, lane);
-                    else run_c_block<LOG2N, T, 0, false>(w, lane);
-                } else {
-                    run_c_blocks<LOG2N, T, 1>(w, dst, lane);
+        // C: backward levels of the big blocks; one more warp unit computes the
+        // lower chain levels C_JM, S_JM of all signals (chain-mid)
+        {
+            for (int u = warp; u < TT * P::NWU + QFT_CHAIN_MID; u += NW) {
+                if (QFT_CHAIN_MID && u == TT * P::NWU) {
+                    run_chain_mid<LOG2N, T, TT>(W, ntr, lane);
+                    continue;
+                }
+                if constexpr (P::NWU > 0) {
+                    const int tau = u / P::NWU, kind = u - tau * P::NWU;
+                    if (tau >= ntr) continue;
+                    vec2<T> *w = W + tau * P::PADDED;
+                    const bool dst = kind & 1;
+                    if (kind < 2) {
+                        if (dst) run_c_block<LOG2N, T, 0, true>(w, lane);
+                        else run_c_block<LOG2N, T, 0, false>(w, lane);
+                    } else {
+                        run_c_blocks<LOG2N, T, 1>(w, dst, lane);
+                    }
                 }
             }
             __syncthreads();

@@ -21,6 +21,10 @@
 #pragma once
 #include "qft_lee.cuh"
 
+#ifndef QFT_CHAIN_MID
+#define QFT_CHAIN_MID 0  // 1: lower chain levels by one warp in phase C; 0: per-thread descent in D
+#endif
+
 namespace qft {
 
 QFT_HD constexpr int padx(int p) { return p + (p >> 5); }
@@ -36,7 +40,12 @@ struct SPlan {
     static constexpr int RF(int j) { return n - 7 - j; }  // big block: L = 32 << RF
     static constexpr int S0 = m;                     // sine region
     static constexpr int BASE = N - 1;               // s(0) at N-1, s(m) at N
-    static constexpr int CELLS = N + 1;
+    static constexpr int JM = RC + 1;                // chain-mid level (computed in phase C)
+    static constexpr int MJM = N >> (JM + 1);        // m_JM: C_JM has MJM+1 cells, S_JM MJM-1
+    static constexpr int CHC = N + 1;                // C_JM cells [CHC, CHC + MJM]
+    static constexpr int CHS = CHC + MJM + 1;        // S_JM harmonic h at CHS + h - 1
+    static constexpr int CELLS = CHS + MJM;
+    static_assert(JM > n - 2 || (1 << (n - 2 - JM)) <= 32, "chain-mid blocks must be finished by phase B");
     static constexpr int PADDED = CELLS + CELLS / 32 + 1;
     static constexpr int NL32 = n >= 7 ? m / 32 - 1 : 0;  // Lee-32 chunks per side
     static constexpr int NWU = 2 * ((JF >= 1) + (JF >= 2)); // phase A/C warp units
@@ -45,6 +54,22 @@ struct SPlan {
 };
 
 // ---------------------------------------------------------------- phase A0
+// Unit k in [0, m/8) folds the pairs (n, N-n) for n = 8k+1 .. 8k+8 and routes
+// them (shared.py:28-35); unit 0 also routes s(0), and n = m is the base s(m).
+template <typename T>
+QFT_HD void ld2(const vec2<T> *p, vec2<T> &a, vec2<T> &b) {  // p 16-byte aligned
+#if defined(__CUDA_ARCH__)
+    if constexpr (sizeof(T) == 4) {
+        const float4 v = *reinterpret_cast<const float4 *>(p);
+        a = {v.x, v.y};
+        b = {v.z, v.w};
+        return;
+    }
+#endif
+    a = p[0];
+    b = p[1];
+}
+
 // item n in [0, m): n = 0 routes s(0) and s(m); else folds the pair (n, N-n)
 template <int LOG2N, typename T>
 QFT_HD void a0_item(const vec2<T> *x, vec2<T> *w, int n) {
@@ -59,6 +84,42 @@ QFT_HD void a0_item(const vec2<T> *x, vec2<T> *w, int n) {
         w[padx(cell)] = vadd(a, b);              // dc[n]   = x[n] + x[N-n]
         w[padx(P::S0 + cell)] = vsub(a, b);      // ds[n-1] = x[n] - x[N-n]
     }
+}
+
+template <int LOG2N, typename T>
+QFT_HD void a0_unit8(const vec2<T> *x, vec2<T> *w, int k) {
+    using P = SPlan<LOG2N>;
+    vec2<T> f[9], r[8];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) ld2(x + 8 * k + e, f[e], f[e + 1]);
+    f[8] = x[8 * k + 8];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) ld2(x + P::N - 8 * k - 8 + e, r[e], r[e + 1]);
+    // r[e] = x[N - n] for n = 8k + 8 - e
+    constexpr int off0 = P::off(0), off1 = P::off(1), off2 = P::off(2);
+    vec2<T> *c0 = w + padx(off0 + 4 * k), *s0 = w + padx(P::S0 + off0 + 4 * k);
+#pragma unroll
+    for (int d = 1; d < 8; d += 2) {  // odd n: block 0, i = 4k + (d-1)/2
+        c0[(d - 1) / 2] = vadd(f[d], r[8 - d]);
+        s0[(d - 1) / 2] = vsub(f[d], r[8 - d]);
+    }
+    vec2<T> *c1 = w + padx(off1 + 2 * k), *s1 = w + padx(P::S0 + off1 + 2 * k);
+    c1[0] = vadd(f[2], r[6]);  // n = 8k+2: block 1, i = 2k
+    s1[0] = vsub(f[2], r[6]);
+    c1[1] = vadd(f[6], r[2]);  // n = 8k+6: i = 2k+1
+    s1[1] = vsub(f[6], r[2]);
+    w[padx(off2 + k)] = vadd(f[4], r[4]);  // n = 8k+4: block 2, i = k
+    w[padx(P::S0 + off2 + k)] = vsub(f[4], r[4]);
+    const int n8 = 8 * k + 8;
+    if (n8 == P::m) {
+        w[padx(P::BASE + 1)] = f[8];  // dc[m] = x[m]
+    } else {
+        const int j = ctz32((uint32_t)n8);
+        const int cell = P::m - (1 << (LOG2N - 1 - j)) + (n8 >> (j + 1));
+        w[padx(cell)] = vadd(f[8], r[0]);
+        w[padx(P::S0 + cell)] = vsub(f[8], r[0]);
+    }
+    if (k == 0) w[padx(P::BASE)] = f[0];  // dc[0] = x[0]
 }
 
 // ---------------------------------------------------------------- phase A
@@ -165,16 +226,53 @@ struct Chain {
     // sine spectrum of Lee block j, harmonic h (slot h-1)
     static QFT_HD vec2<T> OS(const vec2<T> *w, int j, int h) { return w[padx(P::S0 + P::off(j) + h - 1)]; }
 
+    // ---- chain-mid (phase C, one warp per signal): C_j, S_j for j = n-1 .. JM,
+    // bottom-up, in place in the chain cells (elaborations.py:329-340).
+    // C_j[k] = E[k]+O[k], C_j[m_j-k] = E[k]-O[k] (k < q_j), C_j[q_j] = E[q_j];
+    // S_j[h] = O[h]+E[h], S_j[m_j-h] = O[h]-E[h] (h < q_j), S_j[q_j] = O[q_j].
+    static QFT_HD void mid_level_load(const vec2<T> *w, int j, int k, vec2<T> &c, vec2<T> &s) {
+        const int q = qj(j), mm = 2 * q;
+        if (k <= mm) {  // C_j[k]
+            const int kk = k <= q ? k : mm - k;
+            vec2<T> e = w[padx(P::CHC + kk)];
+            if (k == q) c = e;
+            else {
+                vec2<T> o = OC(w, j, kk);
+                c = k < q ? vadd(e, o) : vsub(e, o);
+            }
+        }
+        if (k >= 1 && k < mm) {  // S_j[k]
+            if (k == q) s = OS(w, j, q);
+            else {
+                const int kk = k < q ? k : mm - k;
+                vec2<T> o = OS(w, j, kk);
+                vec2<T> e = w[padx(P::CHS + kk - 1)];
+                s = k < q ? vadd(o, e) : vsub(o, e);
+            }
+        }
+    }
+    static QFT_HD void mid_level_store(vec2<T> *w, int j, int k, vec2<T> c, vec2<T> s) {
+        const int mm = 2 * qj(j);
+        if (k <= mm) w[padx(P::CHC + k)] = c;
+        if (k >= 1 && k < mm) w[padx(P::CHS + k - 1)] = s;
+    }
+    static QFT_HD void mid_base(vec2<T> *w) {  // C_{n-1} = DCT-0 of two points
+        vec2<T> s0 = w[padx(P::BASE)], sm = w[padx(P::BASE + 1)];
+        w[padx(P::CHC)] = vadd(s0, sm);
+        w[padx(P::CHC + 1)] = vsub(s0, sm);
+    }
+
+#if !QFT_CHAIN_MID
     // C_J[k], 0 <= k <= m_J: descend the time-split chain to the DCT base
     template <int J>
-    static QFT_HD vec2<T> descC(const vec2<T> *w, int k) {
+    static QFT_HD vec2<T> descCJ(const vec2<T> *w, int k) {
         if constexpr (J == n - 1) {  // DCT-0 of two points: [s0 + sm, s0 - sm]
             vec2<T> s0 = w[padx(P::BASE)], sm = w[padx(P::BASE + 1)];
             return k == 0 ? vadd(s0, sm) : vsub(s0, sm);
         } else {
             constexpr int q = qj(J), mm = 2 * q;
             const int kk = k <= q ? k : mm - k;
-            vec2<T> e = descC<J + 1>(w, kk);
+            vec2<T> e = descCJ<J + 1>(w, kk);
             if (k == q) return e;                       // out[q] = E[q]
             vec2<T> o = OC(w, J, kk);
             return k < q ? vadd(e, o) : vsub(e, o);     // E+O / E-O
@@ -182,18 +280,40 @@ struct Chain {
     }
     // S_J[k], 1 <= k <= m_J - 1 (k = 0, m_J: unused value, in-bounds reads)
     template <int J>
-    static QFT_HD vec2<T> descS(const vec2<T> *w, int k) {
+    static QFT_HD vec2<T> descSJ(const vec2<T> *w, int k) {
         constexpr int q = qj(J), mm = 2 * q;
         if constexpr (J == n - 2) {
             return OS(w, J, 1);                         // _dst base: copy
         } else {
             if (k == q) return OS(w, J, q);             // out[q-1] = O[q-1]
             const int kk = k < q ? k : mm - k;
-            vec2<T> e = descS<J + 1>(w, kk);
+            vec2<T> e = descSJ<J + 1>(w, kk);
             vec2<T> o = OS(w, J, kk);
             return k < q ? vadd(o, e) : vsub(o, e);     // O+E / O-E
         }
     }
+    static QFT_HD vec2<T> descC(const vec2<T> *w, int k) { return descCJ<P::RC>(w, k); }
+    static QFT_HD vec2<T> descS(const vec2<T> *w, int k) { return descSJ<P::RC>(w, k); }
+#else
+    // C_RC[k], 0 <= k <= m_RC, from the chain-mid C_JM (one level)
+    static QFT_HD vec2<T> descC(const vec2<T> *w, int k) {
+        constexpr int q = qj(P::RC), mm = 2 * q;
+        const int kk = k <= q ? k : mm - k;
+        vec2<T> e = w[padx(P::CHC + kk)];
+        if (k == q) return e;                       // out[q] = E[q]
+        vec2<T> o = OC(w, P::RC, kk);
+        return k < q ? vadd(e, o) : vsub(e, o);     // E+O / E-O
+    }
+    // S_RC[k], 1 <= k <= m_RC - 1 (other k: unused value, in-bounds reads)
+    static QFT_HD vec2<T> descS(const vec2<T> *w, int k) {
+        constexpr int q = qj(P::RC), mm = 2 * q;
+        if (k == q) return OS(w, P::RC, q);         // out[q-1] = O[q-1]
+        const int kk = k < q ? k : mm - k;
+        vec2<T> o = OS(w, P::RC, kk);
+        vec2<T> e = w[padx(P::CHS + (kk > 0 ? kk - 1 : 0))];
+        return k < q ? vadd(o, e) : vsub(o, e);     // O+E / O-E
+    }
+#endif
 
     static QFT_HD void emit(vec2<T> *y, int k, vec2<T> cv, vec2<T> sv) {
         vec2<T> lo, hi;
@@ -243,12 +363,12 @@ struct Chain {
     static QFT_HD void unit(const vec2<T> *w, vec2<T> *y, int t) {
         constexpr int RC = P::RC;
         if (t == 0) {
-            vec2<T> c0 = descC<RC>(w, 0);
+            vec2<T> c0 = descC(w, 0);
             up_s<RC, 0>(w, y, c0, c0);
             constexpr int qq = qj(RC - 1);                 // = MRC
-            up_s<RC - 1, qq>(w, y, descC<RC>(w, qq), OS(w, RC - 1, qq));
+            up_s<RC - 1, qq>(w, y, descC(w, qq), OS(w, RC - 1, qq));
         } else {
-            up<RC>(w, y, t, descC<RC>(w, t), descS<RC>(w, t));
+            up<RC>(w, y, t, descC(w, t), descS(w, t));
         }
     }
 };

@@ -70,7 +70,7 @@ static void emu_one(const vec2<T> *x, vec2<T> *y, const T *U) {
     using P = SPlan<LOG2N>;
     std::vector<vec2<T>> Wv(P::PADDED);
     vec2<T> *w = Wv.data();
-    for (int n = 0; n < P::m; ++n) a0_item<LOG2N, T>(x, w, n);
+    for (int k = 0; k < P::m / 8; ++k) a0_unit8<LOG2N, T>(x, w, k);
     emu_f<LOG2N, T, 0>(w, U);
     for (int k = 0; k < P::NL32; ++k) {
         b_l32<false, T>(w, 32 * k, U);
@@ -79,6 +79,17 @@ static void emu_one(const vec2<T> *x, vec2<T> *y, const T *U) {
     b_small<LOG2N, false, T>(w, U);
     b_small<LOG2N, true, T>(w, U);
     emu_c<LOG2N, T, 0>(w);
+#if QFT_CHAIN_MID
+    // chain-mid: level by level, all loads of a level before its stores (__syncwarp)
+    using C = Chain<LOG2N, T>;
+    C::mid_base(w);
+    for (int j = P::n - 2; j >= P::JM; --j) {
+        const int cnt = 2 * C::qj(j) + 1;
+        std::vector<vec2<T>> cv(cnt), sv(cnt);
+        for (int k = 0; k < cnt; ++k) C::mid_level_load(w, j, k, cv[k], sv[k]);
+        for (int k = 0; k < cnt; ++k) C::mid_level_store(w, j, k, cv[k], sv[k]);
+    }
+#endif
     for (int t = 0; t < P::MRC; ++t) Chain<LOG2N, T>::unit(w, y, t);
 }
 

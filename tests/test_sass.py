@@ -1,0 +1,56 @@
+"""The arithmetic contract at the instruction level: the transform kernels must
+contain no fused multiply-add of any width (FFMA, FFMA2, DFMA, HFMA2), so every
+value is one IEEE-rounded add/sub/mul as in the reference's counted primitives
+(counting.py:40-81).  Also checks the kernels really are sm_100a code and that
+the fp32 path uses the packed FADD2 pipe.  CPU only (cuobjdump)."""
+
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+LIB = os.path.join(ROOT, "paper_1301_0763_b200", "libqftb200.so")
+
+
+def sass_by_function():
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([exe, "-sass", LIB], capture_output=True, text=True).stdout
+    funcs, cur = {}, None
+    for line in out.splitlines():
+        m = re.match(r"\s*Function : (\S+)", line)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = []
+        elif cur:
+            m = re.match(r"\s*/\*[0-9a-f]{4,}\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)([^;]*);", line)
+            if m:
+                op, args = m.group(2), m.group(3)
+                # "HFMA2 Rd, -RZ, RZ, imm, imm" is ptxas's idiom for loading a constant
+                if op.startswith("HFMA2") and "-RZ, RZ" in args:
+                    op = "MOV(HFMA2-imm)"
+                funcs[cur].append(op)
+    return funcs, out
+
+
+def test_no_fused_multiply_add_in_transform_kernels():
+    funcs, _ = sass_by_function()
+    kernels = {k: v for k, v in funcs.items() if "qft_cdft" in k}
+    assert len(kernels) >= 20, "expected the per-size transform kernels"
+    for name, ops in kernels.items():
+        fused = [o for o in ops if re.match(r"(FFMA|DFMA|HFMA)", o)]
+        assert not fused, f"{name}: fused multiply-add {set(fused)} would change rounding"
+
+
+def test_sm100a_and_packed_fp32():
+    funcs, out = sass_by_function()
+    assert "sm_100a" in out
+    smem32 = [k for k in funcs if "qft_cdft_smem" in k and "ILi12EfE" in k]
+    assert smem32, "fp32 N=4096 kernel missing"
+    ops = funcs[smem32[0]]
+    assert any(o.startswith("FADD2") for o in ops), "fp32 adds should use the packed FADD2 pipe"
