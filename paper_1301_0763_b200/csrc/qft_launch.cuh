@@ -14,6 +14,9 @@
 #ifndef QFT_CTAS_PER_SM
 #define QFT_CTAS_PER_SM 1  // shared-memory budget split: CTAs resident per SM
 #endif
+#ifndef QFT_HALO_SHFL
+#define QFT_HALO_SHFL 0    // phase-C halo by warp shuffle (1) or by a shared-memory read (0)
+#endif
 #ifndef QFT_A0_UNIT8
 #define QFT_A0_UNIT8 0     // A0 with 8 pairs per thread (fewer instructions, more bank conflicts)
 #endif
@@ -140,7 +143,12 @@ QFT_DEV void run_c_block(vec2<T> *w, int lane) {
     c.load(w, lane);
     constexpr int G = CBlock<LOG2N, J, DST, T>::G;
     vec2<T> out[G];
+#if QFT_HALO_SHFL
     auto halo = [&](int p) { return shfl_vec(c.own[p], !DST); };
+#else
+    const vec2<T> *hc = CBlock<LOG2N, J, DST, T>::halo_col(w, lane);
+    auto halo = [&](int p) { return hc[33 * p]; };  // read before the __syncwarp below
+#endif
     c.compute(lane, halo, out);
     __syncwarp();
     c.store(w, lane, out);
@@ -201,6 +209,7 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
     const long long nbatch = (batch + TT - 1) / TT;
+    const A0Lane a0l = a0_lane<LOG2N>(lane);
     for (int i = tid; i < P::UCELLS; i += NT) U[i] = Ug[i];
     if (tid == 0) mbar_init(bar, 1);
     __syncthreads();
@@ -221,9 +230,17 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
             if (tau < ntr) a0_unit8<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, k);
         }
 #else
-        for (int tau = 0; tau < TT; ++tau) {
-            if (tau >= ntr) break;
-            for (int nn = tid; nn < P::m; nn += NT) a0_item<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, nn);
+        {
+            // warps take chunks of 32 consecutive n; lane 0's multiples of 32 afterwards
+            constexpr int NCH = P::m / 32;
+            for (int u = warp; u < TT * NCH; u += NW) {
+                const int tau = u / NCH, c = u - tau * NCH;
+                if (tau < ntr && lane) a0_chunk<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, c, lane, a0l);
+            }
+            for (int it = tid; it < TT * NCH; it += NT) {
+                const int tau = it / NCH, c = it - tau * NCH;
+                if (tau < ntr) a0_item<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, 32 * c);
+            }
         }
 #endif
         __syncthreads();

@@ -86,6 +86,31 @@ QFT_HD void a0_item(const vec2<T> *x, vec2<T> *w, int n) {
     }
 }
 
+// A0 by chunks of 32 consecutive n: lane l (1..31) handles n = 32c + l, whose
+// class j = ctz(l) and cell off_j + (n >> (j+1)) = A_l + c * B_l do not depend
+// on c except through B_l; lane 0's n = 32c (c >= 1) are done by a0_item.
+struct A0Lane {
+    int A, B;  // cell = A + c*B (cosine side)
+};
+template <int LOG2N>
+QFT_HD A0Lane a0_lane(int l) {
+    using P = SPlan<LOG2N>;
+    A0Lane r;
+    const int j = ctz32((uint32_t)(l | 32));
+    r.A = P::m - (1 << (LOG2N - 1 - j)) + (l >> (j + 1));
+    r.B = 32 >> (j + 1);
+    return r;
+}
+template <int LOG2N, typename T>
+QFT_HD void a0_chunk(const vec2<T> *x, vec2<T> *w, int c, int l, A0Lane a) {
+    using P = SPlan<LOG2N>;
+    const int n = 32 * c + l;
+    vec2<T> u = x[n], v = x[P::N - n];
+    const int cell = a.A + c * a.B;
+    w[padx(cell)] = vadd(u, v);              // dc[n]   = x[n] + x[N-n]
+    w[padx(P::S0 + cell)] = vsub(u, v);      // ds[n-1] = x[n] - x[N-n]
+}
+
 template <int LOG2N, typename T>
 QFT_HD void a0_unit8(const vec2<T> *x, vec2<T> *w, int k) {
     using P = SPlan<LOG2N>;
@@ -200,6 +225,11 @@ struct CBlock {
         const vec2<T> *c = w + padx(base) + i;
 #pragma unroll
         for (int p = 0; p < G; ++p) own[p] = c[33 * p];
+    }
+    // halo column (i+1 for DCT, i-1 for DST; the edge lane re-reads its own column)
+    QFT_HD static const vec2<T> *halo_col(const vec2<T> *w, int i) {
+        const int ih = DST ? (i > 0 ? i - 1 : i) : (i < 31 ? i + 1 : i);
+        return w + padx(base) + ih;
     }
     // halo(p) must return the neighbour lane's own[p]
     template <class Halo>
@@ -316,10 +346,12 @@ struct Chain {
 #endif
 
     static QFT_HD void emit(vec2<T> *y, int k, vec2<T> cv, vec2<T> sv) {
-        vec2<T> lo, hi;
-        recombine(cv, sv, lo, hi);
-        y[k] = lo;
-        y[P::N - k] = hi;
+        // S(k) = (C1 + S2, C2 - S1), S(N-k) = (C1 - S2, C2 + S1) (shared.py:218-221):
+        // with u = (S2, -S1): S(k) = cv + u, S(N-k) = cv - u, bit for bit
+        // (x - (-y) == x + y and x + (-y) == x - y in IEEE arithmetic).
+        const vec2<T> u = {sv.y, -sv.x};
+        y[k] = vadd(cv, u);
+        y[P::N - k] = vsub(cv, u);
     }
 
     // regular thread: every index stays strictly inside (0, q_j) at every level

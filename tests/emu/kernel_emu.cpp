@@ -49,7 +49,8 @@ static void emu_c_side(vec2<T> *w) {
     for (int i = 0; i < 32; ++i) {
         // the device gets the halo with a shuffle from lane i+1 (DCT) / i-1 (DST)
         const int nb = DST ? i - 1 : i + 1;
-        auto halo = [&](int p) { return (nb >= 0 && nb < 32) ? lanes[nb].own[p] : lanes[i].own[p]; };
+        const vec2<T> *hc = CB::halo_col(w, i);  // the device reads the halo column before any store
+        auto halo = [&](int p) { (void)nb; return hc[33 * p]; };
         lanes[i].compute(i, halo, outs[i].data());
     }
     for (int i = 0; i < 32; ++i) CB::store(w, i, outs[i].data());
@@ -70,7 +71,10 @@ static void emu_one(const vec2<T> *x, vec2<T> *y, const T *U) {
     using P = SPlan<LOG2N>;
     std::vector<vec2<T>> Wv(P::PADDED);
     vec2<T> *w = Wv.data();
-    for (int k = 0; k < P::m / 8; ++k) a0_unit8<LOG2N, T>(x, w, k);
+    for (int c = 0; c < P::m / 32; ++c) {
+        for (int l = 1; l < 32; ++l) a0_chunk<LOG2N, T>(x, w, c, l, a0_lane<LOG2N>(l));
+        a0_item<LOG2N, T>(x, w, 32 * c);
+    }
     emu_f<LOG2N, T, 0>(w, U);
     for (int k = 0; k < P::NL32; ++k) {
         b_l32<false, T>(w, 32 * k, U);
