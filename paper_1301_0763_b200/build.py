@@ -64,6 +64,9 @@ def build(jobs=None, verbose=True, defines=(), lib=None):
     target = lib or LIB
     units = [(os.path.join(CSRC, "qft_capi.cu"), os.path.join(BUILD, f"capi_{dig}.o"), list(defines))]
     for p in PRECS:
+        units.append((os.path.join(CSRC, "qft_large.cu"), os.path.join(BUILD, f"large_{p}_{dig}.o"),
+                      [f"QFT_LARGE_PREC={p}"] + list(defines)))
+    for p in PRECS:
         for l in LOG2NS:
             units.append((os.path.join(CSRC, "qft_inst.cu"), os.path.join(BUILD, f"inst_{p}_{l}_{dig}.o"),
                           [f"QFT_INST_PREC={p}", f"QFT_INST_LOG2N={l}"] + list(defines)))

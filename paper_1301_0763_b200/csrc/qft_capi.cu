@@ -14,6 +14,7 @@
 
 #include "../../include/qft_b200.h"
 #include "qft_launch.cuh"
+#include "qft_large_api.h"
 
 using namespace qft;
 
@@ -123,6 +124,8 @@ struct qft_plan {
     int num_sms = 0;
     void *d_U = nullptr;
     size_t u_bytes = 0;
+    double uhead64[32] = {0};  // host copy of U[0..32) (kernel-parameter constants)
+    float uhead32[32] = {0};
     std::vector<double> t64;
     std::vector<float> t32;
     // scratch for layout conversion / host path
@@ -130,6 +133,9 @@ struct qft_plan {
     size_t scratch_bytes = 0;
     cudaStream_t streams[2] = {nullptr, nullptr};
     std::mutex mu;
+    void *large = nullptr;      // multi-pass schedule (N > 4096)
+    void *d_lscratch = nullptr; // its scratch (two buffers of N+2 cells per signal of a chunk)
+    size_t lscratch_bytes = 0;
 };
 
 // per-instance launchers, one translation unit each (qft_inst.cu)
@@ -153,16 +159,47 @@ typedef void (*cfg_fn)(int *);
 static const cfg_fn kCfg[2][13] = {QFT_CROW(32), QFT_CROW(64)};
 static constexpr int kMaxLog2N = 12;
 
-static int launch_contig(const qft_plan *p, const void *in, void *out, long long batch, cudaStream_t st) {
+static constexpr int kMaxLargeLog2N = 20;
+static bool is_large(const qft_plan *p) { return p->log2n > kMaxLog2N; }
+
+static int launch_large(qft_plan *p, const void *in, void *out, long long batch, cudaStream_t st) {
+    // bound the scratch (two buffers of N+2 cells per signal) to ~2 GiB: chunk the batch
+    const size_t esz = p->prec == QFT_PREC_F32 ? 8 : 16;
+    const size_t per = 2 * ((size_t)p->N + 2) * esz;
+    long long chunk = (long long)(((size_t)2 << 30) / per);
+    if (chunk < 1) chunk = 1;
+    if (chunk > batch) chunk = batch;
+    if (p->lscratch_bytes < per * (size_t)chunk) {
+        if (p->d_lscratch) cudaFree(p->d_lscratch);
+        p->d_lscratch = nullptr;
+        p->lscratch_bytes = 0;
+        CUDA_TRY(cudaMalloc(&p->d_lscratch, per * (size_t)chunk));
+        p->lscratch_bytes = per * (size_t)chunk;
+    }
+    const void *uh = p->prec == QFT_PREC_F32 ? (const void *)p->uhead32 : (const void *)p->uhead64;
+    for (long long b0 = 0; b0 < batch; b0 += chunk) {
+        const long long nb = batch - b0 < chunk ? batch - b0 : chunk;
+        const char *ci = (const char *)in + (size_t)b0 * p->N * esz;
+        char *co = (char *)out + (size_t)b0 * p->N * esz;
+        int e = p->prec == QFT_PREC_F32 ? qft_large_exec_f32(p->large, ci, co, nb, p->d_U, uh, p->d_lscratch, st)
+                                        : qft_large_exec_f64(p->large, ci, co, nb, p->d_U, uh, p->d_lscratch, st);
+        if (e) return fail(QFT_ECUDA, std::string("multi-pass launch: ") + cudaGetErrorString((cudaError_t)e));
+    }
+    return 0;
+}
+
+static int launch_contig(qft_plan *p, const void *in, void *out, long long batch, cudaStream_t st) {
+    if (is_large(p)) return launch_large(p, in, out, batch, st);
     if (p->log2n < 1 || p->log2n > kMaxLog2N)
         return fail(QFT_EUNSUPPORTED, "periodization 2^" + std::to_string(p->log2n) + " not built yet");
-    LaunchArgs a{in, out, batch, p->d_U, p->num_sms, st};
+    LaunchArgs a{in, out, batch, p->d_U, p->prec == QFT_PREC_F32 ? (const void *)p->uhead32 : (const void *)p->uhead64,
+                 p->num_sms, st};
     int e = kLaunch[p->prec == QFT_PREC_F32 ? 0 : 1][p->log2n](&a);
     if (e != 0) return fail(QFT_ECUDA, std::string("kernel launch: ") + cudaGetErrorString((cudaError_t)e));
     return 0;
 }
 
-static bool size_supported(int log2n) { return log2n >= 1 && log2n <= kMaxLog2N; }
+static bool size_supported(int log2n) { return log2n >= 1 && log2n <= kMaxLargeLog2N; }
 
 // Exported functions inherit C linkage from their extern "C" declarations in qft_b200.h.
 
@@ -194,6 +231,7 @@ int qft_plan_create(qft_plan **out, int log2n, int prec, int algo, int device) {
         std::vector<double> U;
         if (p->N >= 8) natural_table_f64(p->N, p->t64);
         level_table(p->N, p->t64, U);
+        for (size_t i = 0; i < 32 && i < U.size(); ++i) p->uhead64[i] = U[i];
         p->u_bytes = U.size() * sizeof(double);
         if (cudaMalloc(&p->d_U, p->u_bytes) != cudaSuccess ||
             cudaMemcpy(p->d_U, U.data(), p->u_bytes, cudaMemcpyHostToDevice) != cudaSuccess)
@@ -202,10 +240,15 @@ int qft_plan_create(qft_plan **out, int log2n, int prec, int algo, int device) {
         std::vector<float> U;
         if (p->N >= 8) natural_table_f32(p->N, p->t32);
         level_table(p->N, p->t32, U);
+        for (size_t i = 0; i < 32 && i < U.size(); ++i) p->uhead32[i] = U[i];
         p->u_bytes = U.size() * sizeof(float);
         if (cudaMalloc(&p->d_U, p->u_bytes) != cudaSuccess ||
             cudaMemcpy(p->d_U, U.data(), p->u_bytes, cudaMemcpyHostToDevice) != cudaSuccess)
             rc = fail(QFT_ECUDA, "table upload failed");
+    }
+    if (!rc && is_large(p)) {
+        int e = prec == QFT_PREC_F32 ? qft_large_create_f32(log2n, &p->large) : qft_large_create_f64(log2n, &p->large);
+        if (e) rc = fail(QFT_ECUDA, "multi-pass schedule upload failed");
     }
     if (rc) {
         qft_plan_destroy(p);
@@ -220,6 +263,11 @@ int qft_plan_destroy(qft_plan *p) {
     cudaSetDevice(p->device);
     if (p->d_U) cudaFree(p->d_U);
     if (p->d_scratch) cudaFree(p->d_scratch);
+    if (p->d_lscratch) cudaFree(p->d_lscratch);
+    if (p->large) {
+        if (p->prec == QFT_PREC_F32) qft_large_destroy_f32(p->large);
+        else qft_large_destroy_f64(p->large);
+    }
     for (auto &s : p->streams)
         if (s) cudaStreamDestroy(s);
     delete p;
@@ -236,6 +284,19 @@ int qft_plan_get_info(const qft_plan *p, qft_plan_info_t *info) {
     info->kernel_launches = 1;
     int cfg[3] = {0, 0, 0};
     if (p->log2n >= 1 && p->log2n <= kMaxLog2N) kCfg[p->prec == QFT_PREC_F32 ? 0 : 1][p->log2n](cfg);
+    if (is_large(p)) {
+        int passes = 0, launches = 0;
+        if (p->prec == QFT_PREC_F32) qft_large_info_f32(p->large, &passes, &launches);
+        else qft_large_info_f64(p->large, &passes, &launches);
+        info->passes = passes;
+        info->kernel_launches = launches;
+        info->smem_bytes = 0;
+        info->threads_per_cta = 256;
+        info->ctas_per_sm = 0;
+        info->signals_per_cta = 0;
+        info->scratch_bytes = (int64_t)(p->scratch_bytes + p->lscratch_bytes);
+        return 0;
+    }
     info->smem_bytes = cfg[0];
     info->threads_per_cta = cfg[1];
     info->ctas_per_sm = p->log2n >= 6 ? 1 : 0;
@@ -262,12 +323,14 @@ int qft_plan_set_table(qft_plan *p, const void *h_table) {
         p->t64.assign(t, t + p->N / 4);
         std::vector<double> U;
         level_table(p->N, p->t64, U);
+        for (size_t i = 0; i < 32 && i < U.size(); ++i) p->uhead64[i] = U[i];
         CUDA_TRY(cudaMemcpy(p->d_U, U.data(), U.size() * sizeof(double), cudaMemcpyHostToDevice));
     } else {
         const float *t = (const float *)h_table;
         p->t32.assign(t, t + p->N / 4);
         std::vector<float> U;
         level_table(p->N, p->t32, U);
+        for (size_t i = 0; i < 32 && i < U.size(); ++i) p->uhead32[i] = U[i];
         CUDA_TRY(cudaMemcpy(p->d_U, U.data(), U.size() * sizeof(float), cudaMemcpyHostToDevice));
     }
     return 0;

@@ -1,0 +1,276 @@
+// qft_large.cuh -- multi-pass improved-QFT for N = 2^13 .. 2^20 (fp32 / fp64).
+//
+// A signal is too large for one CTA, so the Lee blocks of the time-parity
+// chain are decomposed across passes over HBM (one scratch layout per signal,
+// two scratch buffers W0/W1 of N+1 cells, the same cell map as qft_smem.cuh
+// without padding):
+//   fold   x -> W0: x[n] +- x[N-n] routed to Lee block j = ctz(n) (shared.py:28-35)
+//   F(d)   in-place forward fold levels (r <= 5 per pass) of every Lee block
+//          larger than the leaf size; each pass leaves 2^r sub-blocks as
+//          contiguous (possibly reversed) runs of the same cells
+//   leaf   every block / sub-block of size <= LEAF: full Lee DCT-II/DST-II,
+//          one warp (shared memory, F/Lee-32/B with __syncwarp) or one thread
+//   B(d)   backward levels (neighbour sums + interleave), deepest first,
+//          ping-pong W0 <-> W1, output in natural spectrum order
+//   chain  time-split chain + complex recombination -> y (elaborations.py:329-340,
+//          shared.py:58-72); each thread descends the chain from the DCT base
+// The host plan builder (qft_large_plan.cu) compiles the decomposition tree of
+// the reference recursion into these task lists.
+#pragma once
+#include "qft_lee.cuh"
+
+namespace qft {
+
+// ----------------------------------------------------------------- tasks
+struct FTask {        // r forward levels of one run (in place)
+    int c, sg, L;     // run: element e at cell c + sg*e
+};
+struct LeafTask {     // full Lee of one run (in place, spectrum along the run)
+    int c, sg, L, dst;
+};
+struct BTask {        // r backward levels: 2^r sub-block spectra -> natural block spectrum
+    int c, sg, L;     // parent run (its sub-blocks are the runs of run_of(r, L, p))
+    int in_buf, leaf; // sub-block spectra in W[in_buf]; leaf: along each run, else forward at its min cell
+    int out_buf, out0;  // block spectrum written to W[out_buf] cells [out0, out0 + L)
+    int dst;
+};
+
+// runtime-L forward levels (lee_fwd with a runtime block size)
+template <int R, typename T, bool DST>
+QFT_HD void lee_fwd_rt(vec2<T> *v, int t, int L, const T *U) {
+    if constexpr (R > 0) {
+        constexpr int G = 1 << R, H = G / 2;
+        vec2<T> nv[G];
+#pragma unroll
+        for (int s = 0; s < H; ++s) {
+            int c, sg;
+            run_of(R - 1, L / 2, s, c, sg);
+            const int i = c + sg * t;
+            vec2<T> a = v[s], b = v[G - 1 - s];
+            const T k = U[L / 2 + i];
+            if constexpr (!DST) {
+                nv[s] = vadd(a, b);
+                nv[H + s] = vmul(vsub(a, b), k);
+            } else {
+                nv[s] = vsub(a, b);
+                nv[H + s] = vmul(vadd(a, b), k);
+            }
+        }
+        lee_fwd_rt<R - 1, T, DST>(nv, t, L / 2, U);
+        lee_fwd_rt<R - 1, T, DST>(nv + H, t, L / 2, U);
+#pragma unroll
+        for (int s = 0; s < G; ++s) v[s] = nv[s];
+    }
+}
+
+// ----------------------------------------------------------------- fold
+// cells: cosine block j at m - 2^(n-1-j) + i, sine at m + same, s(0) at N-1, s(m) at N
+template <typename T>
+QFT_HD void lg_fold_item(const vec2<T> *x, vec2<T> *w, int n, int N, int log2n) {
+    const int m = N / 2;
+    if (n == 0) {
+        w[N - 1] = x[0];
+        w[N] = x[m];
+    } else {
+        vec2<T> a = x[n], b = x[N - n];
+        const int j = ctz32((uint32_t)n);
+        const int cell = m - (1 << (log2n - 1 - j)) + (n >> (j + 1));
+        w[cell] = vadd(a, b);
+        w[m + cell] = vsub(a, b);
+    }
+}
+
+// ----------------------------------------------------------------- F pass
+template <int R, typename T, bool DST>
+QFT_HD void lg_f_group(vec2<T> *w, const FTask &tk, int t, const T *U) {
+    constexpr int G = 1 << R;
+    vec2<T> v[G];
+    int pos[G];
+#pragma unroll
+    for (int s = 0; s < G; ++s) {
+        int c, sg;
+        run_of(R, tk.L, s, c, sg);
+        pos[s] = tk.c + tk.sg * (c + sg * t);
+        v[s] = w[pos[s]];
+    }
+    lee_fwd_rt<R, T, DST>(v, t, tk.L, U);
+#pragma unroll
+    for (int s = 0; s < G; ++s) w[pos[s]] = v[s];  // slot s keeps its cells (in place)
+}
+
+// ----------------------------------------------------------------- B pass
+template <int R, typename T, bool DST>
+QFT_HD void lg_b_column(vec2<T> *const *W, const BTask &tk, int i) {
+    constexpr int G = 1 << R;
+    const int S = tk.L >> R;
+    const vec2<T> *src = W[tk.in_buf];
+    vec2<T> own[G], hal[G];
+    const int ih = DST ? (i > 0 ? i - 1 : i) : (i < S - 1 ? i + 1 : i);
+#pragma unroll
+    for (int p = 0; p < G; ++p) {
+        int c, sg;
+        run_of(R, tk.L, p, c, sg);
+        const int rc = tk.c + tk.sg * c, rs = tk.sg * sg;  // sub-block run
+        int st, dir;
+        if (tk.leaf) {
+            st = rc;
+            dir = rs;
+        } else {
+            st = rs > 0 ? rc : rc - (S - 1);
+            dir = 1;
+        }
+        own[p] = src[st + dir * i];
+        hal[p] = src[st + dir * ih];
+    }
+    auto halo = [&](int p) { return hal[p]; };
+    vec2<T> out[G];
+    const bool edge = DST ? (i == 0) : (i == S - 1);
+    lee_bwd_fn<R, DST, T>(own, 0, halo, edge, out);
+    vec2<T> *dst = W[tk.out_buf] + tk.out0 + i * G;
+#pragma unroll
+    for (int s = 0; s < G; ++s) dst[s] = out[s];
+}
+
+// ----------------------------------------------------------------- leaf (thread)
+template <int L, typename T, bool DST>
+QFT_HD void lg_leaf_thread(vec2<T> *w, const LeafTask &tk, const T *U) {
+    vec2<T> v[L];
+#pragma unroll
+    for (int e = 0; e < L; ++e) v[e] = w[tk.c + tk.sg * e];
+    lee_full<L, DST, T>(v, U);
+#pragma unroll
+    for (int e = 0; e < L; ++e) w[tk.c + tk.sg * e] = v[e];
+}
+
+// ----------------------------------------------------------------- leaf (warp)
+// Lee block of L = 32 << R cells staged in a padded shared buffer s (natural
+// element order); three lane phases separated by __syncwarp, as in qft_smem.cuh.
+template <int R, typename T, bool DST>
+struct WarpLee {
+    static constexpr int G = 1 << R, L = 32 << R;
+    QFT_HD static int px(int p) { return p + (p >> 5); }
+    // phase 1 (lane t): reflection group -> sub-block-major (element t of sub-block p at 32p + t)
+    struct F {
+        vec2<T> v[G];
+        QFT_HD void load(const vec2<T> *s, int t, const T *U) {
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
+                int c, sg;
+                run_of(R, L, q, c, sg);
+                v[q] = s[px(c + sg * t)];
+            }
+            lee_fwd<R, L, DST, T>(v, t, U);
+        }
+        QFT_HD void store(vec2<T> *s, int t) const {
+#pragma unroll
+            for (int p = 0; p < G; ++p) s[px(32 * p + t)] = v[p];
+        }
+    };
+    // phase 2 (lane p < G): Lee-32 of sub-block p
+    QFT_HD static void lee32(vec2<T> *s, int p, const T *U) {
+        vec2<T> v[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = s[px(32 * p + e)];
+        lee_full<32, DST, T>(v, U);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) s[px(32 * p + e)] = v[e];
+    }
+    // phase 3 (lane i): column i -> block spectrum slots [iG, iG + G)
+    struct B {
+        vec2<T> out[G];
+        QFT_HD void compute(const vec2<T> *s, int i) {
+            vec2<T> own[G];
+            const int ih = DST ? (i > 0 ? i - 1 : i) : (i < 31 ? i + 1 : i);
+#pragma unroll
+            for (int p = 0; p < G; ++p) own[p] = s[px(32 * p + i)];
+            auto halo = [&](int p) { return s[px(32 * p + ih)]; };
+            const bool edge = DST ? (i == 0) : (i == 31);
+            lee_bwd_fn<R, DST, T>(own, 0, halo, edge, out);
+        }
+        QFT_HD void store(vec2<T> *s, int i) const {
+#pragma unroll
+            for (int q = 0; q < G; ++q) s[px(i * G + q)] = out[q];
+        }
+    };
+};
+
+// ----------------------------------------------------------------- chain
+// Each thread t in [0, m_RC] (m_RC = N >> (RC+1)) descends the chain from the
+// DCT base to level RC (index at level J: the distance of t to the nearest
+// multiple of m_{J-1}), then unfolds RC levels and writes 2^(RC+1) outputs.
+// Duplicate slots (self-paired indices) write identical values twice.
+template <typename T>
+struct GChain {
+    const vec2<T> *w0, *w1;  // scratch buffers (base pair s(0), s(m) in W0)
+    uint32_t cmask, smask;   // bit j: the cosine / sine spectrum of block j is in W1
+    int n, N, m;
+
+    QFT_HD int off(int j) const { return m - (1 << (n - 1 - j)); }
+    QFT_HD vec2<T> OC(int j, int k) const { return ((cmask >> j) & 1 ? w1 : w0)[off(j) + k]; }
+    QFT_HD vec2<T> OS(int j, int h) const { return ((smask >> j) & 1 ? w1 : w0)[m + off(j) + h - 1]; }
+    QFT_HD int qj(int j) const { return 1 << (n - 2 - j); }
+
+    // C_RC[t], S_RC[t]
+    template <int RC>
+    QFT_HD void descend(int t, vec2<T> &cv, vec2<T> &sv) const {
+        // level n-1: [s0 + sm, s0 - sm] at index kk_{n-1} in {0, 1}
+        auto kk = [&](int J) -> int {  // index at level J
+            if (J == RC) return t;
+            const int P = 2 << (n - 1 - J);  // m_{J-1}
+            const int r = t & (P - 1);
+            return r < P - r ? r : P - r;
+        };
+        {
+            const vec2<T> s0 = w0[N - 1], sm = w0[N];
+            cv = kk(n - 1) == 0 ? vadd(s0, sm) : vsub(s0, sm);
+        }
+        sv = vec2<T>{(T)0, (T)0};
+        for (int J = n - 2; J >= RC; --J) {
+            const int k = kk(J), q = qj(J);
+            const int k1 = k < q ? k : 2 * q - k;  // index at level J+1
+            if (k != q) {
+                const vec2<T> o = OC(J, k1);
+                cv = k < q ? vadd(cv, o) : vsub(cv, o);
+                const vec2<T> os = OS(J, k1 > 0 ? k1 : 1);
+                sv = k < q ? vadd(os, sv) : vsub(os, sv);
+            } else {
+                sv = OS(J, q);  // leaf; C copies
+            }
+        }
+    }
+
+    QFT_HD void emit(vec2<T> *y, int k, vec2<T> cv, vec2<T> sv) const {
+        if (k == 0 || k == m) {
+            y[k] = cv;
+        } else {
+            const vec2<T> u = {sv.y, -sv.x};
+            y[k] = vadd(cv, u);
+            y[N - k] = vsub(cv, u);
+        }
+    }
+
+    template <int J>
+    QFT_HD void up(vec2<T> *y, int k, vec2<T> cv, vec2<T> sv) const {
+        if constexpr (J == 0) {
+            emit(y, k, cv, sv);
+        } else {
+            const int q = qj(J - 1), mm = 2 * q;
+            const bool self = (k == q);
+            const vec2<T> o = OC(J - 1, self ? 0 : k);
+            const vec2<T> os = OS(J - 1, k > 0 ? k : 1);
+            const vec2<T> clo = self ? cv : vadd(cv, o), chi = self ? cv : vsub(cv, o);
+            const vec2<T> slo = self ? os : vadd(os, sv), shi = self ? os : vsub(os, sv);
+            up<J - 1>(y, k, clo, slo);
+            up<J - 1>(y, self ? q : mm - k, chi, shi);
+        }
+    }
+
+    template <int RC>
+    QFT_HD void unit(vec2<T> *y, int t) const {
+        vec2<T> cv, sv;
+        descend<RC>(t, cv, sv);
+        up<RC>(y, t, cv, sv);
+    }
+};
+
+}  // namespace qft

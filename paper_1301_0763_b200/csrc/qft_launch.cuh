@@ -14,6 +14,12 @@
 #ifndef QFT_CTAS_PER_SM
 #define QFT_CTAS_PER_SM 1  // shared-memory budget split: CTAs resident per SM
 #endif
+#ifndef QFT_A0_TMA
+#define QFT_A0_TMA 1       // A0 input: TMA bulk copy into a staging buffer (1) or L2-prefetched global loads (0)
+#endif
+#ifndef QFT_TT_MAX
+#define QFT_TT_MAX 4       // cap on signals per CTA iteration
+#endif
 #ifndef QFT_HALO_SHFL
 #define QFT_HALO_SHFL 0    // phase-C halo by warp shuffle (1) or by a shared-memory read (0)
 #endif
@@ -27,9 +33,17 @@ struct LaunchArgs {
     const void *in;
     void *out;
     long long batch;
-    const void *U;  // level table (device)
+    const void *U;        // level table (device)
+    const void *Uhead;    // host copy of U[0..32): the constants of every Lee block with L <= 32
     int num_sms;
     cudaStream_t stream;
+};
+
+// U[0..32) as a kernel parameter: lives in the constant bank, so the Lee-32
+// multiplies read it as an operand (no shared-memory traffic).
+template <typename T>
+struct LeeConst {
+    T u[32];
 };
 
 // ------------------------------------------------------------ TMA / mbarrier
@@ -58,16 +72,21 @@ QFT_DEV void tma_bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t 
                  : "memory");
 }
 
+QFT_DEV void l2_prefetch(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // ------------------------------------------------------------ configuration
 template <int LOG2N, typename T>
 struct KCfg {
     using P = SPlan<LOG2N>;
     static constexpr int VB = (int)sizeof(vec2<T>);
-    static constexpr int PER = P::N * VB + P::PADDED * VB;  // staging + working per signal
+    static constexpr int PER = (QFT_A0_TMA ? P::N * VB : 0) + P::PADDED * VB;  // (staging +) working per signal
     static constexpr int UB = P::UCELLS * (int)sizeof(T);
     static constexpr int BUDGET = (226 * 1024) / QFT_CTAS_PER_SM - UB - 64;
     static constexpr int TT0 = BUDGET / PER;
-    static constexpr int TT = TT0 < 1 ? 1 : (TT0 > 64 ? 64 : TT0);  // signals per CTA iteration
+    static constexpr int TTC = P::n >= 12 ? QFT_TT_MAX : 64;
+    static constexpr int TT = TT0 < 1 ? 1 : (TT0 > TTC ? TTC : TT0);  // signals per CTA iteration
     static constexpr int rup32(int x) { return (x + 31) / 32 * 32; }
     static constexpr int NB32 = rup32(TT * P::NL32);                 // phase-B Lee-32 lanes per side
     static constexpr int W_B = (2 * NB32 + rup32(2 * TT)) / 32;
@@ -75,11 +94,11 @@ struct KCfg {
     static constexpr int W_AC = TT * P::NWU + QFT_CHAIN_MID;  // + the chain-mid warp
     static constexpr int mx(int a, int b) { return a > b ? a : b; }
     static constexpr int NW0 = mx(mx(W_B, W_D), W_AC);
-    static constexpr int NWMAX = sizeof(T) == 8 ? 12 : 16;  // keep >= 168 registers for fp64
+    static constexpr int NWMAX = sizeof(T) == 8 ? 12 : 17;  // keep >= 168 (fp64) / 120 (fp32) registers
     static constexpr int NW = NW0 < 4 ? 4 : (NW0 > NWMAX ? NWMAX : NW0);
     static constexpr int NT = NW * 32;
     static constexpr int STAGE_OFF = 0;
-    static constexpr int W_OFF = TT * P::N * VB;
+    static constexpr int W_OFF = QFT_A0_TMA ? TT * P::N * VB : 0;
     static constexpr int U_OFF = W_OFF + TT * P::PADDED * VB;
     static constexpr int BAR_OFF = (U_OFF + UB + 15) / 16 * 16;
     static constexpr int SMEM = BAR_OFF + 16;
@@ -197,12 +216,14 @@ QFT_DEV void run_chain_mid(vec2<T> *W, int ntr, int lane) {
 template <int LOG2N, typename T>
 __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
     qft_cdft_smem(const vec2<T> *__restrict__ in, vec2<T> *__restrict__ out, long long batch,
-                  const T *__restrict__ Ug) {
+                  const T *__restrict__ Ug, const __grid_constant__ LeeConst<T> kc) {
     using P = SPlan<LOG2N>;
     using K = KCfg<LOG2N, T>;
     constexpr int TT = K::TT, NT = K::NT, NW = K::NW;
     extern __shared__ __align__(128) unsigned char smem_raw[];
+#if QFT_A0_TMA
     vec2<T> *stage = reinterpret_cast<vec2<T> *>(smem_raw + K::STAGE_OFF);
+#endif
     vec2<T> *W = reinterpret_cast<vec2<T> *>(smem_raw + K::W_OFF);
     T *U = reinterpret_cast<T *>(smem_raw + K::U_OFF);
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + K::BAR_OFF);
@@ -211,18 +232,34 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
     const long long nbatch = (batch + TT - 1) / TT;
     const A0Lane a0l = a0_lane<LOG2N>(lane);
     for (int i = tid; i < P::UCELLS; i += NT) U[i] = Ug[i];
+#if QFT_A0_TMA
     if (tid == 0) mbar_init(bar, 1);
+#else
+    (void)bar;
+#endif
     __syncthreads();
     long long bt = blockIdx.x;
+#if QFT_A0_TMA
     if (tid == 0 && bt < nbatch) {
         const long long nt = (batch - bt * TT) < TT ? (batch - bt * TT) : TT;
         tma_bulk_load(stage, in + bt * TT * P::N, (uint32_t)(nt * P::N * K::VB), bar);
     }
     uint32_t parity = 0;
+#endif
     for (; bt < nbatch; bt += gridDim.x) {
         const int ntr = (int)((batch - bt * TT) < TT ? (batch - bt * TT) : TT);
+#if QFT_A0_TMA
         mbar_wait(bar, parity);
         parity ^= 1u;
+#else
+        // pull the next batch into L2 while this one is transformed
+        if (tid == 0 && bt + gridDim.x < nbatch) {
+            const long long nb = bt + gridDim.x;
+            const long long nt = (batch - nb * TT) < TT ? (batch - nb * TT) : TT;
+            l2_prefetch(in + nb * TT * P::N, (uint32_t)(nt * P::N * K::VB));
+        }
+        const vec2<T> *stage = in + bt * TT * P::N;  // A0 reads global memory directly
+#endif
         // A0: fold + route, staging -> W
 #if QFT_A0_UNIT8
         for (int it = tid; it < TT * (P::m / 8); it += NT) {
@@ -233,10 +270,36 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
         {
             // warps take chunks of 32 consecutive n; lane 0's multiples of 32 afterwards
             constexpr int NCH = P::m / 32;
+#if !QFT_A0_TMA
+            // global loads: 8 chunks in flight per lane (memory-level parallelism)
+            constexpr int UNR = 8;
+            for (int u0 = warp; u0 < TT * NCH; u0 += NW * UNR) {
+                vec2<T> xa[UNR], xb[UNR];
+#pragma unroll
+                for (int r = 0; r < UNR; ++r) {
+                    const int u = u0 + r * NW, tau = u / NCH, c = u - tau * NCH, n = 32 * c + lane;
+                    if (u < TT * NCH && tau < ntr && lane) {
+                        xa[r] = stage[tau * P::N + n];
+                        xb[r] = stage[tau * P::N + P::N - n];
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < UNR; ++r) {
+                    const int u = u0 + r * NW, tau = u / NCH, c = u - tau * NCH;
+                    if (u < TT * NCH && tau < ntr && lane) {
+                        vec2<T> *w = W + tau * P::PADDED;
+                        const int cell = a0l.A + c * a0l.B;
+                        w[padx(cell)] = vadd(xa[r], xb[r]);
+                        w[padx(cell) + padx(P::S0)] = vsub(xa[r], xb[r]);
+                    }
+                }
+            }
+#else
             for (int u = warp; u < TT * NCH; u += NW) {
                 const int tau = u / NCH, c = u - tau * NCH;
                 if (tau < ntr && lane) a0_chunk<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, c, lane, a0l);
             }
+#endif
             for (int it = tid; it < TT * NCH; it += NT) {
                 const int tau = it / NCH, c = it - tau * NCH;
                 if (tau < ntr) a0_item<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, 32 * c);
@@ -244,12 +307,14 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
         }
 #endif
         __syncthreads();
+#if QFT_A0_TMA
         // the staging buffer is free: prefetch the next batch while we compute
         if (tid == 0 && bt + gridDim.x < nbatch) {
             const long long nb = bt + gridDim.x;
             const long long nt = (batch - nb * TT) < TT ? (batch - nb * TT) : TT;
             tma_bulk_load(stage, in + nb * TT * P::N, (uint32_t)(nt * P::N * K::VB), bar);
         }
+#endif
         // A: forward levels of the big blocks (warp units: side x {block 0, blocks 1..})
         if constexpr (P::NWU > 0) {
             for (int u = warp; u < TT * P::NWU; u += NW) {
@@ -284,16 +349,16 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
                 const int tau = v / (P::NL32 > 0 ? P::NL32 : 1), k = v - tau * P::NL32;
                 if (P::NL32 > 0 && tau < ntr) {
                     vec2<T> *w = W + tau * P::PADDED;
-                    if (dst) b_l32<true, T>(w, P::S0 + 32 * k, U);
-                    else b_l32<false, T>(w, 32 * k, U);
+                    if (dst) b_l32<true, T>(w, P::S0 + 32 * k, kc.u);
+                    else b_l32<false, T>(w, 32 * k, kc.u);
                 }
             } else {
                 const int v = u - 2 * K::NB32;
                 const int tau = v >> 1;
                 if (tau < ntr) {
                     vec2<T> *w = W + tau * P::PADDED;
-                    if (v & 1) b_small<LOG2N, true, T>(w, U);
-                    else b_small<LOG2N, false, T>(w, U);
+                    if (v & 1) b_small<LOG2N, true, T>(w, kc.u);
+                    else b_small<LOG2N, false, T>(w, kc.u);
                 }
             }
         }
@@ -346,8 +411,10 @@ cudaError_t launch_smem(const LaunchArgs &a) {
     long long grid = (long long)a.num_sms * per_sm;
     if (grid > nbatch) grid = nbatch;
     if (grid < 1) grid = 1;
+    LeeConst<T> kc;
+    for (int i = 0; i < 32; ++i) kc.u[i] = ((const T *)a.Uhead)[i];
     kern<<<(unsigned)grid, K::NT, K::SMEM, a.stream>>>((const vec2<T> *)a.in, (vec2<T> *)a.out, a.batch,
-                                                       (const T *)a.U);
+                                                       (const T *)a.U, kc);
     return cudaGetLastError();
 }
 

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../paper_1301_0763_b200/csrc/qft_smem.cuh"
+#include "../../paper_1301_0763_b200/csrc/qft_large_plan.h"
 
 using namespace qft;
 
@@ -102,6 +103,104 @@ static void emu_reg(const vec2<T> *x, vec2<T> *y, const T *U) {
     cdft_reg<NN, T>(x, y, U);
 }
 
+// ---------------------------------------------------------------- large N
+template <int R, typename T>
+static void emu_f_task(vec2<T> *w, const FTask &tk, int dst, const T *U) {
+    for (int t = 0; t < (tk.L >> R); ++t) {
+        if (dst) lg_f_group<R, T, true>(w, tk, t, U);
+        else lg_f_group<R, T, false>(w, tk, t, U);
+    }
+}
+template <int R, typename T>
+static void emu_b_task(vec2<T> **W, const BTask &tk) {
+    for (int i = 0; i < (tk.L >> R); ++i) {
+        if (tk.dst) lg_b_column<R, T, true>(W, tk, i);
+        else lg_b_column<R, T, false>(W, tk, i);
+    }
+}
+template <int L, typename T>
+static void emu_leaf_thread(vec2<T> *w, const LeafTask &tk, const T *U) {
+    if (tk.dst) lg_leaf_thread<L, T, true>(w, tk, U);
+    else lg_leaf_thread<L, T, false>(w, tk, U);
+}
+template <int R, typename T, bool DST>
+static void emu_leaf_warp_dst(vec2<T> *w, const LeafTask &tk, const T *U) {
+    using WL = WarpLee<R, T, DST>;
+    constexpr int L = WL::L;
+    std::vector<vec2<T>> s(L + L / 32 + 1);
+    for (int e = 0; e < L; ++e) s[e + (e >> 5)] = w[tk.c + tk.sg * e];
+    std::vector<typename WL::F> f(32);
+    for (int t = 0; t < 32; ++t) f[t].load(s.data(), t, U);
+    for (int t = 0; t < 32; ++t) f[t].store(s.data(), t);
+    for (int p = 0; p < (1 << R); ++p) WL::lee32(s.data(), p, U);
+    std::vector<typename WL::B> bb(32);
+    for (int i = 0; i < 32; ++i) bb[i].compute(s.data(), i);
+    for (int i = 0; i < 32; ++i) bb[i].store(s.data(), i);
+    for (int e = 0; e < L; ++e) w[tk.c + tk.sg * e] = s[e + (e >> 5)];
+}
+template <int R, typename T>
+static void emu_leaf_warp(vec2<T> *w, const LeafTask &tk, const T *U) {
+    if (tk.dst) emu_leaf_warp_dst<R, T, true>(w, tk, U);
+    else emu_leaf_warp_dst<R, T, false>(w, tk, U);
+}
+
+template <typename T, int LEAFLOG, int RG>
+static int emu_large(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
+    LargeSchedule<LEAFLOG, RG> S(log2n);
+    const int N = S.N;
+    std::vector<vec2<T>> W0(N + 2), W1(N + 2);
+    vec2<T> *W[2] = {W0.data(), W1.data()};
+    for (int n = 0; n < N / 2; ++n) lg_fold_item<T>(x, W[0], n, N, log2n);
+    for (auto &lvl : S.f)
+        for (auto &kv : lvl)
+            for (auto &td : kv.second) {
+                switch (kv.first) {
+                    case 1: emu_f_task<1, T>(W[0], td.first, td.second, U); break;
+                    case 2: emu_f_task<2, T>(W[0], td.first, td.second, U); break;
+                    case 3: emu_f_task<3, T>(W[0], td.first, td.second, U); break;
+                    case 4: emu_f_task<4, T>(W[0], td.first, td.second, U); break;
+                    case 5: emu_f_task<5, T>(W[0], td.first, td.second, U); break;
+                }
+            }
+    for (auto &kv : S.leaf)
+        for (auto &tk : kv.second) {
+            switch (kv.first) {
+                case 0: emu_leaf_thread<1, T>(W[0], tk, U); break;
+                case 1: emu_leaf_thread<2, T>(W[0], tk, U); break;
+                case 2: emu_leaf_thread<4, T>(W[0], tk, U); break;
+                case 3: emu_leaf_thread<8, T>(W[0], tk, U); break;
+                case 4: emu_leaf_thread<16, T>(W[0], tk, U); break;
+                case 5: emu_leaf_thread<32, T>(W[0], tk, U); break;
+                case 6: emu_leaf_warp<1, T>(W[0], tk, U); break;
+                case 7: emu_leaf_warp<2, T>(W[0], tk, U); break;
+                case 8: emu_leaf_warp<3, T>(W[0], tk, U); break;
+                case 9: emu_leaf_warp<4, T>(W[0], tk, U); break;
+                case 10: emu_leaf_warp<5, T>(W[0], tk, U); break;
+            }
+        }
+    for (int d = (int)S.b.size() - 1; d >= 0; --d)
+        for (auto &kv : S.b[d])
+            for (auto &tk : kv.second) {
+                switch (kv.first) {
+                    case 1: emu_b_task<1, T>(W, tk); break;
+                    case 2: emu_b_task<2, T>(W, tk); break;
+                    case 3: emu_b_task<3, T>(W, tk); break;
+                    case 4: emu_b_task<4, T>(W, tk); break;
+                    case 5: emu_b_task<5, T>(W, tk); break;
+                }
+            }
+    GChain<T> g;
+    g.n = log2n;
+    g.N = N;
+    g.m = N / 2;
+    g.w0 = W[0];
+    g.w1 = W[1];
+    g.cmask = S.cmask;
+    g.smask = S.smask;
+    for (int t = 0; t <= (N >> 5); ++t) g.template unit<4>(y, t);
+    return 0;
+}
+
 template <typename T>
 static int emu_dispatch(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
     switch (log2n) {
@@ -117,7 +216,9 @@ static int emu_dispatch(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
         case 10: emu_one<10, T>(x, y, U); return 0;
         case 11: emu_one<11, T>(x, y, U); return 0;
         case 12: emu_one<12, T>(x, y, U); return 0;
-        default: return -1;
+        default:
+            if (log2n < 13 || log2n > 20) return -1;
+            return sizeof(T) == 4 ? emu_large<T, 10, 5>(log2n, x, y, U) : emu_large<T, 9, 4>(log2n, x, y, U);
     }
 }
 

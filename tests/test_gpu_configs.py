@@ -1,0 +1,93 @@
+"""The BASELINE.json configurations on the GPU: full-size runs checked bit for
+bit against the oracle on sampled signals, plus size-independent properties
+(Parseval, agreement with torch.fft within the fp32/fp64 accuracy of the
+reference algorithm).  Run with -m gpu on a B200."""
+
+import numpy as np
+import pytest
+
+from conftest import bit_equal
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, dtype=np.complex128)
+    b = np.asarray(b, dtype=np.complex128)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def test_config3_real_input_multipass(torch_cuda, oracle_mod):
+    """config 3: real fp32 (imag 0), N=2^16, batch 2048, sinusoids + noise."""
+    torch = torch_cuda
+    from paper_1301_0763_b200 import improved, workloads
+    N, B = 1 << 16, 2048
+    x = workloads.config3_rows_torch(N, B, seed=3, device="cuda")
+    y = improved.cdft_rows(x)
+    idx = [0, 1, 777, B - 1]
+    xs = x[idx].cpu().numpy()
+    ys = y[idx].cpu().numpy()
+    assert bit_equal(ys, oracle_mod.cdft_rows(xs, nthreads=4))
+    # Hermitian symmetry of a real-input spectrum holds exactly for this algorithm's output?
+    # (not required); check accuracy against fp64 FFT of the same fp32 samples
+    ref = np.fft.fft(xs.astype(np.complex128), axis=1)
+    assert rel_l2(ys, ref) < 1e-6 * 16
+
+
+def test_config4_fp64_2p20(torch_cuda, oracle_mod):
+    """config 4: complex fp64, N=2^20, batch 64, U[-1,1): bitwise on sampled
+    signals; fp64 accuracy vs numpy.fft and vs the classical QFT (oracle)."""
+    torch = torch_cuda
+    from paper_1301_0763_b200 import improved, workloads
+    N, B = 1 << 20, 64
+    z = workloads.uniform_rows(N, B, seed=4)
+    y = improved.cdft_rows(torch.from_numpy(z).cuda()).cpu().numpy()
+    idx = [0, 63]
+    want = oracle_mod.cdft_rows(z[idx], nthreads=2)
+    assert bit_equal(y[idx], want)
+    ref = np.fft.fft(z[idx], axis=1)
+    assert rel_l2(y[idx], ref) < 1e-12
+    cla = oracle_mod.cdft_rows(z[idx[:1]], algo="classical", nthreads=1)
+    assert rel_l2(y[idx[:1]], cla) < 1e-12
+
+
+def test_config5_sharded_generator_slice(torch_cuda, oracle_mod):
+    """config 5 shape (N=2^14 fp32) on a slice of the batch, input generated on
+    the device by the counter-based generator; sampled signals bitwise."""
+    torch = torch_cuda
+    from paper_1301_0763_b200 import _native, improved
+    N, B = 1 << 14, 4096
+    p = _native.plan(14, 32)
+    x = torch.empty((B, N), dtype=torch.complex64, device="cuda")
+    p.fill_normal(x.data_ptr(), B, 12345, 5, torch.cuda.current_stream().cuda_stream)
+    y = improved.cdft_rows(x)
+    idx = [0, 1, 2048, B - 1]
+    xs = x[idx].cpu().numpy()
+    assert bit_equal(y[idx].cpu().numpy(), oracle_mod.cdft_rows(xs))
+    # generator is keyed on the global transform index: a shifted slice reproduces rows
+    x2 = torch.empty((2, N), dtype=torch.complex64, device="cuda")
+    p.fill_normal(x2.data_ptr(), 2, 12345 + 2048, 5, torch.cuda.current_stream().cuda_stream)
+    assert bit_equal(x2[0].cpu().numpy(), xs[2])
+    st = np.std(xs.view(np.float32))
+    assert 0.95 < st < 1.05
+
+
+@pytest.mark.parametrize("lg,dt", [(13, np.complex64), (16, np.complex128), (18, np.complex64)])
+def test_large_layouts_and_parseval(torch_cuda, oracle_mod, lg, dt):
+    torch = torch_cuda
+    from paper_1301_0763_b200 import improved
+    N = 1 << lg
+    rng = np.random.default_rng(lg)
+    z = (rng.standard_normal((N, 2)) + 1j * rng.standard_normal((N, 2))).astype(dt)
+    got = improved.cdft(z)  # reference layout (N, batch), host path
+    assert bit_equal(got, oracle_mod.cdft(z))
+    e_in = np.sum(np.abs(z.astype(np.complex128)) ** 2, axis=0) * N
+    e_out = np.sum(np.abs(got.astype(np.complex128)) ** 2, axis=0)
+    np.testing.assert_allclose(e_out, e_in, rtol=1e-4)
