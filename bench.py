@@ -38,6 +38,16 @@ SEED = 2
 METRIC = "batched FFT transforms/s (improved QFT, complex fp32, N=2^12)"
 UNIT = "transforms/s"
 
+# --config k selects another BASELINE.json configuration (default: config 2,
+# the headline single-GPU workload).  (log2 N, batch per GPU, precision, kind)
+CONFIG_TABLE = {
+    1: (10, 64, 64, "uniform"),
+    2: (12, 16384, 32, "normal"),
+    3: (16, 2048, 32, "sinusoids"),
+    4: (20, 64, 64, "uniform"),
+    5: (14, 1 << 18, 32, "normal"),  # whole box; per GPU batch = 2^18 / n_gpus (strong)
+}
+
 
 def read_peaks():
     try:
@@ -102,13 +112,15 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline_port(seconds, threads):
+def cpu_baseline_port(seconds, threads, prec=32):
     """Oracle port (scalar C restatement of the reference recursion) on the host."""
     import numpy as np
     from oracle import oracle
     rng = np.random.default_rng(SEED)
-    sample = 512 * max(1, threads)
-    z = (rng.standard_normal((sample, N)) + 1j * rng.standard_normal((sample, N))).astype(np.complex64)
+    per = max(1, min(512, (1 << 21) // N))
+    sample = per * max(1, threads)
+    z = (rng.standard_normal((sample, N)) + 1j * rng.standard_normal((sample, N))).astype(
+        np.complex64 if prec == 32 else np.complex128)
     oracle.cdft_rows(z[: min(sample, 64)], nthreads=threads)  # warm
     done, t0 = 0, time.perf_counter()
     while True:
@@ -134,19 +146,24 @@ def run_reference(args):
     from oracle import oracle
     threads = oracle.max_threads()
     vals = []
+    samples = []
     for i in range(args.warmup + args.steps):
-        v, done, el = cpu_baseline_port(args.ref_seconds, threads)
+        v, done, el = cpu_baseline_port(args.ref_seconds, threads, args.prec)
         if i >= args.warmup:
             vals.append(v)
+            samples.append(done)
     value = sorted(vals)[len(vals) // 2]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * BATCH / value,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "config2: improved-QFT cdft N=2^12 batch 16384 complex64 N(0,1)",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if args.prec == 32 else "f64", "data": "synthetic",
+        "config": {"workload": f"config{args.config}: improved-QFT cdft N=2^{LOG2N} batch {BATCH} "
+                               f"{'complex64' if args.prec == 32 else 'complex128'} {args.kind}",
                    "N": N, "batch": BATCH, "parallelism": "host threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{512 * threads} transforms per repeat, repeated for >= {args.ref_seconds}s per step"},
+                         "sample": f"bounded sample: {samples[0]} transforms of the config's shape per step "
+                                   f"(>= {args.ref_seconds}s of host work), oracle port on {threads} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -154,6 +171,7 @@ def run_reference(args):
 
 
 def main():
+    global LOG2N, N, BATCH, METRIC
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -164,7 +182,14 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=5.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIG_TABLE))
     args = ap.parse_args()
+    lg, bt, prec, kind = CONFIG_TABLE[args.config]
+    LOG2N, N = lg, 1 << lg
+    BATCH = bt
+    ctype = "complex fp32" if prec == 32 else "complex fp64"
+    METRIC = f"batched FFT transforms/s (improved QFT, {ctype}, N=2^{lg})"
+    args.prec, args.kind = prec, kind
     if args.impl == "reference":
         return run_reference(args)
 
@@ -181,12 +206,27 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    B = args.batch
-    plan = _native.plan(LOG2N, 32, 0, local)
-    x = torch.empty((B, N), dtype=torch.complex64, device=dev)
-    y = torch.empty_like(x)
+    B = args.batch if args.config == 2 or args.batch != 16384 else BATCH
+    scaling = "weak"
+    if args.config == 5:  # the box-wide batch 2^18 is split evenly (no collective)
+        B = BATCH // ws
+        scaling = "strong"
+    prec = args.prec
+    cdt = torch.complex64 if prec == 32 else torch.complex128
+    esz = 8 if prec == 32 else 16
+    plan = _native.plan(LOG2N, prec, 0, local)
     stream = torch.cuda.current_stream(dev)
-    plan.fill_normal(x.data_ptr(), B, rank * B, SEED, stream.cuda_stream)
+    if args.kind == "sinusoids":
+        from paper_1301_0763_b200 import workloads
+        x = workloads.config3_rows_torch(N, B, SEED + rank, dev)
+    else:
+        x = torch.empty((B, N), dtype=cdt, device=dev)
+        if args.kind == "uniform":
+            from paper_1301_0763_b200 import workloads
+            x.copy_(torch.from_numpy(workloads.uniform_rows(N, B, SEED + rank, np.complex64 if prec == 32 else np.complex128)))
+        else:
+            plan.fill_normal(x.data_ptr(), B, rank * B, SEED, stream.cuda_stream)
+    y = torch.empty_like(x)
 
     def step():
         plan.exec_device(x.data_ptr(), y.data_ptr(), B, (N, 1), (N, 1), stream.cuda_stream)
@@ -217,8 +257,8 @@ def main():
     # e2e: the C-ABI host call with pinned host buffers (H2D + transform + D2H)
     e2e = None
     if not args.no_e2e:
-        hb = min(B, 16384)
-        hin = torch.empty((hb, N), dtype=torch.complex64, pin_memory=True)
+        hb = min(B, max(1, (1 << 30) // (N * esz)))
+        hin = torch.empty((hb, N), dtype=cdt, pin_memory=True)
         hout = torch.empty_like(hin, pin_memory=True)
         hin.copy_(x[:hb].cpu())
         for _ in range(2):
@@ -234,42 +274,44 @@ def main():
             t = torch.tensor([el], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        e2e = {"value": ws * hb / el, "unit": UNIT, "h2d_bytes_per_step": hb * N * 8,
-               "d2h_bytes_per_step": hb * N * 8, "ms_per_step": el * 1000.0, "batch_per_step": hb,
+        e2e = {"value": ws * hb / el, "unit": UNIT, "h2d_bytes_per_step": hb * N * esz,
+               "d2h_bytes_per_step": hb * N * esz, "ms_per_step": el * 1000.0, "batch_per_step": hb,
                "path": "qft_exec_cdft_host (pinned host buffers, 2-stream chunked pipeline)"}
 
     # parity spot check of this run's own data (sampled rows vs the oracle)
     parity = None
     if rank == 0:
         from oracle import oracle
-        idx = [0, B // 2, B - 1]
+        idx = [0, B // 2, B - 1] if N <= 1 << 16 else [0, B - 1]
         zs = x[idx].cpu().numpy()
         ys = y[idx].cpu().numpy()
-        parity = bool(np.array_equal(ys.view(np.uint8), oracle.cdft_rows(zs).view(np.uint8)))
+        parity = bool(np.array_equal(ys.view(np.uint8), oracle.cdft_rows(zs, nthreads=2).view(np.uint8)))
 
     if rank == 0:
         peak, peak_kind = read_peaks()
-        algo_bytes = 16 * N * B
+        algo_bytes = 2 * esz * N * B
         achieved = algo_bytes / (ms / 1000.0) / 1e9
         cpu = None
         if not args.no_cpu:
             from oracle import oracle
             thr = 1
-            v, done, el = cpu_baseline_port(args.cpu_seconds, thr)
+            v, done, el = cpu_baseline_port(args.cpu_seconds, thr, prec)
             cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "port",
-                   "sample": f"{done} transforms of config 2 (N=2^12 complex64) in {el:.1f}s, 1 thread"}
+                   "sample": f"{done} transforms of config {args.config} shape (N=2^{LOG2N}) in {el:.1f}s, 1 thread"}
         info = plan.info()
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "config2: improved-QFT cdft N=2^12 batch 16384/GPU complex64 N(0,1)",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f32" if prec == 32 else "f64", "data": "synthetic",
+            "config": {"workload": f"config{args.config}: improved-QFT cdft N=2^{LOG2N} batch {B}/GPU "
+                                   f"{'complex64' if prec == 32 else 'complex128'} {args.kind}",
                        "N": N, "batch_per_gpu": B, "parallelism": f"batch-sharded x{ws}, no collective",
-                       "l2": "input 1 GiB/GPU > 126 MB L2 (no flush needed)"},
+                       "l2": ("input > 126 MB L2 (no flush needed)" if B * N * esz > (126 << 20)
+                              else "input fits L2: steps re-read a warm L2 (small config)")},
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                         "algorithmic_bytes_per_transform": 16 * N, "passes": info.passes},
+                         "algorithmic_bytes_per_transform": 2 * esz * N, "passes": info.passes},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": args.steps * info.kernel_launches,
