@@ -49,6 +49,22 @@ CONFIG_TABLE = {
 }
 
 
+def read_traffic(config):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    (profiles/r*_summary.json), or None."""
+    import glob
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_summary.json"))):
+        try:
+            with open(f) as fh:
+                d = json.load(fh).get(f"config{config}")
+            if d and d.get("traffic_bytes_per_launch"):
+                best = d
+        except Exception:
+            pass
+    return best
+
+
 def read_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -310,7 +326,10 @@ def main():
                               else "input fits L2: steps re-read a warm L2 (small config)")},
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / peak, "peak_kind": peak_kind,
+                         "traffic": (lambda d: None if not d or B != BATCH else
+                                     d["traffic_bytes_per_launch"] / (ms / 1000.0) / 1e9)(read_traffic(args.config)),
+                         "traffic_unit": "GB/s of measured DRAM bytes (ncu, committed under profiles/) at this launch time",
                          "algorithmic_bytes_per_transform": 2 * esz * N, "passes": info.passes},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),

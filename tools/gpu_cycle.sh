@@ -1,6 +1,6 @@
 #!/bin/bash
 # one GPU cycle: parity tests, bench, then ncu of the smem kernel (only if the plain run exited 0)
-# usage (inside gpurun): bash tools_gpu_cycle.sh <tag> [extra bench args]
+# usage (inside gpurun): bash tools/gpu_cycle.sh <tag> [extra bench args]
 tag=${1:-x}; shift
 export PYTHONUNBUFFERED=1
 timeout 500 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_gpu.log
