@@ -224,8 +224,11 @@ def main():
     torch.cuda.set_device(dev)
     B = args.batch if args.config == 2 or args.batch != 16384 else BATCH
     scaling = "weak"
+    first = rank * B  # global index of this rank's first signal (generator key)
     if args.config == 5:  # the box-wide batch 2^18 is split evenly (no collective)
-        B = BATCH // ws
+        from paper_1301_0763_b200.sharding import shard_bounds
+        b0, b1 = shard_bounds(BATCH, ws, rank)
+        B, first = b1 - b0, b0
         scaling = "strong"
     prec = args.prec
     cdt = torch.complex64 if prec == 32 else torch.complex128
@@ -241,7 +244,7 @@ def main():
             from paper_1301_0763_b200 import workloads
             x.copy_(torch.from_numpy(workloads.uniform_rows(N, B, SEED + rank, np.complex64 if prec == 32 else np.complex128)))
         else:
-            plan.fill_normal(x.data_ptr(), B, rank * B, SEED, stream.cuda_stream)
+            plan.fill_normal(x.data_ptr(), B, first, SEED, stream.cuda_stream)
     y = torch.empty_like(x)
 
     def step():
