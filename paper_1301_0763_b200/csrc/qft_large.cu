@@ -36,6 +36,7 @@ constexpr int kLeafLog = QFT_LARGE_PREC == 32 ? 10 : 9;  // warp leaf: L <= 1024
 constexpr int kRG = QFT_LARGE_PREC == 32 ? 5 : 4;         // fold levels per F/B pass
 constexpr int kRC = 4;                                    // chain levels unfolded per thread
 constexpr int kChunk = 256;
+constexpr int kBChunk = 128;  // columns per CTA of a backward pass (outputs staged in shared memory)
 
 template <typename T>
 struct LeeConstL {
@@ -82,48 +83,68 @@ __global__ void lg_fold_kernel(const vec2<T> *__restrict__ x, vec2<T> *__restric
 
 template <int R, typename T>
 __global__ void lg_f_kernel(vec2<T> *__restrict__ W0, const FTask *__restrict__ tasks, const int *__restrict__ dsts,
-                            const Chunk *__restrict__ chunks, const T *__restrict__ U, long long batch, long long Ws) {
+                            const Chunk *__restrict__ chunks, const T *__restrict__ U, long long batch, long long Ws,
+                            const vec2<T> *__restrict__ x, int N) {
     const Chunk ch = chunks[blockIdx.x];
     const FTask tk = tasks[ch.task];
     const int t = ch.t0 + threadIdx.x;
     if (t >= (tk.L >> R)) return;
     const bool dst = dsts[ch.task];
     for (long long b = blockIdx.y; b < batch; b += gridDim.y) {
-        if (dst) lg_f_group<R, T, true>(W0 + b * Ws, tk, t, U);
-        else lg_f_group<R, T, false>(W0 + b * Ws, tk, t, U);
+        if (dst) lg_f_group<R, T, true>(W0 + b * Ws, tk, t, U, x + b * N, N);
+        else lg_f_group<R, T, false>(W0 + b * Ws, tk, t, U, x + b * N, N);
     }
 }
 
 template <int R, typename T>
-__global__ void lg_b_kernel(vec2<T> *W0, vec2<T> *W1, const BTask *__restrict__ tasks, const Chunk *__restrict__ chunks,
-                            long long batch, long long Ws) {
+__global__ void __launch_bounds__(kBChunk) lg_b_kernel(vec2<T> *W0, vec2<T> *W1, const BTask *__restrict__ tasks,
+                                                      const Chunk *__restrict__ chunks, long long batch, long long Ws) {
+    constexpr int G = 1 << R, CELLS = kBChunk * G;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    vec2<T> *stg = reinterpret_cast<vec2<T> *>(smem_raw);  // padded: cell p at p + p/32
     const Chunk ch = chunks[blockIdx.x];
     const BTask tk = tasks[ch.task];
     const int i = ch.t0 + threadIdx.x;
-    if (i >= (tk.L >> R)) return;
+    const int ncols = min(kBChunk, (tk.L >> R) - ch.t0);
     for (long long b = blockIdx.y; b < batch; b += gridDim.y) {
         vec2<T> *W[2] = {W0 + b * Ws, W1 + b * Ws};
-        if (tk.dst) lg_b_column<R, T, true>(W, tk, i);
-        else lg_b_column<R, T, false>(W, tk, i);
+        if (threadIdx.x < ncols) {
+            vec2<T> out[G];
+            if (tk.dst) lg_b_column_out<R, T, true>(W, tk, i, out);
+            else lg_b_column_out<R, T, false>(W, tk, i, out);
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
+                const int p = threadIdx.x * G + q;
+                stg[p + (p >> 5)] = out[q];
+            }
+        }
+        __syncthreads();
+        // the chunk's outputs are the contiguous cells [out0 + t0*G, out0 + (t0+ncols)*G)
+        vec2<T> *dst = W[tk.out_buf] + tk.out0 + ch.t0 * G;
+        for (int p = threadIdx.x; p < ncols * G; p += kBChunk) dst[p] = stg[p + (p >> 5)];
+        __syncthreads();
+        (void)CELLS;
     }
 }
 
 template <int L, typename T>
 __global__ void lg_leaf_thread_kernel(vec2<T> *W0, const LeafTask *__restrict__ tasks, int ntasks, long long batch,
-                                      long long Ws, const __grid_constant__ LeeConstL<T> kc) {
+                                      long long Ws, const __grid_constant__ LeeConstL<T> kc,
+                                      const vec2<T> *__restrict__ x, int N) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= ntasks) return;
     const LeafTask tk = tasks[k];
     for (long long b = blockIdx.y; b < batch; b += gridDim.y) {
-        if (tk.dst) lg_leaf_thread<L, T, true>(W0 + b * Ws, tk, kc.u);
-        else lg_leaf_thread<L, T, false>(W0 + b * Ws, tk, kc.u);
+        if (tk.dst) lg_leaf_thread<L, T, true>(W0 + b * Ws, tk, kc.u, x + b * N, N);
+        else lg_leaf_thread<L, T, false>(W0 + b * Ws, tk, kc.u, x + b * N, N);
     }
 }
 
 template <int R, typename T>
 __global__ void __launch_bounds__(128) lg_leaf_warp_kernel(vec2<T> *W0, const LeafTask *__restrict__ tasks, int ntasks,
                                                            long long batch, long long Ws, const T *__restrict__ U,
-                                                           const __grid_constant__ LeeConstL<T> kc) {
+                                                           const __grid_constant__ LeeConstL<T> kc,
+                                                           const vec2<T> *__restrict__ x, int N) {
     constexpr int L = 32 << R, PADL = L + L / 32 + 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -133,7 +154,15 @@ __global__ void __launch_bounds__(128) lg_leaf_warp_kernel(vec2<T> *W0, const Le
     const LeafTask tk = tasks[k];
     for (long long b = blockIdx.y; b < batch; b += gridDim.y) {
         vec2<T> *w = W0 + b * Ws;
-        for (int e = lane; e < L; e += 32) s[e + (e >> 5)] = w[tk.c + tk.sg * e];
+        if (tk.j >= 0) {
+            const vec2<T> *xb = x + b * N;
+#pragma unroll 4
+            for (int e = lane; e < L; e += 32)
+                s[e + (e >> 5)] = tk.dst ? fold_load<T, true>(xb, N, tk.j, e) : fold_load<T, false>(xb, N, tk.j, e);
+        } else {
+#pragma unroll 8
+            for (int e = lane; e < L; e += 32) s[e + (e >> 5)] = w[tk.c + tk.sg * e];
+        }
         __syncwarp();
         if (tk.dst) {
             using WL = WarpLee<R, T, true>;
@@ -168,19 +197,20 @@ __global__ void __launch_bounds__(128) lg_leaf_warp_kernel(vec2<T> *W0, const Le
     }
 }
 
-template <typename T>
-__global__ void lg_chain_kernel(const vec2<T> *W0, const vec2<T> *W1, vec2<T> *__restrict__ y, int log2n,
-                                uint32_t cmask, uint32_t smask, long long batch, long long Ws) {
-    const int N = 1 << log2n;
+template <typename T, int LOG2N>
+__global__ void lg_chain_kernel(const vec2<T> *W0, const vec2<T> *W1, const vec2<T> *__restrict__ x,
+                                vec2<T> *__restrict__ y, uint32_t cmask, uint32_t smask, long long batch, long long Ws) {
+    constexpr int N = 1 << LOG2N;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t > (N >> (kRC + 1))) return;
     for (long long b = blockIdx.y; b < batch; b += gridDim.y) {
         GChain<T> g;
-        g.n = log2n;
+        g.n = LOG2N;
         g.N = N;
         g.m = N / 2;
         g.w0 = W0 + b * Ws;
         g.w1 = W1 + b * Ws;
+        g.x = x + (long long)b * N;
         g.cmask = cmask;
         g.smask = smask;
         g.template unit<kRC>(y + b * N, t);
@@ -228,7 +258,7 @@ int QFT_LG(qft_large_create)(int log2n, void **out) {
             std::vector<Chunk> ch;
             for (size_t i = 0; i < kv.second.size(); ++i) {
                 const int cols = kv.second[i].L >> kv.first;
-                for (int t0 = 0; t0 < cols; t0 += kChunk) ch.push_back({(int)i, t0});
+                for (int t0 = 0; t0 < cols; t0 += kBChunk) ch.push_back({(int)i, t0});
             }
             ts.ntasks = (int)kv.second.size();
             ts.nchunks = (int)ch.size();
@@ -289,9 +319,6 @@ int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long ba
     memcpy(kc.u, uhead, sizeof(kc.u));
     const unsigned yb = ybatch(batch);
     cudaError_t e;
-    // fold + route
-    e = launch(lg_fold_kernel<T>, dim3((S.m + 255) / 256, yb), dim3(256), 0, st, x, W0, S.N, S.n, batch, Ws);
-    if (e) return (int)e;
     // forward passes
     for (auto &v : p->fset)
         for (auto &ts : v) {
@@ -300,12 +327,12 @@ int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long ba
             const FTask *tk = (const FTask *)ts.d_tasks;
             const Chunk *ch = (const Chunk *)ts.d_chunks;
             switch (ts.R) {
-                case 1: e = launch(lg_f_kernel<1, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws); break;
-                case 2: e = launch(lg_f_kernel<2, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws); break;
-                case 3: e = launch(lg_f_kernel<3, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws); break;
-                case 4: e = launch(lg_f_kernel<4, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws); break;
+                case 1: e = launch(lg_f_kernel<1, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws, x, S.N); break;
+                case 2: e = launch(lg_f_kernel<2, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws, x, S.N); break;
+                case 3: e = launch(lg_f_kernel<3, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws, x, S.N); break;
+                case 4: e = launch(lg_f_kernel<4, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws, x, S.N); break;
 #if QFT_LARGE_PREC == 32
-                case 5: e = launch(lg_f_kernel<5, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws); break;
+                case 5: e = launch(lg_f_kernel<5, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws, x, S.N); break;
 #endif
                 default: return (int)cudaErrorInvalidValue;
             }
@@ -318,43 +345,44 @@ int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long ba
         if (lg <= 5) {
             dim3 g((ts.ntasks + 127) / 128, yb);
             switch (lg) {
-                case 0: e = launch(lg_leaf_thread_kernel<1, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc); break;
-                case 1: e = launch(lg_leaf_thread_kernel<2, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc); break;
-                case 2: e = launch(lg_leaf_thread_kernel<4, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc); break;
-                case 3: e = launch(lg_leaf_thread_kernel<8, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc); break;
-                case 4: e = launch(lg_leaf_thread_kernel<16, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc); break;
-                case 5: e = launch(lg_leaf_thread_kernel<32, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc); break;
+                case 0: e = launch(lg_leaf_thread_kernel<1, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc, x, S.N); break;
+                case 1: e = launch(lg_leaf_thread_kernel<2, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc, x, S.N); break;
+                case 2: e = launch(lg_leaf_thread_kernel<4, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc, x, S.N); break;
+                case 3: e = launch(lg_leaf_thread_kernel<8, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc, x, S.N); break;
+                case 4: e = launch(lg_leaf_thread_kernel<16, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc, x, S.N); break;
+                case 5: e = launch(lg_leaf_thread_kernel<32, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc, x, S.N); break;
             }
         } else {
             const int R = lg - 5, L = 32 << R;
             const size_t smem = 4 * (size_t)(L + L / 32 + 1) * sizeof(vec2<T>);
             dim3 g((ts.ntasks + 3) / 4, yb);
             switch (R) {
-                case 1: e = launch(lg_leaf_warp_kernel<1, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc); break;
-                case 2: e = launch(lg_leaf_warp_kernel<2, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc); break;
-                case 3: e = launch(lg_leaf_warp_kernel<3, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc); break;
-                case 4: e = launch(lg_leaf_warp_kernel<4, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc); break;
+                case 1: e = launch(lg_leaf_warp_kernel<1, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc, x, S.N); break;
+                case 2: e = launch(lg_leaf_warp_kernel<2, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc, x, S.N); break;
+                case 3: e = launch(lg_leaf_warp_kernel<3, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc, x, S.N); break;
+                case 4: e = launch(lg_leaf_warp_kernel<4, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc, x, S.N); break;
 #if QFT_LARGE_PREC == 32
-                case 5: e = launch(lg_leaf_warp_kernel<5, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc); break;
+                case 5: e = launch(lg_leaf_warp_kernel<5, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc, x, S.N); break;
 #endif
                 default: return (int)cudaErrorInvalidValue;
             }
         }
         if (e) return (int)e;
     }
-    // backward passes, deepest first
+    // backward passes, deepest first (outputs staged in shared memory: G*128 cells)
+    auto bsm = [](int R) { const int c = kBChunk << R; return (size_t)(c + c / 32 + 1) * sizeof(vec2<T>); };
     for (int d = (int)p->bset.size() - 1; d >= 0; --d)
         for (auto &ts : p->bset[d]) {
             dim3 g(ts.nchunks, yb);
             const BTask *tk = (const BTask *)ts.d_tasks;
             const Chunk *ch = (const Chunk *)ts.d_chunks;
             switch (ts.R) {
-                case 1: e = launch(lg_b_kernel<1, T>, g, dim3(kChunk), 0, st, W0, W1, tk, ch, batch, Ws); break;
-                case 2: e = launch(lg_b_kernel<2, T>, g, dim3(kChunk), 0, st, W0, W1, tk, ch, batch, Ws); break;
-                case 3: e = launch(lg_b_kernel<3, T>, g, dim3(kChunk), 0, st, W0, W1, tk, ch, batch, Ws); break;
-                case 4: e = launch(lg_b_kernel<4, T>, g, dim3(kChunk), 0, st, W0, W1, tk, ch, batch, Ws); break;
+                case 1: e = launch(lg_b_kernel<1, T>, g, dim3(kBChunk), bsm(1), st, W0, W1, tk, ch, batch, Ws); break;
+                case 2: e = launch(lg_b_kernel<2, T>, g, dim3(kBChunk), bsm(2), st, W0, W1, tk, ch, batch, Ws); break;
+                case 3: e = launch(lg_b_kernel<3, T>, g, dim3(kBChunk), bsm(3), st, W0, W1, tk, ch, batch, Ws); break;
+                case 4: e = launch(lg_b_kernel<4, T>, g, dim3(kBChunk), bsm(4), st, W0, W1, tk, ch, batch, Ws); break;
 #if QFT_LARGE_PREC == 32
-                case 5: e = launch(lg_b_kernel<5, T>, g, dim3(kChunk), 0, st, W0, W1, tk, ch, batch, Ws); break;
+                case 5: e = launch(lg_b_kernel<5, T>, g, dim3(kBChunk), bsm(5), st, W0, W1, tk, ch, batch, Ws); break;
 #endif
                 default: return (int)cudaErrorInvalidValue;
             }
@@ -362,8 +390,14 @@ int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long ba
         }
     // chain + recombination
     const int threads = (S.N >> (kRC + 1)) + 1;
-    e = launch(lg_chain_kernel<T>, dim3((threads + 127) / 128, yb), dim3(128), 0, st, (const vec2<T> *)W0,
-               (const vec2<T> *)W1, y, S.n, S.cmask, S.smask, batch, Ws);
+    const dim3 cg((threads + 127) / 128, yb), cb(128);
+    const vec2<T> *w0 = W0, *w1 = W1;
+    switch (S.n) {
+#define QFT_CH(LG) case LG: e = launch(lg_chain_kernel<T, LG>, cg, cb, 0, st, w0, w1, x, y, S.cmask, S.smask, batch, Ws); break;
+        QFT_CH(13) QFT_CH(14) QFT_CH(15) QFT_CH(16) QFT_CH(17) QFT_CH(18) QFT_CH(19) QFT_CH(20)
+#undef QFT_CH
+        default: return (int)cudaErrorInvalidValue;
+    }
     return (int)e;
 }
 

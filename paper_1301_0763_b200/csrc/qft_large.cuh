@@ -24,10 +24,21 @@ namespace qft {
 // ----------------------------------------------------------------- tasks
 struct FTask {        // r forward levels of one run (in place)
     int c, sg, L;     // run: element e at cell c + sg*e
+    int j;            // >= 0: the run is all of Lee block j -> fold x on load (no fold pass)
 };
 struct LeafTask {     // full Lee of one run (in place, spectrum along the run)
     int c, sg, L, dst;
+    int j;            // >= 0: all of Lee block j -> fold x on load
 };
+
+// element i of Lee block j read straight from the input: sample n = 2^j (2i+1),
+// dc = x[n] + x[N-n], ds = x[n] - x[N-n] (shared.py:28-35)
+template <typename T, bool DST>
+QFT_HD vec2<T> fold_load(const vec2<T> *x, int N, int j, int i) {
+    const int n = (2 * i + 1) << j;
+    const vec2<T> a = x[n], b = x[N - n];
+    return DST ? vsub(a, b) : vadd(a, b);
+}
 struct BTask {        // r backward levels: 2^r sub-block spectra -> natural block spectrum
     int c, sg, L;     // parent run (its sub-blocks are the runs of run_of(r, L, p))
     int in_buf, leaf; // sub-block spectra in W[in_buf]; leaf: along each run, else forward at its min cell
@@ -82,7 +93,7 @@ QFT_HD void lg_fold_item(const vec2<T> *x, vec2<T> *w, int n, int N, int log2n) 
 
 // ----------------------------------------------------------------- F pass
 template <int R, typename T, bool DST>
-QFT_HD void lg_f_group(vec2<T> *w, const FTask &tk, int t, const T *U) {
+QFT_HD void lg_f_group(vec2<T> *w, const FTask &tk, int t, const T *U, const vec2<T> *x = nullptr, int N = 0) {
     constexpr int G = 1 << R;
     vec2<T> v[G];
     int pos[G];
@@ -91,7 +102,7 @@ QFT_HD void lg_f_group(vec2<T> *w, const FTask &tk, int t, const T *U) {
         int c, sg;
         run_of(R, tk.L, s, c, sg);
         pos[s] = tk.c + tk.sg * (c + sg * t);
-        v[s] = w[pos[s]];
+        v[s] = tk.j >= 0 ? fold_load<T, DST>(x, N, tk.j, c + sg * t) : w[pos[s]];
     }
     lee_fwd_rt<R, T, DST>(v, t, tk.L, U);
 #pragma unroll
@@ -100,7 +111,7 @@ QFT_HD void lg_f_group(vec2<T> *w, const FTask &tk, int t, const T *U) {
 
 // ----------------------------------------------------------------- B pass
 template <int R, typename T, bool DST>
-QFT_HD void lg_b_column(vec2<T> *const *W, const BTask &tk, int i) {
+QFT_HD void lg_b_column_out(vec2<T> *const *W, const BTask &tk, int i, vec2<T> *out) {
     constexpr int G = 1 << R;
     const int S = tk.L >> R;
     const vec2<T> *src = W[tk.in_buf];
@@ -123,9 +134,14 @@ QFT_HD void lg_b_column(vec2<T> *const *W, const BTask &tk, int i) {
         hal[p] = src[st + dir * ih];
     }
     auto halo = [&](int p) { return hal[p]; };
-    vec2<T> out[G];
     const bool edge = DST ? (i == 0) : (i == S - 1);
     lee_bwd_fn<R, DST, T>(own, 0, halo, edge, out);
+}
+template <int R, typename T, bool DST>
+QFT_HD void lg_b_column(vec2<T> *const *W, const BTask &tk, int i) {
+    constexpr int G = 1 << R;
+    vec2<T> out[G];
+    lg_b_column_out<R, T, DST>(W, tk, i, out);
     vec2<T> *dst = W[tk.out_buf] + tk.out0 + i * G;
 #pragma unroll
     for (int s = 0; s < G; ++s) dst[s] = out[s];
@@ -133,10 +149,10 @@ QFT_HD void lg_b_column(vec2<T> *const *W, const BTask &tk, int i) {
 
 // ----------------------------------------------------------------- leaf (thread)
 template <int L, typename T, bool DST>
-QFT_HD void lg_leaf_thread(vec2<T> *w, const LeafTask &tk, const T *U) {
+QFT_HD void lg_leaf_thread(vec2<T> *w, const LeafTask &tk, const T *U, const vec2<T> *x = nullptr, int N = 0) {
     vec2<T> v[L];
 #pragma unroll
-    for (int e = 0; e < L; ++e) v[e] = w[tk.c + tk.sg * e];
+    for (int e = 0; e < L; ++e) v[e] = tk.j >= 0 ? fold_load<T, DST>(x, N, tk.j, e) : w[tk.c + tk.sg * e];
     lee_full<L, DST, T>(v, U);
 #pragma unroll
     for (int e = 0; e < L; ++e) w[tk.c + tk.sg * e] = v[e];
@@ -201,7 +217,8 @@ struct WarpLee {
 // Duplicate slots (self-paired indices) write identical values twice.
 template <typename T>
 struct GChain {
-    const vec2<T> *w0, *w1;  // scratch buffers (base pair s(0), s(m) in W0)
+    const vec2<T> *w0, *w1;  // scratch buffers
+    const vec2<T> *x;        // the input signal: base pair s(0) = x[0], s(m) = x[m]
     uint32_t cmask, smask;   // bit j: the cosine / sine spectrum of block j is in W1
     int n, N, m;
 
@@ -221,10 +238,11 @@ struct GChain {
             return r < P - r ? r : P - r;
         };
         {
-            const vec2<T> s0 = w0[N - 1], sm = w0[N];
+            const vec2<T> s0 = x[0], sm = x[m];
             cv = kk(n - 1) == 0 ? vadd(s0, sm) : vsub(s0, sm);
         }
         sv = vec2<T>{(T)0, (T)0};
+#pragma unroll 20
         for (int J = n - 2; J >= RC; --J) {
             const int k = kk(J), q = qj(J);
             const int k1 = k < q ? k : 2 * q - k;  // index at level J+1

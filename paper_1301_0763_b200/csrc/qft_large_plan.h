@@ -31,11 +31,11 @@ struct LargeSchedule {
         int buf, leaf;
     };
 
-    Loc decompose(int c, int sg, int L, int dst, int depth) {
+    Loc decompose(int c, int sg, int L, int dst, int depth, int j = -1) {
         int lg = 0;
         while ((1 << lg) < L) ++lg;
         if (lg <= LEAFLOG) {
-            leaf[lg].push_back({c, sg, L, dst});
+            leaf[lg].push_back({c, sg, L, dst, j});
             return {0, 1};
         }
         const int r = RG < lg - LEAFLOG ? RG : lg - LEAFLOG;
@@ -43,7 +43,7 @@ struct LargeSchedule {
             f.resize(depth + 1);
             b.resize(depth + 1);
         }
-        f[depth][r].push_back({FTask{c, sg, L}, dst});
+        f[depth][r].push_back({FTask{c, sg, L, j}, dst});
         const int S = L >> r;
         Loc sub{0, 1};
         for (int p = 0; p < (1 << r); ++p) {
@@ -59,11 +59,11 @@ struct LargeSchedule {
         for (int side = 0; side < 2; ++side)
             for (int j = 0; j <= n - 2; ++j) {
                 const int L = 1 << (n - 2 - j);
-                Loc l = decompose(side * m + m - 2 * L, 1, L, side, 0);
+                Loc l = decompose(side * m + m - 2 * L, 1, L, side, 0, j);  // first touch folds x
                 if (l.buf) (side ? smask : cmask) |= 1u << j;
             }
     }
-    int passes() const { return 3 + 2 * (int)f.size(); }  // fold, F..., leaves, B..., chain
+    int passes() const { return 2 + 2 * (int)f.size(); }  // F... (fold on load), leaves, B..., chain
 };
 
 }  // namespace qft

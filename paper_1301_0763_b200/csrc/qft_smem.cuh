@@ -21,8 +21,10 @@
 #pragma once
 #include "qft_lee.cuh"
 
+// QFT_CHAIN_MID = k > 0: the bottom k chain levels are computed once by one warp
+// in phase C (the rest by each phase-D thread's descent); 0: all by descent
 #ifndef QFT_CHAIN_MID
-#define QFT_CHAIN_MID 0  // 1: lower chain levels by one warp in phase C; 0: per-thread descent in D
+#define QFT_CHAIN_MID 0
 #endif
 
 namespace qft {
@@ -40,7 +42,8 @@ struct SPlan {
     static constexpr int RF(int j) { return n - 7 - j; }  // big block: L = 32 << RF
     static constexpr int S0 = m;                     // sine region
     static constexpr int BASE = N - 1;               // s(0) at N-1, s(m) at N
-    static constexpr int JM = RC + 1;                // chain-mid level (computed in phase C)
+    static constexpr int JM0 = n - 1 - QFT_CHAIN_MID;
+    static constexpr int JM = QFT_CHAIN_MID ? (JM0 > RC + 1 ? JM0 : RC + 1) : n - 1;  // chain-mid level
     static constexpr int MJM = N >> (JM + 1);        // m_JM: C_JM has MJM+1 cells, S_JM MJM-1
     static constexpr int CHC = N + 1;                // C_JM cells [CHC, CHC + MJM]
     static constexpr int CHS = CHC + MJM + 1;        // S_JM harmonic h at CHS + h - 1
@@ -292,11 +295,13 @@ struct Chain {
         w[padx(P::CHC + 1)] = vsub(s0, sm);
     }
 
-#if !QFT_CHAIN_MID
-    // C_J[k], 0 <= k <= m_J: descend the time-split chain to the DCT base
+    // C_J[k], 0 <= k <= m_J: descend the time-split chain to the DCT base (or to
+    // the chain-mid level JM computed in phase C)
     template <int J>
     static QFT_HD vec2<T> descCJ(const vec2<T> *w, int k) {
-        if constexpr (J == n - 1) {  // DCT-0 of two points: [s0 + sm, s0 - sm]
+        if constexpr (QFT_CHAIN_MID && J == P::JM) {
+            return w[padx(P::CHC + k)];
+        } else if constexpr (J == n - 1) {  // DCT-0 of two points: [s0 + sm, s0 - sm]
             vec2<T> s0 = w[padx(P::BASE)], sm = w[padx(P::BASE + 1)];
             return k == 0 ? vadd(s0, sm) : vsub(s0, sm);
         } else {
@@ -312,7 +317,9 @@ struct Chain {
     template <int J>
     static QFT_HD vec2<T> descSJ(const vec2<T> *w, int k) {
         constexpr int q = qj(J), mm = 2 * q;
-        if constexpr (J == n - 2) {
+        if constexpr (QFT_CHAIN_MID && J == P::JM) {
+            return w[padx(P::CHS + (k > 0 ? k - 1 : 0))];
+        } else if constexpr (J == n - 2) {
             return OS(w, J, 1);                         // _dst base: copy
         } else {
             if (k == q) return OS(w, J, q);             // out[q-1] = O[q-1]
@@ -324,26 +331,6 @@ struct Chain {
     }
     static QFT_HD vec2<T> descC(const vec2<T> *w, int k) { return descCJ<P::RC>(w, k); }
     static QFT_HD vec2<T> descS(const vec2<T> *w, int k) { return descSJ<P::RC>(w, k); }
-#else
-    // C_RC[k], 0 <= k <= m_RC, from the chain-mid C_JM (one level)
-    static QFT_HD vec2<T> descC(const vec2<T> *w, int k) {
-        constexpr int q = qj(P::RC), mm = 2 * q;
-        const int kk = k <= q ? k : mm - k;
-        vec2<T> e = w[padx(P::CHC + kk)];
-        if (k == q) return e;                       // out[q] = E[q]
-        vec2<T> o = OC(w, P::RC, kk);
-        return k < q ? vadd(e, o) : vsub(e, o);     // E+O / E-O
-    }
-    // S_RC[k], 1 <= k <= m_RC - 1 (other k: unused value, in-bounds reads)
-    static QFT_HD vec2<T> descS(const vec2<T> *w, int k) {
-        constexpr int q = qj(P::RC), mm = 2 * q;
-        if (k == q) return OS(w, P::RC, q);         // out[q-1] = O[q-1]
-        const int kk = k < q ? k : mm - k;
-        vec2<T> o = OS(w, P::RC, kk);
-        vec2<T> e = w[padx(P::CHS + (kk > 0 ? kk - 1 : 0))];
-        return k < q ? vadd(o, e) : vsub(o, e);     // O+E / O-E
-    }
-#endif
 
     static QFT_HD void emit(vec2<T> *y, int k, vec2<T> cv, vec2<T> sv) {
         // S(k) = (C1 + S2, C2 - S1), S(N-k) = (C1 - S2, C2 + S1) (shared.py:218-221):

@@ -105,10 +105,10 @@ static void emu_reg(const vec2<T> *x, vec2<T> *y, const T *U) {
 
 // ---------------------------------------------------------------- large N
 template <int R, typename T>
-static void emu_f_task(vec2<T> *w, const FTask &tk, int dst, const T *U) {
+static void emu_f_task(vec2<T> *w, const FTask &tk, int dst, const T *U, const vec2<T> *x, int N) {
     for (int t = 0; t < (tk.L >> R); ++t) {
-        if (dst) lg_f_group<R, T, true>(w, tk, t, U);
-        else lg_f_group<R, T, false>(w, tk, t, U);
+        if (dst) lg_f_group<R, T, true>(w, tk, t, U, x, N);
+        else lg_f_group<R, T, false>(w, tk, t, U, x, N);
     }
 }
 template <int R, typename T>
@@ -119,16 +119,17 @@ static void emu_b_task(vec2<T> **W, const BTask &tk) {
     }
 }
 template <int L, typename T>
-static void emu_leaf_thread(vec2<T> *w, const LeafTask &tk, const T *U) {
-    if (tk.dst) lg_leaf_thread<L, T, true>(w, tk, U);
-    else lg_leaf_thread<L, T, false>(w, tk, U);
+static void emu_leaf_thread(vec2<T> *w, const LeafTask &tk, const T *U, const vec2<T> *x, int N) {
+    if (tk.dst) lg_leaf_thread<L, T, true>(w, tk, U, x, N);
+    else lg_leaf_thread<L, T, false>(w, tk, U, x, N);
 }
 template <int R, typename T, bool DST>
-static void emu_leaf_warp_dst(vec2<T> *w, const LeafTask &tk, const T *U) {
+static void emu_leaf_warp_dst(vec2<T> *w, const LeafTask &tk, const T *U, const vec2<T> *x, int N) {
     using WL = WarpLee<R, T, DST>;
     constexpr int L = WL::L;
     std::vector<vec2<T>> s(L + L / 32 + 1);
-    for (int e = 0; e < L; ++e) s[e + (e >> 5)] = w[tk.c + tk.sg * e];
+    for (int e = 0; e < L; ++e)
+        s[e + (e >> 5)] = tk.j >= 0 ? fold_load<T, DST>(x, N, tk.j, e) : w[tk.c + tk.sg * e];
     std::vector<typename WL::F> f(32);
     for (int t = 0; t < 32; ++t) f[t].load(s.data(), t, U);
     for (int t = 0; t < 32; ++t) f[t].store(s.data(), t);
@@ -139,9 +140,9 @@ static void emu_leaf_warp_dst(vec2<T> *w, const LeafTask &tk, const T *U) {
     for (int e = 0; e < L; ++e) w[tk.c + tk.sg * e] = s[e + (e >> 5)];
 }
 template <int R, typename T>
-static void emu_leaf_warp(vec2<T> *w, const LeafTask &tk, const T *U) {
-    if (tk.dst) emu_leaf_warp_dst<R, T, true>(w, tk, U);
-    else emu_leaf_warp_dst<R, T, false>(w, tk, U);
+static void emu_leaf_warp(vec2<T> *w, const LeafTask &tk, const T *U, const vec2<T> *x, int N) {
+    if (tk.dst) emu_leaf_warp_dst<R, T, true>(w, tk, U, x, N);
+    else emu_leaf_warp_dst<R, T, false>(w, tk, U, x, N);
 }
 
 template <typename T, int LEAFLOG, int RG>
@@ -150,32 +151,31 @@ static int emu_large(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
     const int N = S.N;
     std::vector<vec2<T>> W0(N + 2), W1(N + 2);
     vec2<T> *W[2] = {W0.data(), W1.data()};
-    for (int n = 0; n < N / 2; ++n) lg_fold_item<T>(x, W[0], n, N, log2n);
     for (auto &lvl : S.f)
         for (auto &kv : lvl)
             for (auto &td : kv.second) {
                 switch (kv.first) {
-                    case 1: emu_f_task<1, T>(W[0], td.first, td.second, U); break;
-                    case 2: emu_f_task<2, T>(W[0], td.first, td.second, U); break;
-                    case 3: emu_f_task<3, T>(W[0], td.first, td.second, U); break;
-                    case 4: emu_f_task<4, T>(W[0], td.first, td.second, U); break;
-                    case 5: emu_f_task<5, T>(W[0], td.first, td.second, U); break;
+                    case 1: emu_f_task<1, T>(W[0], td.first, td.second, U, x, N); break;
+                    case 2: emu_f_task<2, T>(W[0], td.first, td.second, U, x, N); break;
+                    case 3: emu_f_task<3, T>(W[0], td.first, td.second, U, x, N); break;
+                    case 4: emu_f_task<4, T>(W[0], td.first, td.second, U, x, N); break;
+                    case 5: emu_f_task<5, T>(W[0], td.first, td.second, U, x, N); break;
                 }
             }
     for (auto &kv : S.leaf)
         for (auto &tk : kv.second) {
             switch (kv.first) {
-                case 0: emu_leaf_thread<1, T>(W[0], tk, U); break;
-                case 1: emu_leaf_thread<2, T>(W[0], tk, U); break;
-                case 2: emu_leaf_thread<4, T>(W[0], tk, U); break;
-                case 3: emu_leaf_thread<8, T>(W[0], tk, U); break;
-                case 4: emu_leaf_thread<16, T>(W[0], tk, U); break;
-                case 5: emu_leaf_thread<32, T>(W[0], tk, U); break;
-                case 6: emu_leaf_warp<1, T>(W[0], tk, U); break;
-                case 7: emu_leaf_warp<2, T>(W[0], tk, U); break;
-                case 8: emu_leaf_warp<3, T>(W[0], tk, U); break;
-                case 9: emu_leaf_warp<4, T>(W[0], tk, U); break;
-                case 10: emu_leaf_warp<5, T>(W[0], tk, U); break;
+                case 0: emu_leaf_thread<1, T>(W[0], tk, U, x, N); break;
+                case 1: emu_leaf_thread<2, T>(W[0], tk, U, x, N); break;
+                case 2: emu_leaf_thread<4, T>(W[0], tk, U, x, N); break;
+                case 3: emu_leaf_thread<8, T>(W[0], tk, U, x, N); break;
+                case 4: emu_leaf_thread<16, T>(W[0], tk, U, x, N); break;
+                case 5: emu_leaf_thread<32, T>(W[0], tk, U, x, N); break;
+                case 6: emu_leaf_warp<1, T>(W[0], tk, U, x, N); break;
+                case 7: emu_leaf_warp<2, T>(W[0], tk, U, x, N); break;
+                case 8: emu_leaf_warp<3, T>(W[0], tk, U, x, N); break;
+                case 9: emu_leaf_warp<4, T>(W[0], tk, U, x, N); break;
+                case 10: emu_leaf_warp<5, T>(W[0], tk, U, x, N); break;
             }
         }
     for (int d = (int)S.b.size() - 1; d >= 0; --d)
@@ -195,6 +195,7 @@ static int emu_large(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
     g.m = N / 2;
     g.w0 = W[0];
     g.w1 = W[1];
+    g.x = x;
     g.cmask = S.cmask;
     g.smask = S.smask;
     for (int t = 0; t <= (N >> 5); ++t) g.template unit<4>(y, t);
