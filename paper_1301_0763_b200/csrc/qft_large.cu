@@ -49,7 +49,7 @@ struct Chunk {
 
 struct TaskSet {  // one launch: tasks of one kind and one R (or log2 L for leaves)
     int R = 0;
-    void *d_tasks = nullptr, *d_dsts = nullptr, *d_chunks = nullptr;
+    void *d_tasks = nullptr, *d_dsts = nullptr, *d_chunks = nullptr, *d_rs = nullptr;
     int ntasks = 0, nchunks = 0;
 };
 
@@ -82,17 +82,39 @@ __global__ void lg_fold_kernel(const vec2<T> *__restrict__ x, vec2<T> *__restric
 }
 
 template <int R, typename T>
-__global__ void lg_f_kernel(vec2<T> *__restrict__ W0, const FTask *__restrict__ tasks, const int *__restrict__ dsts,
-                            const Chunk *__restrict__ chunks, const T *__restrict__ U, long long batch, long long Ws,
-                            const vec2<T> *__restrict__ x, int N) {
-    const Chunk ch = chunks[blockIdx.x];
-    const FTask tk = tasks[ch.task];
-    const int t = ch.t0 + threadIdx.x;
+__device__ __forceinline__ void lg_f_dispatch_r(vec2<T> *w, const FTask &tk, int t, bool dst, const T *U,
+                                                const vec2<T> *x, int N) {
     if (t >= (tk.L >> R)) return;
-    const bool dst = dsts[ch.task];
-    for (long long b = blockIdx.y; b < batch; b += gridDim.y) {
-        if (dst) lg_f_group<R, T, true>(W0 + b * Ws, tk, t, U, x + b * N, N);
-        else lg_f_group<R, T, false>(W0 + b * Ws, tk, t, U, x + b * N, N);
+    if (dst) lg_f_group<R, T, true>(w, tk, t, U, x, N);
+    else lg_f_group<R, T, false>(w, tk, t, U, x, N);
+}
+
+// all forward tasks of one depth in one launch (R per task, uniform per CTA):
+// grid.x enumerates (signal, chunk) with the chunks of one signal adjacent, so
+// the strided sample gathers of its blocks share L2-resident sectors
+template <typename T>
+__global__ void __launch_bounds__(kChunk) lg_f_kernel(vec2<T> *__restrict__ W0, const FTask *__restrict__ tasks,
+                                                      const int *__restrict__ dsts, const int *__restrict__ rs,
+                                                      const Chunk *__restrict__ chunks, int nchunks,
+                                                      const T *__restrict__ U, long long batch, long long Ws,
+                                                      const vec2<T> *__restrict__ x, int N) {
+    for (long long g = blockIdx.x; g < (long long)nchunks * batch; g += gridDim.x) {
+        const long long b = g / nchunks;
+        const Chunk ch = chunks[g - b * nchunks];
+        const FTask tk = tasks[ch.task];
+        const int t = ch.t0 + threadIdx.x;
+        const bool dst = dsts[ch.task];
+        vec2<T> *w = W0 + b * Ws;
+        const vec2<T> *xb = x + b * N;
+        switch (rs[ch.task]) {
+            case 1: lg_f_dispatch_r<1, T>(w, tk, t, dst, U, xb, N); break;
+            case 2: lg_f_dispatch_r<2, T>(w, tk, t, dst, U, xb, N); break;
+            case 3: lg_f_dispatch_r<3, T>(w, tk, t, dst, U, xb, N); break;
+            case 4: lg_f_dispatch_r<4, T>(w, tk, t, dst, U, xb, N); break;
+#if QFT_LARGE_PREC == 32
+            case 5: lg_f_dispatch_r<5, T>(w, tk, t, dst, U, xb, N); break;
+#endif
+        }
     }
 }
 
@@ -235,21 +257,23 @@ int QFT_LG(qft_large_create)(int log2n, void **out) {
     p->fset.resize(S.f.size());
     p->bset.resize(S.b.size());
     for (size_t d = 0; d < S.f.size(); ++d) {
-        for (auto &kv : S.f[d]) {
+        {
             TaskSet ts;
-            ts.R = kv.first;
             std::vector<FTask> tk;
-            std::vector<int> ds;
+            std::vector<int> ds, rs;
             std::vector<Chunk> ch;
-            for (size_t i = 0; i < kv.second.size(); ++i) {
-                tk.push_back(kv.second[i].first);
-                ds.push_back(kv.second[i].second);
-                const int groups = kv.second[i].first.L >> kv.first;
-                for (int t0 = 0; t0 < groups; t0 += kChunk) ch.push_back({(int)i, t0});
-            }
+            for (auto &kv : S.f[d])
+                for (size_t i = 0; i < kv.second.size(); ++i) {
+                    const int id = (int)tk.size();
+                    tk.push_back(kv.second[i].first);
+                    ds.push_back(kv.second[i].second);
+                    rs.push_back(kv.first);
+                    const int groups = kv.second[i].first.L >> kv.first;
+                    for (int t0 = 0; t0 < groups; t0 += kChunk) ch.push_back({id, t0});
+                }
             ts.ntasks = (int)tk.size();
             ts.nchunks = (int)ch.size();
-            rc |= upload(tk, &ts.d_tasks) | upload(ds, &ts.d_dsts) | upload(ch, &ts.d_chunks);
+            rc |= upload(tk, &ts.d_tasks) | upload(ds, &ts.d_dsts) | upload(rs, &ts.d_rs) | upload(ch, &ts.d_chunks);
             p->fset[d].push_back(ts);
         }
         for (auto &kv : S.b[d]) {
@@ -289,6 +313,7 @@ void QFT_LG(qft_large_destroy)(void *pp) {
                 cudaFree(t.d_tasks);
                 cudaFree(t.d_dsts);
                 cudaFree(t.d_chunks);
+                cudaFree(t.d_rs);
             }
     for (auto &t : p->lset) cudaFree(t.d_tasks);
     delete p;
@@ -319,23 +344,14 @@ int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long ba
     memcpy(kc.u, uhead, sizeof(kc.u));
     const unsigned yb = ybatch(batch);
     cudaError_t e;
-    // forward passes
+    // forward passes: one launch per depth
     for (auto &v : p->fset)
         for (auto &ts : v) {
-            const int *dsts = (const int *)ts.d_dsts;
-            dim3 g(ts.nchunks, yb);
-            const FTask *tk = (const FTask *)ts.d_tasks;
-            const Chunk *ch = (const Chunk *)ts.d_chunks;
-            switch (ts.R) {
-                case 1: e = launch(lg_f_kernel<1, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws, x, S.N); break;
-                case 2: e = launch(lg_f_kernel<2, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws, x, S.N); break;
-                case 3: e = launch(lg_f_kernel<3, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws, x, S.N); break;
-                case 4: e = launch(lg_f_kernel<4, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws, x, S.N); break;
-#if QFT_LARGE_PREC == 32
-                case 5: e = launch(lg_f_kernel<5, T>, g, dim3(kChunk), 0, st, W0, tk, dsts, ch, U, batch, Ws, x, S.N); break;
-#endif
-                default: return (int)cudaErrorInvalidValue;
-            }
+            const long long work = (long long)ts.nchunks * batch;
+            const unsigned grid = (unsigned)std::min<long long>(work, 1 << 20);
+            e = launch(lg_f_kernel<T>, dim3(grid), dim3(kChunk), 0, st, W0, (const FTask *)ts.d_tasks,
+                       (const int *)ts.d_dsts, (const int *)ts.d_rs, (const Chunk *)ts.d_chunks, ts.nchunks, U, batch,
+                       Ws, x, S.N);
             if (e) return (int)e;
         }
     // leaves

@@ -96,17 +96,19 @@ template <int R, typename T, bool DST>
 QFT_HD void lg_f_group(vec2<T> *w, const FTask &tk, int t, const T *U, const vec2<T> *x = nullptr, int N = 0) {
     constexpr int G = 1 << R;
     vec2<T> v[G];
-    int pos[G];
 #pragma unroll
     for (int s = 0; s < G; ++s) {
         int c, sg;
         run_of(R, tk.L, s, c, sg);
-        pos[s] = tk.c + tk.sg * (c + sg * t);
-        v[s] = tk.j >= 0 ? fold_load<T, DST>(x, N, tk.j, c + sg * t) : w[pos[s]];
+        v[s] = tk.j >= 0 ? fold_load<T, DST>(x, N, tk.j, c + sg * t) : w[tk.c + tk.sg * (c + sg * t)];
     }
     lee_fwd_rt<R, T, DST>(v, t, tk.L, U);
 #pragma unroll
-    for (int s = 0; s < G; ++s) w[pos[s]] = v[s];  // slot s keeps its cells (in place)
+    for (int s = 0; s < G; ++s) {  // slot s keeps its cells (in place)
+        int c, sg;
+        run_of(R, tk.L, s, c, sg);
+        w[tk.c + tk.sg * (c + sg * t)] = v[s];
+    }
 }
 
 // ----------------------------------------------------------------- B pass
