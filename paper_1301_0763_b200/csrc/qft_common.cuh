@@ -19,6 +19,12 @@
 #define QFT_DEV inline
 #endif
 
+#if defined(__CUDACC__)
+// (-0, -0) as a packed fp32 pair in a mutable device global (see vmul<float>);
+// declared for both compilation passes so the host stub can register it.
+static __device__ unsigned long long qft_mzero_pair = 0x8000000080000000ull;
+#endif
+
 namespace qft {
 
 // One complex sample, or -- inside the real-factor recursion -- the pair
@@ -110,6 +116,18 @@ QFT_DEV vec2<float> vsub<float>(vec2<float> a, vec2<float> b) {
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
     return upk(r);
 }
+#if !defined(QFT_SCALAR_MUL)
+// Packed multiply without contraction: x*c + z with z = (-0, -0) read from a
+// mutable device global, so ptxas cannot fold a following add into it.
+// x*c + (-0) == x*c bit for bit (x*c = +0 gives +0 + -0 = +0, -0 stays -0).
+template <>
+QFT_DEV vec2<float> vmul<float>(vec2<float> a, float c) {
+    unsigned long long r;
+    const unsigned long long z = __ldg(&::qft_mzero_pair);
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a)), "l"(pk(vec2<float>{c, c})), "l"(z));
+    return upk(r);
+}
+#endif
 
 #endif
 template <typename T>

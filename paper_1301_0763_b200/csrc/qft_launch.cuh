@@ -20,6 +20,9 @@
 #ifndef QFT_TT_MAX
 #define QFT_TT_MAX 4       // cap on signals per CTA iteration
 #endif
+#ifndef QFT_FUSED_ABC
+#define QFT_FUSED_ABC 1    // phases A, B, C fused per warp (no CTA barriers between them)
+#endif
 #ifndef QFT_HALO_SHFL
 #define QFT_HALO_SHFL 0    // phase-C halo by warp shuffle (1) or by a shared-memory read (0)
 #endif
@@ -93,7 +96,9 @@ struct KCfg {
     static constexpr int W_D = (TT * P::MRC + 31) / 32;
     static constexpr int W_AC = TT * P::NWU + QFT_CHAIN_MID;  // + the chain-mid warp
     static constexpr int mx(int a, int b) { return a > b ? a : b; }
-    static constexpr int NW0 = mx(mx(W_B, W_D), W_AC);
+    static constexpr int NU = P::JF >= 1 ? 4 : 2;  // fused warp units per signal
+    static constexpr int W_U = TT * NU;
+    static constexpr int NW0 = QFT_FUSED_ABC ? mx(W_U, W_D) : mx(mx(W_B, W_D), W_AC);
     static constexpr int NWMAX = sizeof(T) == 8 ? 12 : 17;  // keep >= 168 (fp64) / 120 (fp32) registers
     static constexpr int NW = NW0 < 4 ? 4 : (NW0 > NWMAX ? NWMAX : NW0);
     static constexpr int NT = NW * 32;
@@ -213,6 +218,40 @@ QFT_DEV void run_chain_mid(vec2<T> *W, int ntr, int lane) {
     }
 }
 
+// ---- fused forward / Lee-32 / backward work of one side of one signal, one warp.
+// The F -> Lee-32 -> B work of a Lee block depends on no other block, so a warp
+// runs it start to finish with __syncwarp only (no CTA barrier).
+// unit 0: block 0 (its 2^RF(0) sub-blocks = one Lee-32 per lane)
+template <int LOG2N, typename T, bool DST>
+QFT_DEV void unit_block0(vec2<T> *w, const T *U, const T *kcu, int lane) {
+    using P = SPlan<LOG2N>;
+    if constexpr (P::JF >= 1) {
+        constexpr int sb = DST ? P::S0 : 0;
+        FBlock<LOG2N, 0, DST, T> f;
+        f.load(w, U, lane);
+        __syncwarp();
+        f.store(w, lane);
+        __syncwarp();
+        if (lane < (1 << P::RF(0))) b_l32<DST, T>(w, sb + 32 * lane, kcu);
+        __syncwarp();
+        run_c_block<LOG2N, T, 0, DST>(w, lane);
+    }
+}
+// unit 1: blocks 1..JF-1, the L = 32 block and the blocks with L <= 16
+template <int LOG2N, typename T, bool DST>
+QFT_DEV void unit_rest(vec2<T> *w, const T *U, const T *kcu, int lane) {
+    using P = SPlan<LOG2N>;
+    constexpr int sb = DST ? P::S0 : 0;
+    constexpr int K0 = P::JF >= 1 ? (1 << P::RF(0)) : 0;  // first chunk after block 0
+    constexpr int CNT = P::NL32 - K0;
+    run_f_blocks<LOG2N, T, 1>(w, U, DST, lane);
+    __syncwarp();
+    if (lane < CNT) b_l32<DST, T>(w, sb + 32 * (K0 + lane), kcu);
+    else if (lane == CNT) b_small<LOG2N, DST, T>(w, kcu);
+    __syncwarp();
+    run_c_blocks<LOG2N, T, 1>(w, DST, lane);
+}
+
 template <int LOG2N, typename T>
 __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
     qft_cdft_smem(const vec2<T> *__restrict__ in, vec2<T> *__restrict__ out, long long batch,
@@ -315,6 +354,24 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
             tma_bulk_load(stage, in + nb * TT * P::N, (uint32_t)(nt * P::N * K::VB), bar);
         }
 #endif
+#if QFT_FUSED_ABC
+        // A+B+C fused: one warp per (signal, side, unit) -- no CTA barrier inside
+        for (int u = warp; u < TT * K::NU; u += NW) {
+            const int tau = u / K::NU, kind = u - tau * K::NU;
+            if (tau >= ntr) continue;
+            vec2<T> *w = W + tau * P::PADDED;
+            const bool dst = kind & 1;
+            if (K::NU == 4 && kind < 2) {
+                if (dst) unit_block0<LOG2N, T, true>(w, U, kc.u, lane);
+                else unit_block0<LOG2N, T, false>(w, U, kc.u, lane);
+            } else {
+                if (dst) unit_rest<LOG2N, T, true>(w, U, kc.u, lane);
+                else unit_rest<LOG2N, T, false>(w, U, kc.u, lane);
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+#else
         // A: forward levels of the big blocks (warp units: side x {block 0, blocks 1..})
         if constexpr (P::NWU > 0) {
             for (int u = warp; u < TT * P::NWU; u += NW) {
@@ -386,6 +443,7 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
             }
             __syncthreads();
         }
+#endif
         // D: chain + recombination -> global
         for (int it = tid; it < TT * P::MRC; it += NT) {
             const int tau = it / P::MRC, t = it - tau * P::MRC;

@@ -76,6 +76,8 @@ static void emu_one(const vec2<T> *x, vec2<T> *y, const T *U) {
         for (int l = 1; l < 32; ++l) a0_chunk<LOG2N, T>(x, w, c, l, a0_lane<LOG2N>(l));
         a0_item<LOG2N, T>(x, w, 32 * c);
     }
+    // the kernel fuses F -> Lee-32 -> B per warp; blocks are independent, so the
+    // emulator may run the three stages block-set by block-set in any order
     emu_f<LOG2N, T, 0>(w, U);
     for (int k = 0; k < P::NL32; ++k) {
         b_l32<false, T>(w, 32 * k, U);

@@ -34,17 +34,32 @@ def sass_by_function():
                 # "HFMA2 Rd, -RZ, RZ, imm, imm" is ptxas's idiom for loading a constant
                 if op.startswith("HFMA2") and "-RZ, RZ" in args:
                     op = "MOV(HFMA2-imm)"
-                funcs[cur].append(op)
+                funcs[cur].append((op, args))
     return funcs, out
 
 
 def test_no_fused_multiply_add_in_transform_kernels():
+    """No scalar FFMA/DFMA/HFMA2 at all.  FFMA2 is allowed only as the packed
+    multiply x*c + z whose addend z is the opaque (-0,-0) pair: every register
+    feeding an FFMA2 addend must be written only by loads/moves (never by
+    arithmetic), so no product is ever fused into a sum."""
     funcs, _ = sass_by_function()
-    kernels = {k: v for k, v in funcs.items() if "qft_cdft" in k}
+    kernels = {k: v for k, v in funcs.items() if "qft_cdft" in k or "lg_" in k}
     assert len(kernels) >= 20, "expected the per-size transform kernels"
     for name, ops in kernels.items():
-        fused = [o for o in ops if re.match(r"(FFMA|DFMA|HFMA)", o)]
+        fused = [o for o, _ in ops if re.match(r"(FFMA(?!2)|DFMA|HFMA)", o)]
         assert not fused, f"{name}: fused multiply-add {set(fused)} would change rounding"
+        writers = {}
+        for o, args in ops:
+            m = re.match(r"\s*(U?R\d+)", args)
+            if m:
+                writers.setdefault(m.group(1), set()).add(o.split(".")[0])
+        for o, args in ops:
+            if not o.startswith("FFMA2"):
+                continue
+            addend = re.findall(r"(U?R\d+)", args)[-1]
+            bad = writers.get(addend, set()) - {"LDG", "LDC", "LDCU", "ULDC", "MOV", "UMOV", "LDS", "IMAD", "LDL"}
+            assert not bad, f"{name}: FFMA2 addend {addend} is produced by {bad}"
 
 
 def test_sm100a_and_packed_fp32():
@@ -53,4 +68,4 @@ def test_sm100a_and_packed_fp32():
     smem32 = [k for k in funcs if "qft_cdft_smem" in k and "ILi12EfE" in k]
     assert smem32, "fp32 N=4096 kernel missing"
     ops = funcs[smem32[0]]
-    assert any(o.startswith("FADD2") for o in ops), "fp32 adds should use the packed FADD2 pipe"
+    assert any(o.startswith("FADD2") for o, _ in ops), "fp32 adds should use the packed FADD2 pipe"
