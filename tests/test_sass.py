@@ -28,13 +28,13 @@ def sass_by_function():
             cur = m.group(1)
             funcs[cur] = []
         elif cur:
-            m = re.match(r"\s*/\*[0-9a-f]{4,}\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)([^;]*);", line)
+            m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)([^;]*);", line)
             if m:
-                op, args = m.group(2), m.group(3)
+                addr, op, args = int(m.group(1), 16), m.group(3), m.group(4)
                 # "HFMA2 Rd, -RZ, RZ, imm, imm" is ptxas's idiom for loading a constant
                 if op.startswith("HFMA2") and "-RZ, RZ" in args:
                     op = "MOV(HFMA2-imm)"
-                funcs[cur].append((op, args))
+                funcs[cur].append((op, args, addr))
     return funcs, out
 
 
@@ -47,19 +47,32 @@ def test_no_fused_multiply_add_in_transform_kernels():
     kernels = {k: v for k, v in funcs.items() if "qft_cdft" in k or "lg_" in k}
     assert len(kernels) >= 20, "expected the per-size transform kernels"
     for name, ops in kernels.items():
-        fused = [o for o, _ in ops if re.match(r"(FFMA(?!2)|DFMA|HFMA)", o)]
+        fused = [o for o, _, _ in ops if re.match(r"(FFMA(?!2)|DFMA|HFMA)", o)]
         assert not fused, f"{name}: fused multiply-add {set(fused)} would change rounding"
-        writers = {}
-        for o, args in ops:
-            m = re.match(r"\s*(U?R\d+)", args)
-            if m:
-                writers.setdefault(m.group(1), set()).add(o.split(".")[0])
-        for o, args in ops:
+        ok_src = {"LDG", "LDC", "LDCU", "ULDC", "MOV", "UMOV", "LDS", "IMAD", "LDL", "R2UR"}
+        # basic-block starts: branch targets and instructions after a branch
+        starts = set()
+        for k, (o, a, addr) in enumerate(ops):
+            if o.startswith(("BRA", "EXIT", "RET", "JMP", "BSYNC", "WARPSYNC", "CALL")):
+                tgt = re.search(r"0x([0-9a-f]+)", a)
+                if tgt:
+                    starts.add(int(tgt.group(1), 16))
+                if k + 1 < len(ops):
+                    starts.add(ops[k + 1][2])
+        for i, (o, args, addr) in enumerate(ops):
             if not o.startswith("FFMA2"):
                 continue
             addend = re.findall(r"(U?R\d+)", args)[-1]
-            bad = writers.get(addend, set()) - {"LDG", "LDC", "LDCU", "ULDC", "MOV", "UMOV", "LDS", "IMAD", "LDL"}
-            assert not bad, f"{name}: FFMA2 addend {addend} is produced by {bad}"
+            # nearest earlier definition of the addend inside the same basic block
+            src = None
+            for o2, a2, ad2 in reversed(ops[:i]):
+                m = re.match(r"\s*(U?R\d+)", a2)
+                if m and m.group(1) == addend:
+                    src = o2.split(".")[0]
+                    break
+                if ad2 in starts:
+                    break
+            assert src is None or src in ok_src, f"{name}: FFMA2 addend {addend} defined by {src}"
 
 
 def test_sm100a_and_packed_fp32():
@@ -68,4 +81,4 @@ def test_sm100a_and_packed_fp32():
     smem32 = [k for k in funcs if "qft_cdft_smem" in k and "ILi12EfE" in k]
     assert smem32, "fp32 N=4096 kernel missing"
     ops = funcs[smem32[0]]
-    assert any(o.startswith("FADD2") for o, _ in ops), "fp32 adds should use the packed FADD2 pipe"
+    assert any(o.startswith("FADD2") for o, _, _ in ops), "fp32 adds should use the packed FADD2 pipe"
