@@ -78,6 +78,15 @@ def build(jobs=None, verbose=True, defines=(), lib=None):
         with cf.ThreadPoolExecutor(jobs) as ex:
             list(ex.map(lambda u: _compile(*u), todo))
     objs = [u[1] for u in units]
+    if not defines:  # drop objects of older source digests (keeps build/ small)
+        keep = set(objs) | {o + ".log" for o in objs}
+        for f in os.listdir(BUILD):
+            full = os.path.join(BUILD, f)
+            if full not in keep and ("_" + dig.split("_")[0]) not in f and f.endswith((".o", ".o.log")):
+                try:
+                    os.remove(full)
+                except OSError:
+                    pass
     tmp = target + ".tmp"
     cmd = [nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart"]
     subprocess.check_call(cmd)

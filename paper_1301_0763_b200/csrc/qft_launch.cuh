@@ -93,7 +93,7 @@ struct KCfg {
     static constexpr int rup32(int x) { return (x + 31) / 32 * 32; }
     static constexpr int NB32 = rup32(TT * P::NL32);                 // phase-B Lee-32 lanes per side
     static constexpr int W_B = (2 * NB32 + rup32(2 * TT)) / 32;
-    static constexpr int W_D = (TT * P::MRC + 31) / 32;
+    static constexpr int W_D = (TT * P::DT + 31) / 32;
     static constexpr int W_AC = TT * P::NWU + QFT_CHAIN_MID;  // + the chain-mid warp
     static constexpr int mx(int a, int b) { return a > b ? a : b; }
     static constexpr int NU = P::JF >= 1 ? 4 : 2;  // fused warp units per signal
@@ -334,9 +334,14 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
                 }
             }
 #else
-            for (int u = warp; u < TT * NCH; u += NW) {
-                const int tau = u / NCH, c = u - tau * NCH;
-                if (tau < ntr && lane) a0_chunk<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, c, lane, a0l);
+            // the warp walks its chunks of each signal with fixed per-lane constants
+            for (int tau = 0; tau < ntr; ++tau) {
+                const vec2<T> *xs = stage + tau * P::N;
+                vec2<T> *ws = W + tau * P::PADDED;
+                if (lane) {
+#pragma unroll 4
+                    for (int c = warp; c < NCH; c += NW) a0_chunk<LOG2N, T>(xs, ws, c, lane, a0l);
+                }
             }
 #endif
             for (int it = tid; it < TT * NCH; it += NT) {
@@ -445,8 +450,8 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
         }
 #endif
         // D: chain + recombination -> global
-        for (int it = tid; it < TT * P::MRC; it += NT) {
-            const int tau = it / P::MRC, t = it - tau * P::MRC;
+        for (int it = tid; it < TT * P::DT; it += NT) {
+            const int tau = it / P::DT, t = it - tau * P::DT;
             if (tau < ntr) Chain<LOG2N, T>::unit(W + tau * P::PADDED, out + (bt * TT + tau) * P::N, t);
         }
         __syncthreads();

@@ -52,7 +52,8 @@ struct SPlan {
     static constexpr int PADDED = CELLS + CELLS / 32 + 1;
     static constexpr int NL32 = n >= 7 ? m / 32 - 1 : 0;  // Lee-32 chunks per side
     static constexpr int NWU = 2 * ((JF >= 1) + (JF >= 2)); // phase A/C warp units
-    static constexpr int MRC = N >> (RC + 1);        // phase D threads per signal
+    static constexpr int MRC = N >> (RC + 1);        // m_RC: phase-D thread t in [0, MRC]
+    static constexpr int DT = MRC + 1;               // phase D threads per signal
     static constexpr int UCELLS = N / 4;             // level-table entries
 };
 
@@ -93,15 +94,19 @@ QFT_HD void a0_item(const vec2<T> *x, vec2<T> *w, int n) {
 // class j = ctz(l) and cell off_j + (n >> (j+1)) = A_l + c * B_l do not depend
 // on c except through B_l; lane 0's n = 32c (c >= 1) are done by a0_item.
 struct A0Lane {
-    int A, B;  // cell = A + c*B (cosine side)
+    int A, B, sh;  // padded cosine cell of chunk c: A + c*B + (c >> sh)
 };
 template <int LOG2N>
 QFT_HD A0Lane a0_lane(int l) {
     using P = SPlan<LOG2N>;
     A0Lane r;
     const int j = ctz32((uint32_t)(l | 32));
-    r.A = P::m - (1 << (LOG2N - 1 - j)) + (l >> (j + 1));
+    // cell = off_j + (n >> (j+1)) with off_j a multiple of 32 and (l >> (j+1)) + c*B mod 32 < 32,
+    // so padx(cell) = off_j + off_j/32 + (l >> (j+1)) + c*B + (c >> (j+1))
+    const int off = P::m - (1 << (LOG2N - 1 - j));
+    r.A = off + (off >> 5) + (l >> (j + 1));
     r.B = 32 >> (j + 1);
+    r.sh = j + 1;
     return r;
 }
 template <int LOG2N, typename T>
@@ -109,9 +114,9 @@ QFT_HD void a0_chunk(const vec2<T> *x, vec2<T> *w, int c, int l, A0Lane a) {
     using P = SPlan<LOG2N>;
     const int n = 32 * c + l;
     vec2<T> u = x[n], v = x[P::N - n];
-    const int cell = a.A + c * a.B;
-    w[padx(cell)] = vadd(u, v);              // dc[n]   = x[n] + x[N-n]
-    w[padx(P::S0 + cell)] = vsub(u, v);      // ds[n-1] = x[n] - x[N-n]
+    const int pc = a.A + c * a.B + (c >> a.sh);
+    w[pc] = vadd(u, v);                      // dc[n]   = x[n] + x[N-n]
+    w[pc + padx(P::S0)] = vsub(u, v);        // ds[n-1] = x[n] - x[N-n]  (S0 is a multiple of 32)
 }
 
 template <int LOG2N, typename T>
@@ -379,16 +384,65 @@ struct Chain {
     }
 
     // t in [0, MRC): t = 0 is the special thread (groups 0 and MRC)
-    static QFT_HD void unit(const vec2<T> *w, vec2<T> *y, int t) {
-        constexpr int RC = P::RC;
-        if (t == 0) {
-            vec2<T> c0 = descC(w, 0);
-            up_s<RC, 0>(w, y, c0, c0);
-            constexpr int qq = qj(RC - 1);                 // = MRC
-            up_s<RC - 1, qq>(w, y, descC(w, qq), OS(w, RC - 1, qq));
+    // ---- uniform phase-D thread (t in [0, MRC], no special path) ----------
+    // index of thread t's chain value at level J > RC: the distance of t to the
+    // nearest multiple of m_{J-1} (composition of the folds k -> min(k, m_j - k))
+    template <int J>
+    static QFT_HD int kk(int t) {
+        if constexpr (J == P::RC) {
+            return t;
         } else {
-            up<RC>(w, y, t, descC(w, t), descS(w, t));
+            constexpr int Pm = 2 << (n - 1 - J);  // m_{J-1}
+            const int r = t & (Pm - 1);
+            return r < Pm - r ? r : Pm - r;
         }
+    }
+    // C_J / S_J at index kk<J>(t), bottom-up; every load address depends on t
+    // only, so all loads issue before the dependent add chain
+    template <int J>
+    static QFT_HD void desc2(const vec2<T> *w, int t, vec2<T> &cv, vec2<T> &sv) {
+        if constexpr (J == n - 1) {
+            const vec2<T> s0 = w[padx(P::BASE)], sm = w[padx(P::BASE + 1)];
+            cv = kk<J>(t) == 0 ? vadd(s0, sm) : vsub(s0, sm);  // DCT-0 of two points
+            sv = s0;                                             // (unused)
+        } else {
+            desc2<J + 1>(w, t, cv, sv);
+            constexpr int q = qj(J);
+            const int k = kk<J>(t), k1 = kk<J + 1>(t);  // k1 = min(k, 2q - k)
+            const vec2<T> o = OC(w, J, k1);
+            const vec2<T> os = OS(w, J, k1 > 0 ? k1 : 1);
+            const bool self = (k == q), lo = (k < q);
+            cv = self ? cv : (lo ? vadd(cv, o) : vsub(cv, o));   // E+O / E-O / E[q]
+            sv = self ? os : (lo ? vadd(os, sv) : vsub(os, sv)); // O+E / O-E / O[q]
+        }
+    }
+
+    static QFT_HD void emit_u(vec2<T> *y, int k, vec2<T> cv, vec2<T> sv) {
+        const vec2<T> u = {sv.y, -sv.x};
+        const bool edge = (k == 0) || (k == P::m);  // harmonics 0, N/2: copies
+        y[k] = edge ? cv : vadd(cv, u);
+        if (!edge) y[P::N - k] = vsub(cv, u);
+    }
+    // unfold with self-paired indices (k == q_j) duplicated: both children get
+    // the C copy / S leaf and write identical values
+    template <int J>
+    static QFT_HD void up_u(const vec2<T> *w, vec2<T> *y, int k, vec2<T> cv, vec2<T> sv) {
+        if constexpr (J == 0) {
+            emit_u(y, k, cv, sv);
+        } else {
+            constexpr int q = qj(J - 1), mm = 2 * q;
+            const bool self = (k == q);
+            const vec2<T> o = OC(w, J - 1, k < q ? k : 0);
+            const vec2<T> os = OS(w, J - 1, k > 0 ? k : 1);
+            up_u<J - 1>(w, y, k, self ? cv : vadd(cv, o), self ? os : vadd(os, sv));
+            up_u<J - 1>(w, y, self ? q : mm - k, self ? cv : vsub(cv, o), self ? os : vsub(os, sv));
+        }
+    }
+
+    static QFT_HD void unit(const vec2<T> *w, vec2<T> *y, int t) {
+        vec2<T> cv, sv;
+        if constexpr (P::RC < n - 1) desc2<P::RC>(w, t, cv, sv);
+        up_u<P::RC>(w, y, t, cv, sv);
     }
 };
 

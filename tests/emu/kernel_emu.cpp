@@ -97,7 +97,7 @@ static void emu_one(const vec2<T> *x, vec2<T> *y, const T *U) {
         for (int k = 0; k < cnt; ++k) C::mid_level_store(w, j, k, cv[k], sv[k]);
     }
 #endif
-    for (int t = 0; t < P::MRC; ++t) Chain<LOG2N, T>::unit(w, y, t);
+    for (int t = 0; t < P::DT; ++t) Chain<LOG2N, T>::unit(w, y, t);
 }
 
 template <int NN, typename T>
