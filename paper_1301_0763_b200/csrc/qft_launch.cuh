@@ -20,6 +20,9 @@
 #ifndef QFT_TT_MAX
 #define QFT_TT_MAX 4       // cap on signals per CTA iteration
 #endif
+#ifndef QFT_A0_64
+#define QFT_A0_64 1        // A0 by 64-sample chunks (conflict-free block-0 stores, paired loads)
+#endif
 #ifndef QFT_FUSED_ABC
 #define QFT_FUSED_ABC 1    // phases A, B, C fused per warp (no CTA barriers between them)
 #endif
@@ -270,6 +273,7 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
 
     const long long nbatch = (batch + TT - 1) / TT;
     const A0Lane a0l = a0_lane<LOG2N>(lane);
+    const A0Lane64 a0l64 = a0_lane64<LOG2N>(lane);
     for (int i = tid; i < P::UCELLS; i += NT) U[i] = Ug[i];
 #if QFT_A0_TMA
     if (tid == 0) mbar_init(bar, 1);
@@ -334,6 +338,27 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
                 }
             }
 #else
+#if QFT_A0_64
+            // chunks of 64 consecutive n; the multiples of 64 (and n = 0) afterwards
+            // (N = 64 has a single 32-sample half: one chunk of lanes 0..15 suffices
+            //  only for m >= 64, so small N keep the 32-sample chunks below)
+            if constexpr (P::m >= 64) {
+            constexpr int NC64 = P::m / 64;
+            auto shfl_up = [](vec2<T> v) { return shfl_vec(v, false); };
+            for (int u = warp; u < TT * NC64; u += NW) {
+                const int tau = u / NC64, c = u - tau * NC64;
+                if (tau < ntr) a0_chunk64<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, c, lane, a0l64, shfl_up);
+            }
+            for (int it = tid; it < TT * NC64; it += NT) {
+                const int tau = it / NC64, c = it - tau * NC64;
+                if (tau < ntr) a0_item<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, 64 * c);
+            }
+            } else {
+                for (int tau = 0; tau < ntr; ++tau)
+                    for (int nn = tid; nn < P::m; nn += NT)
+                        a0_item<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, nn);
+            }
+#else
             // the warp walks its chunks of each signal with fixed per-lane constants
             for (int tau = 0; tau < ntr; ++tau) {
                 const vec2<T> *xs = stage + tau * P::N;
@@ -343,13 +368,14 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
                     for (int c = warp; c < NCH; c += NW) a0_chunk<LOG2N, T>(xs, ws, c, lane, a0l);
                 }
             }
-#endif
             for (int it = tid; it < TT * NCH; it += NT) {
                 const int tau = it / NCH, c = it - tau * NCH;
                 if (tau < ntr) a0_item<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, 32 * c);
             }
-        }
 #endif
+#endif  // QFT_A0_TMA
+        }
+#endif  // QFT_A0_UNIT8
         __syncthreads();
 #if QFT_A0_TMA
         // the staging buffer is free: prefetch the next batch while we compute

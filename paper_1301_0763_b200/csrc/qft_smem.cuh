@@ -119,6 +119,41 @@ QFT_HD void a0_chunk(const vec2<T> *x, vec2<T> *w, int c, int l, A0Lane a) {
     w[pc + padx(P::S0)] = vsub(u, v);        // ds[n-1] = x[n] - x[N-n]  (S0 is a multiple of 32)
 }
 
+// A0 by chunks of 64 consecutive n (n = 64c + 2l and 64c + 2l + 1 for lane l):
+// one aligned pair load per side, the odd samples (Lee block 0) go to 32
+// consecutive cells, the even ones to block 1 + ctz(l); lane l's even mirror
+// x[N - 64c - 2l] is the first element of lane l-1's mirror pair.
+struct A0Lane64 {
+    int A, B, sh;  // padded cosine cell of the even sample of chunk c: A + c*B + (c >> sh)
+};
+template <int LOG2N>
+QFT_HD A0Lane64 a0_lane64(int l) {
+    using P = SPlan<LOG2N>;
+    A0Lane64 r;
+    const int j = 1 + ctz32((uint32_t)(l | 32));  // block of n = 64c + 2l (l != 0)
+    const int off = P::m - (1 << (LOG2N - 1 - j));
+    r.A = off + (off >> 5) + (l >> j);
+    r.B = 32 >> j;
+    r.sh = j;
+    return r;
+}
+template <int LOG2N, typename T, class ShflUp>
+QFT_HD void a0_chunk64(const vec2<T> *x, vec2<T> *w, int c, int l, A0Lane64 a, ShflUp &&shfl_up) {
+    using P = SPlan<LOG2N>;
+    vec2<T> xe, xo, mn, mo;
+    ld2(x + 64 * c + 2 * l, xe, xo);                // x[n_e], x[n_o]
+    ld2(x + P::N - 64 * c - 2 * l - 2, mn, mo);     // x[N - n_e - 2], x[N - n_o]
+    const vec2<T> me = shfl_up(mn);                  // x[N - n_e] from lane l-1
+    const int po = 33 * c + l;                       // block 0 cell 32c + l, padded
+    w[po] = vadd(xo, mo);
+    w[po + padx(P::S0)] = vsub(xo, mo);
+    if (l) {
+        const int pe = a.A + c * a.B + (c >> a.sh);
+        w[pe] = vadd(xe, me);
+        w[pe + padx(P::S0)] = vsub(xe, me);
+    }
+}
+
 template <int LOG2N, typename T>
 QFT_HD void a0_unit8(const vec2<T> *x, vec2<T> *w, int k) {
     using P = SPlan<LOG2N>;

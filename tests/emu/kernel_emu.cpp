@@ -72,9 +72,19 @@ static void emu_one(const vec2<T> *x, vec2<T> *y, const T *U) {
     using P = SPlan<LOG2N>;
     std::vector<vec2<T>> Wv(P::PADDED);
     vec2<T> *w = Wv.data();
-    for (int c = 0; c < P::m / 32; ++c) {
-        for (int l = 1; l < 32; ++l) a0_chunk<LOG2N, T>(x, w, c, l, a0_lane<LOG2N>(l));
-        a0_item<LOG2N, T>(x, w, 32 * c);
+    if (P::m < 64)
+        for (int n = 0; n < P::m; ++n) a0_item<LOG2N, T>(x, w, n);
+    for (int c = 0; c < P::m / 64; ++c) {
+        // the device shuffles lane l-1's first mirror element up; emulate with the same loads
+        for (int l = 0; l < 32; ++l) {
+            auto shfl_up = [&](vec2<T> v) {
+                (void)v;
+                const int lp = l > 0 ? l - 1 : l;
+                return x[P::N - 64 * c - 2 * lp - 2];
+            };
+            a0_chunk64<LOG2N, T>(x, w, c, l, a0_lane64<LOG2N>(l), shfl_up);
+        }
+        a0_item<LOG2N, T>(x, w, 64 * c);
     }
     // the kernel fuses F -> Lee-32 -> B per warp; blocks are independent, so the
     // emulator may run the three stages block-set by block-set in any order
