@@ -38,6 +38,10 @@ extern "C" {
 #define QFT_ALGO_IMPROVED 0
 #define QFT_ALGO_CLASSICAL 1
 
+#define QFT_KIND_RDFT 1 /* improved.rdft (improved.py:131-136) */
+#define QFT_KIND_DCT0 2 /* improved.dct0 (improved.py:117-121) */
+#define QFT_KIND_DST0 3 /* improved.dst0 (improved.py:124-128) */
+
 typedef struct qft_plan qft_plan;
 
 typedef struct {
@@ -81,6 +85,16 @@ int qft_plan_set_table(qft_plan *plan, const void *h_table);
 int qft_exec_cdft(const qft_plan *plan, const void *d_in, void *d_out, int64_t batch,
                   int64_t in_batch_stride, int64_t in_elem_stride,
                   int64_t out_batch_stride, int64_t out_elem_stride, void *stream);
+
+/* Real-input transforms of the same plan (periodization N = 2^log2n) on
+ * device rows, batch-major contiguous:
+ *   QFT_KIND_RDFT: rows of N reals -> rows of N/2+1 complex (k = 0..N/2; the
+ *                  reference's packed half spectrum, complex_from_packed, shared.py:94-101)
+ *   QFT_KIND_DCT0: rows of N/2+1 reals s(0..N/2) -> N/2+1 reals
+ *   QFT_KIND_DST0: rows of N/2-1 reals s(1..N/2-1) -> N/2-1 reals
+ * Precision = the plan's (real float32 for QFT_PREC_F32).  Two rows share one
+ * complex-typed lane of the kernels; every row is bit-identical to the reference. */
+int qft_exec_real(const qft_plan *plan, int kind, const void *d_in, void *d_out, int64_t nrows, void *stream);
 
 /* Same transform on HOST buffers: chunked host->device copy, transform and
  * device->host copy, pipelined over the plan's streams.  Synchronous.  Pinned

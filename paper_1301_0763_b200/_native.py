@@ -16,6 +16,7 @@ QFT_PREC_F32 = 32
 QFT_PREC_F64 = 64
 QFT_ALGO_IMPROVED = 0
 QFT_ALGO_CLASSICAL = 1
+QFT_KIND_RDFT, QFT_KIND_DCT0, QFT_KIND_DST0 = 1, 2, 3
 
 QFT_EINVAL = -1
 QFT_EUNSUPPORTED = -2
@@ -50,6 +51,7 @@ SIGNATURES = {
     "qft_plan_set_table": (_I, [_P, _P]),
     "qft_exec_cdft": (_I, [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _P]),
     "qft_exec_cdft_host": (_I, [_P, _P, _P, _I64, _I64, _I64, _I64, _I64]),
+    "qft_exec_real": (_I, [_P, _I, _P, _P, _I64, _P]),
     "qft_fill_normal": (_I, [_P, _P, _I64, _I64, ctypes.c_uint64, _P]),
     "qft_last_error": (ctypes.c_char_p, []),
 }
@@ -136,6 +138,9 @@ class Plan:
     def exec_device(self, d_in, d_out, batch, in_strides, out_strides, stream=0):
         check(self._lib.qft_exec_cdft(self.handle, d_in, d_out, batch, in_strides[0], in_strides[1],
                                       out_strides[0], out_strides[1], stream), "qft_exec_cdft")
+
+    def exec_real(self, kind, d_in, d_out, nrows, stream=0):
+        check(self._lib.qft_exec_real(self.handle, kind, d_in, d_out, nrows, stream), "qft_exec_real")
 
     def exec_host(self, h_in, h_out, batch, in_strides, out_strides):
         check(self._lib.qft_exec_cdft_host(self.handle, h_in, h_out, batch, in_strides[0], in_strides[1],

@@ -56,6 +56,16 @@ def improved_cdft_counts(N):
     return 3 * N * lg - 3 * N + 4, N * lg - 3 * N + 4
 
 
+def improved_real_counts(kind, N):
+    """(adds, muls) of improved.rdft / dct0 / dst0 (costmodel.py:72-82)."""
+    lg = _lg(N)
+    if kind == "rdft":
+        return (3 * N * lg // 2 - 5 * N // 2 + 4, N * lg // 2 - 3 * N // 2 + 2)
+    if kind == "dct0":
+        return (3 * N * lg // 4 - 7 * N // 4 + lg + 3, N * lg // 4 - 3 * N // 4 + 1)
+    return (3 * N * lg // 4 - 7 * N // 4 - lg + 3, N * lg // 4 - 3 * N // 4 + 1)
+
+
 def _cos_turns_wide(j, d, ftype):
     """cos(2 pi j/d) one tier above the working dtype."""
     if ftype is np.float32:

@@ -139,13 +139,13 @@ struct qft_plan {
 };
 
 // per-instance launchers, one translation unit each (qft_inst.cu)
-#define QFT_DECL(P, L) int qft_inst_launch_##P##_##L(const LaunchArgs *); void qft_inst_cfg_##P##_##L(int *);
+#define QFT_DECL(P, L) int qft_inst_launch_##P##_##L(const LaunchArgs *, int); void qft_inst_cfg_##P##_##L(int *);
 #define QFT_DECL_ALL(P) \
     QFT_DECL(P, 1) QFT_DECL(P, 2) QFT_DECL(P, 3) QFT_DECL(P, 4) QFT_DECL(P, 5) QFT_DECL(P, 6) QFT_DECL(P, 7) \
     QFT_DECL(P, 8) QFT_DECL(P, 9) QFT_DECL(P, 10) QFT_DECL(P, 11) QFT_DECL(P, 12)
 QFT_DECL_ALL(32)
 QFT_DECL_ALL(64)
-typedef int (*launch_fn)(const LaunchArgs *);
+typedef int (*launch_fn)(const LaunchArgs *, int);
 #define QFT_ROW(P)                                                                                              \
     {nullptr, qft_inst_launch_##P##_1, qft_inst_launch_##P##_2, qft_inst_launch_##P##_3, qft_inst_launch_##P##_4, \
      qft_inst_launch_##P##_5, qft_inst_launch_##P##_6, qft_inst_launch_##P##_7, qft_inst_launch_##P##_8,         \
@@ -194,7 +194,7 @@ static int launch_contig(qft_plan *p, const void *in, void *out, long long batch
         return fail(QFT_EUNSUPPORTED, "periodization 2^" + std::to_string(p->log2n) + " not built yet");
     LaunchArgs a{in, out, batch, p->d_U, p->prec == QFT_PREC_F32 ? (const void *)p->uhead32 : (const void *)p->uhead64,
                  p->num_sms, st};
-    int e = kLaunch[p->prec == QFT_PREC_F32 ? 0 : 1][p->log2n](&a);
+    int e = kLaunch[p->prec == QFT_PREC_F32 ? 0 : 1][p->log2n](&a, 0);
     if (e != 0) return fail(QFT_ECUDA, std::string("kernel launch: ") + cudaGetErrorString((cudaError_t)e));
     return 0;
 }
@@ -411,6 +411,25 @@ int qft_exec_cdft(const qft_plan *cp, const void *d_in, void *d_out, int64_t bat
     CUDA_TRY(cudaSetDevice(p->device));
     std::lock_guard<std::mutex> lk(p->mu);
     return exec_impl(p, d_in, d_out, batch, ibs, ies, obs, oes, (cudaStream_t)stream);
+}
+
+int qft_exec_real(const qft_plan *cp, int kind, const void *d_in, void *d_out, int64_t nrows, void *stream) {
+    qft_plan *p = const_cast<qft_plan *>(cp);
+    if (!p || (nrows && (!d_in || !d_out))) return fail(QFT_EINVAL, "NULL argument");
+    if (kind < QFT_KIND_RDFT || kind > QFT_KIND_DST0) return fail(QFT_EINVAL, "kind must be rdft, dct0 or dst0");
+    if (nrows < 0) return fail(QFT_EINVAL, "negative row count");
+    if (kind == QFT_KIND_DST0 && p->log2n < 2) return fail(QFT_EINVAL, "the sine transform needs N >= 4");
+    if (nrows == 0) return 0;
+    if (d_in == d_out) return fail(QFT_EINVAL, "transform is out-of-place: d_in must differ from d_out");
+    if (p->log2n > kMaxLog2N) return fail(QFT_EUNSUPPORTED, "real transforms are built for N <= 4096");
+    CUDA_TRY(cudaSetDevice(p->device));
+    std::lock_guard<std::mutex> lk(p->mu);
+    LaunchArgs a{d_in, d_out, (nrows + 1) / 2, p->d_U,
+                 p->prec == QFT_PREC_F32 ? (const void *)p->uhead32 : (const void *)p->uhead64, p->num_sms,
+                 (cudaStream_t)stream, nrows};
+    int e = kLaunch[p->prec == QFT_PREC_F32 ? 0 : 1][p->log2n](&a, kind);
+    if (e != 0) return fail(QFT_ECUDA, std::string("kernel launch: ") + cudaGetErrorString((cudaError_t)e));
+    return 0;
 }
 
 int qft_exec_cdft_host(qft_plan *p, const void *h_in, void *h_out, int64_t batch, int64_t ibs, int64_t ies,

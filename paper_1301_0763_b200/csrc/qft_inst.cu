@@ -33,10 +33,25 @@ void QFT_CFGNAME(QFT_INST_PREC, QFT_INST_LOG2N)(int *cfg) {
 #endif
 }
 
-int QFT_NAME(QFT_INST_PREC, QFT_INST_LOG2N)(const qft::LaunchArgs *a) {
+// mode: 0 cdft, 1 rdft, 2 dct0, 3 dst0 (real modes: a->batch = row pairs, a->nreal = rows)
+int QFT_NAME(QFT_INST_PREC, QFT_INST_LOG2N)(const qft::LaunchArgs *a, int mode) {
+    constexpr int L = QFT_INST_LOG2N;
 #if QFT_INST_LOG2N <= 5
-    return (int)qft::launch_reg<(1 << QFT_INST_LOG2N), Real>(*a);
+    switch (mode) {
+        case 0: return (int)qft::launch_reg<(1 << L), Real, 0>(*a);
+        case 1: return (int)qft::launch_reg<(1 << L), Real, 1>(*a);
+        case 2: return (int)qft::launch_reg<(1 << L), Real, 2>(*a);
+        case 3:
+            if constexpr (L >= 2) return (int)qft::launch_reg<(1 << L), Real, 3>(*a);
+            return (int)cudaErrorInvalidValue;
+    }
 #else
-    return (int)qft::launch_smem<QFT_INST_LOG2N, Real>(*a);
+    switch (mode) {
+        case 0: return (int)qft::launch_smem<L, Real, 0>(*a);
+        case 1: return (int)qft::launch_smem<L, Real, 1>(*a);
+        case 2: return (int)qft::launch_smem<L, Real, 2>(*a);
+        case 3: return (int)qft::launch_smem<L, Real, 3>(*a);
+    }
 #endif
+    return (int)cudaErrorInvalidValue;
 }

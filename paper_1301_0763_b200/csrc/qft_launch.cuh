@@ -43,6 +43,7 @@ struct LaunchArgs {
     const void *Uhead;    // host copy of U[0..32): the constants of every Lee block with L <= 32
     int num_sms;
     cudaStream_t stream;
+    long long nreal = 0;  // real modes: number of real rows (batch = row pairs)
 };
 
 // U[0..32) as a kernel parameter: lives in the constant bank, so the Lee-32
@@ -113,20 +114,78 @@ struct KCfg {
 };
 
 // ------------------------------------------------------------ small N
-template <int NN, typename T>
+template <int NN, typename T, int MODE = 0>
 __global__ void __launch_bounds__(128) qft_cdft_reg(const vec2<T> *__restrict__ in, vec2<T> *__restrict__ out,
-                                                    long long batch, const T *__restrict__ U) {
+                                                    long long batch, const T *__restrict__ U, long long nreal = 0) {
     __shared__ T sU[NN / 4 >= 2 ? NN / 4 : 2];
     for (int i = threadIdx.x; i < (NN / 4 >= 2 ? NN / 4 : 2); i += blockDim.x) sU[i] = U[i];
     __syncthreads();
+    constexpr int m = NN / 2;
     for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < batch;
          b += (long long)gridDim.x * blockDim.x) {
-        vec2<T> x[NN], y[NN];
+        if constexpr (MODE == 0) {
+            vec2<T> x[NN], y[NN];
 #pragma unroll
-        for (int n = 0; n < NN; ++n) x[n] = in[b * NN + n];
-        cdft_reg<NN, T>(x, y, sU);
+            for (int n = 0; n < NN; ++n) x[n] = in[b * NN + n];
+            cdft_reg<NN, T>(x, y, sU);
 #pragma unroll
-        for (int n = 0; n < NN; ++n) out[b * NN + n] = y[n];
+            for (int n = 0; n < NN; ++n) out[b * NN + n] = y[n];
+        } else {
+            constexpr int RL = MODE == 1 ? NN : (MODE == 2 ? m + 1 : (m > 1 ? m - 1 : 1));
+            const T *xr = reinterpret_cast<const T *>(in);
+            const long long ra = 2 * b, rb = ra + 1 < nreal ? ra + 1 : ra;
+            const bool has_b = ra + 1 < nreal;
+            vec2<T> x[RL];
+#pragma unroll
+            for (int n = 0; n < RL; ++n) x[n] = {xr[ra * RL + n], xr[rb * RL + n]};
+            if constexpr (MODE == 1) {  // rdft_packed (shared.py:21-43) per component
+                vec2<T> *ya = out + ra * (m + 1);
+                if constexpr (NN == 2) {
+                    const vec2<T> s = vadd(x[0], x[1]), d = vsub(x[0], x[1]);
+                    ya[0] = {s.x, (T)0};
+                    ya[1] = {d.x, (T)0};
+                    if (has_b) {
+                        ya[2] = {s.y, (T)0};
+                        ya[3] = {d.y, (T)0};
+                    }
+                } else {
+                    vec2<T> dc[m + 1], ds[m - 1], C[m + 1], S[m - 1];
+                    dc[0] = x[0];
+                    dc[m] = x[m];
+#pragma unroll
+                    for (int n = 1; n < m; ++n) {
+                        dc[n] = vadd(x[n], x[NN - n]);
+                        ds[n - 1] = vsub(x[n], x[NN - n]);
+                    }
+                    dct0_reg<NN, T>(dc, C, sU);
+                    dst0_reg<NN, T>(ds, S, sU);
+#pragma unroll
+                    for (int k = 0; k <= m; ++k) {
+                        const bool edge = (k == 0) || (k == m);
+                        ya[k] = {C[k].x, edge ? (T)0 : -S[edge ? 0 : k - 1].x};
+                        if (has_b) ya[m + 1 + k] = {C[k].y, edge ? (T)0 : -S[edge ? 0 : k - 1].y};
+                    }
+                }
+            } else if constexpr (MODE == 2) {
+                vec2<T> C[m + 1];
+                dct0_reg<NN, T>(x, C, sU);
+                T *ya = reinterpret_cast<T *>(out) + ra * (m + 1);
+#pragma unroll
+                for (int k = 0; k <= m; ++k) {
+                    ya[k] = C[k].x;
+                    if (has_b) ya[m + 1 + k] = C[k].y;
+                }
+            } else {
+                vec2<T> S[RL];
+                dst0_reg<NN, T>(x, S, sU);
+                T *ya = reinterpret_cast<T *>(out) + ra * RL;
+#pragma unroll
+                for (int k = 0; k < RL; ++k) {
+                    ya[k] = S[k].x;
+                    if (has_b) ya[RL + k] = S[k].y;
+                }
+            }
+        }
     }
 }
 
@@ -255,10 +314,13 @@ QFT_DEV void unit_rest(vec2<T> *w, const T *U, const T *kcu, int lane) {
     run_c_blocks<LOG2N, T, 1>(w, DST, lane);
 }
 
-template <int LOG2N, typename T>
+// MODE 0: complex cdft on (batch, N) complex rows.  MODE 1/2/3: rdft / dct0 /
+// dst0 on real rows (nreal rows of the mode's stored length), two rows per vec2
+// signal; `batch` then counts row pairs.
+template <int LOG2N, typename T, int MODE = 0>
 __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
     qft_cdft_smem(const vec2<T> *__restrict__ in, vec2<T> *__restrict__ out, long long batch,
-                  const T *__restrict__ Ug, const __grid_constant__ LeeConst<T> kc) {
+                  const T *__restrict__ Ug, const __grid_constant__ LeeConst<T> kc, long long nreal = 0) {
     using P = SPlan<LOG2N>;
     using K = KCfg<LOG2N, T>;
     constexpr int TT = K::TT, NT = K::NT, NW = K::NW;
@@ -283,7 +345,7 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
     __syncthreads();
     long long bt = blockIdx.x;
 #if QFT_A0_TMA
-    if (tid == 0 && bt < nbatch) {
+    if (MODE == 0 && tid == 0 && bt < nbatch) {
         const long long nt = (batch - bt * TT) < TT ? (batch - bt * TT) : TT;
         tma_bulk_load(stage, in + bt * TT * P::N, (uint32_t)(nt * P::N * K::VB), bar);
     }
@@ -292,8 +354,10 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
     for (; bt < nbatch; bt += gridDim.x) {
         const int ntr = (int)((batch - bt * TT) < TT ? (batch - bt * TT) : TT);
 #if QFT_A0_TMA
-        mbar_wait(bar, parity);
-        parity ^= 1u;
+        if constexpr (MODE == 0) {
+            mbar_wait(bar, parity);
+            parity ^= 1u;
+        }
 #else
         // pull the next batch into L2 while this one is transformed
         if (tid == 0 && bt + gridDim.x < nbatch) {
@@ -304,6 +368,16 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
         const vec2<T> *stage = in + bt * TT * P::N;  // A0 reads global memory directly
 #endif
         // A0: fold + route, staging -> W
+        if constexpr (MODE != 0) {
+            // real modes: rows of the mode's stored length straight from global memory
+            constexpr int RL = MODE == 1 ? P::N : (MODE == 2 ? P::m + 1 : P::m - 1);
+            const T *xr = reinterpret_cast<const T *>(in);
+            for (int tau = 0; tau < ntr; ++tau) {
+                const long long ra = 2 * (bt * TT + tau), rb = ra + 1 < nreal ? ra + 1 : ra;
+                for (int nn = tid; nn <= P::m; nn += NT)
+                    a0_item_real<LOG2N, T, MODE>(xr + ra * RL, xr + rb * RL, W + tau * P::PADDED, nn);
+            }
+        } else {
 #if QFT_A0_UNIT8
         for (int it = tid; it < TT * (P::m / 8); it += NT) {
             const int tau = it / (P::m / 8), k = it - tau * (P::m / 8);
@@ -376,10 +450,11 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
 #endif  // QFT_A0_TMA
         }
 #endif  // QFT_A0_UNIT8
+        }
         __syncthreads();
 #if QFT_A0_TMA
         // the staging buffer is free: prefetch the next batch while we compute
-        if (tid == 0 && bt + gridDim.x < nbatch) {
+        if (MODE == 0 && tid == 0 && bt + gridDim.x < nbatch) {
             const long long nb = bt + gridDim.x;
             const long long nt = (batch - nb * TT) < TT ? (batch - nb * TT) : TT;
             tma_bulk_load(stage, in + nb * TT * P::N, (uint32_t)(nt * P::N * K::VB), bar);
@@ -392,6 +467,7 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
             if (tau >= ntr) continue;
             vec2<T> *w = W + tau * P::PADDED;
             const bool dst = kind & 1;
+            if ((MODE == 2 && dst) || (MODE == 3 && !dst)) continue;  // side not needed
             if (K::NU == 4 && kind < 2) {
                 if (dst) unit_block0<LOG2N, T, true>(w, U, kc.u, lane);
                 else unit_block0<LOG2N, T, false>(w, U, kc.u, lane);
@@ -478,7 +554,33 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
         // D: chain + recombination -> global
         for (int it = tid; it < TT * P::DT; it += NT) {
             const int tau = it / P::DT, t = it - tau * P::DT;
-            if (tau < ntr) Chain<LOG2N, T>::unit(W + tau * P::PADDED, out + (bt * TT + tau) * P::N, t);
+            if (tau >= ntr) continue;
+            if constexpr (MODE == 0) {
+                Chain<LOG2N, T>::unit(W + tau * P::PADDED, out + (bt * TT + tau) * P::N, t);
+            } else {
+                // per-signal outputs: rdft packed half spectrum (shared.py:38-43 with
+                // complex_from_packed, shared.py:94-101), dct0 / dst0 real spectra
+                const long long ra = 2 * (bt * TT + tau);
+                const bool has_b = ra + 1 < nreal;
+                auto emit = [&](int k, vec2<T> cv, vec2<T> sv) {
+                    if constexpr (MODE == 1) {
+                        vec2<T> *ya = out + ra * (P::m + 1);
+                        const bool edge = (k == 0) || (k == P::m);
+                        ya[k] = {cv.x, edge ? (T)0 : -sv.x};
+                        if (has_b) ya[P::m + 1 + k] = {cv.y, edge ? (T)0 : -sv.y};
+                    } else if constexpr (MODE == 2) {
+                        T *ya = reinterpret_cast<T *>(out) + ra * (P::m + 1);
+                        ya[k] = cv.x;
+                        if (has_b) ya[P::m + 1 + k] = cv.y;
+                    } else {
+                        if (k == 0 || k == P::m) return;
+                        T *ya = reinterpret_cast<T *>(out) + ra * (P::m - 1);
+                        ya[k - 1] = sv.x;
+                        if (has_b) ya[P::m - 1 + k - 1] = sv.y;
+                    }
+                };
+                Chain<LOG2N, T>::unit_e(W + tau * P::PADDED, emit, t);
+            }
         }
         __syncthreads();
     }
@@ -486,10 +588,10 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
 
 inline int smem_bytes_for_cfg(int smem) { return smem; }
 
-template <int LOG2N, typename T>
+template <int LOG2N, typename T, int MODE = 0>
 cudaError_t launch_smem(const LaunchArgs &a) {
     using K = KCfg<LOG2N, T>;
-    auto kern = qft_cdft_smem<LOG2N, T>;
+    auto kern = qft_cdft_smem<LOG2N, T, MODE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -503,21 +605,21 @@ cudaError_t launch_smem(const LaunchArgs &a) {
     LeeConst<T> kc;
     for (int i = 0; i < 32; ++i) kc.u[i] = ((const T *)a.Uhead)[i];
     kern<<<(unsigned)grid, K::NT, K::SMEM, a.stream>>>((const vec2<T> *)a.in, (vec2<T> *)a.out, a.batch,
-                                                       (const T *)a.U, kc);
+                                                       (const T *)a.U, kc, a.nreal);
     return cudaGetLastError();
 }
 
 template <int LOG2N, typename T>
 constexpr int smem_config_bytes() { return KCfg<LOG2N, T>::SMEM; }
 
-template <int NN, typename T>
+template <int NN, typename T, int MODE = 0>
 cudaError_t launch_reg(const LaunchArgs &a) {
     long long blocks = (a.batch + 127) / 128;
     long long cap = (long long)a.num_sms * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    qft_cdft_reg<NN, T><<<(unsigned)blocks, 128, 0, a.stream>>>((const vec2<T> *)a.in, (vec2<T> *)a.out, a.batch,
-                                                                (const T *)a.U);
+    qft_cdft_reg<NN, T, MODE><<<(unsigned)blocks, 128, 0, a.stream>>>((const vec2<T> *)a.in, (vec2<T> *)a.out,
+                                                                      a.batch, (const T *)a.U, a.nreal);
     return cudaGetLastError();
 }
 

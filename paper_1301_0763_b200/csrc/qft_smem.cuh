@@ -154,6 +154,37 @@ QFT_HD void a0_chunk64(const vec2<T> *x, vec2<T> *w, int c, int l, A0Lane64 a, S
     }
 }
 
+// ---------------------------------------------------------------- modes
+// MODE 0 cdft (complex signals), 1 rdft, 2 dct0, 3 dst0.  For the real modes two
+// real signals a, b ride in one vec2 (both follow the identical DAG).
+// A0 item n in [0, m] of a real pair (rows xa, xb of the mode's stored length).
+template <int LOG2N, typename T, int MODE>
+QFT_HD void a0_item_real(const T *xa, const T *xb, vec2<T> *w, int n) {
+    using P = SPlan<LOG2N>;
+    auto at = [&](int i) { return vec2<T>{xa[i], xb[i]}; };
+    auto cell_of = [&](int nn) {
+        const int j = ctz32((uint32_t)nn);
+        return P::m - (1 << (LOG2N - 1 - j)) + (nn >> (j + 1));
+    };
+    if constexpr (MODE == 1) {  // rdft: fold x[n] +- x[N-n] (shared.py:28-35)
+        if (n == 0) {
+            w[padx(P::BASE)] = at(0);
+            w[padx(P::BASE + 1)] = at(P::m);
+        } else if (n < P::m) {
+            const vec2<T> a = at(n), b = at(P::N - n);
+            const int c = cell_of(n);
+            w[padx(c)] = vadd(a, b);
+            w[padx(P::S0 + c)] = vsub(a, b);
+        }
+    } else if constexpr (MODE == 2) {  // dct0: values s(0..m) are the cosine signal
+        if (n == 0) w[padx(P::BASE)] = at(0);
+        else if (n == P::m) w[padx(P::BASE + 1)] = at(P::m);
+        else w[padx(cell_of(n))] = at(n);
+    } else {  // dst0: values s(1..m-1) are the sine signal (slot n-1)
+        if (n > 0 && n < P::m) w[padx(P::S0 + cell_of(n))] = at(n - 1);
+    }
+}
+
 template <int LOG2N, typename T>
 QFT_HD void a0_unit8(const vec2<T> *x, vec2<T> *w, int k) {
     using P = SPlan<LOG2N>;
@@ -459,25 +490,30 @@ struct Chain {
         if (!edge) y[P::N - k] = vsub(cv, u);
     }
     // unfold with self-paired indices (k == q_j) duplicated: both children get
-    // the C copy / S leaf and write identical values
-    template <int J>
-    static QFT_HD void up_u(const vec2<T> *w, vec2<T> *y, int k, vec2<T> cv, vec2<T> sv) {
+    // the C copy / S leaf and write identical values.  emit(k, C_0[k], S_0[k]).
+    template <int J, class Emit>
+    static QFT_HD void up_e(const vec2<T> *w, Emit &emit, int k, vec2<T> cv, vec2<T> sv) {
         if constexpr (J == 0) {
-            emit_u(y, k, cv, sv);
+            emit(k, cv, sv);
         } else {
             constexpr int q = qj(J - 1), mm = 2 * q;
             const bool self = (k == q);
             const vec2<T> o = OC(w, J - 1, k < q ? k : 0);
             const vec2<T> os = OS(w, J - 1, k > 0 ? k : 1);
-            up_u<J - 1>(w, y, k, self ? cv : vadd(cv, o), self ? os : vadd(os, sv));
-            up_u<J - 1>(w, y, self ? q : mm - k, self ? cv : vsub(cv, o), self ? os : vsub(os, sv));
+            up_e<J - 1>(w, emit, k, self ? cv : vadd(cv, o), self ? os : vadd(os, sv));
+            up_e<J - 1>(w, emit, self ? q : mm - k, self ? cv : vsub(cv, o), self ? os : vsub(os, sv));
         }
     }
 
-    static QFT_HD void unit(const vec2<T> *w, vec2<T> *y, int t) {
+    template <class Emit>
+    static QFT_HD void unit_e(const vec2<T> *w, Emit &emit, int t) {
         vec2<T> cv, sv;
         if constexpr (P::RC < n - 1) desc2<P::RC>(w, t, cv, sv);
-        up_u<P::RC>(w, y, t, cv, sv);
+        up_e<P::RC>(w, emit, t, cv, sv);
+    }
+    static QFT_HD void unit(const vec2<T> *w, vec2<T> *y, int t) {
+        auto emit = [&](int k, vec2<T> cv, vec2<T> sv) { emit_u(y, k, cv, sv); };
+        unit_e(w, emit, t);
     }
 };
 

@@ -14,8 +14,10 @@ dtype rule, layout and errors (/root/reference/pkg/src/quickfourier/improved.py:
 
 numpy inputs go through the C-ABI host path (H2D, transform, D2H); a CUDA
 ``torch.Tensor`` stays on its device.  ``cdft_rows`` is the batch-major fast
-path ((batch, N) tensor, transform along the last axis).  There is no CPU
-fallback: without the CUDA library or a GPU these functions raise.
+path ((batch, N) tensor, transform along the last axis).  ``rdft``, ``dct0`` and
+``dst0`` (improved.py:117-136) run the same kernels on real rows, two rows per
+complex lane (``qft_exec_real``; N <= 4096).  There is no CPU fallback: without
+the CUDA library or a GPU these functions raise.
 """
 
 import weakref
@@ -23,7 +25,7 @@ import weakref
 import numpy as np
 
 from . import _native
-from .counting import OpCounter, improved_cdft_counts, natural_constants
+from .counting import OpCounter, improved_cdft_counts, improved_real_counts, natural_constants
 
 __all__ = ["cdft", "cdft_rows", "rdft", "dct0", "dst0"]
 
@@ -163,25 +165,67 @@ def cdft_rows(x, table=None, counter=None, out=None):
     return out
 
 
-def _not_built(name):
-    raise NotImplementedError(
-        f"improved.{name} has no sm_100a kernel yet (next in SURVEY.md §8(f)); "
-        "there is no CPU fallback by design")
+_KINDS = {"rdft": (_native.QFT_KIND_RDFT, 2), "dct0": (_native.QFT_KIND_DCT0, 2), "dst0": (_native.QFT_KIND_DST0, 4)}
+
+
+def _real(values, table, counter, kind):
+    """classical._prep_real (classical.py:48-61) + the device transform."""
+    import torch
+    code, min_n = _KINDS[kind]
+    on_dev = _is_torch(values) and values.is_cuda
+    if _is_torch(values):
+        t = values
+        if t.dtype not in (torch.float32, torch.float64):
+            t = t.to(torch.float64)
+        dt = np.float32 if t.dtype == torch.float32 else np.float64
+    else:
+        x = np.asarray(values)
+        if x.dtype not in (np.float32, np.float64):
+            x = x.astype(np.float64)
+        dt = x.dtype.type
+    shape = tuple(t.shape) if _is_torch(values) else x.shape
+    n_vals = shape[0] if len(shape) else 0
+    N = {"rdft": n_vals, "dct0": 2 * (n_vals - 1), "dst0": 2 * (n_vals + 1)}[kind]
+    if N < min_n or N & (N - 1):
+        raise ValueError(f"stored length {n_vals} does not give a power-of-two periodization >= {min_n}")
+    batch_shape = shape[1:]
+    B = int(np.prod(batch_shape)) if batch_shape else 1
+    p = _native.plan(N.bit_length() - 1, 32 if dt == np.float32 else 64, ALGO,
+                     (values.device.index or 0) if on_dev else 0)
+    dev = values.device if on_dev else torch.device("cuda", p.device)
+    src = (t if _is_torch(values) else torch.from_numpy(np.ascontiguousarray(x))).to(dev)
+    rows = src.reshape(n_vals, B).t().contiguous()  # (B, stored length): batch-major rows
+    m = N // 2
+    if kind == "rdft":
+        out = torch.empty((B, m + 1), dtype=torch.complex64 if dt == np.float32 else torch.complex128, device=dev)
+    else:
+        out = torch.empty((B, n_vals), dtype=rows.dtype, device=dev)
+    with p.lock:
+        _apply_table(p, table, dt, N)
+        p.exec_real(code, rows.data_ptr(), out.data_ptr(), B, torch.cuda.current_stream(dev).cuda_stream)
+    if counter is not None:
+        adds, muls = improved_real_counts(kind, N)
+        counter.adds += adds * B
+        counter.muls += muls * B
+    res = out.t().reshape((out.shape[1],) + tuple(batch_shape))
+    if on_dev:
+        return res.contiguous()
+    return res.cpu().numpy().copy()
 
 
 def rdft(values, table=None, counter=None):
-    """Improved real-input DFT (improved.py:131-136) -- kernel not built yet."""
-    _not_built("rdft")
+    """Improved real-input DFT, reported for k = 0..N/2 (improved.py:131-136)."""
+    return _real(values, table, counter, "rdft")
 
 
 def dct0(values, table=None, counter=None):
-    """Improved cosine transform (improved.py:117-121) -- kernel not built yet."""
-    _not_built("dct0")
+    """Improved cosine transform; values are s(0)..s(N/2) (improved.py:117-121)."""
+    return _real(values, table, counter, "dct0")
 
 
 def dst0(values, table=None, counter=None):
-    """Improved sine transform (improved.py:124-128) -- kernel not built yet."""
-    _not_built("dst0")
+    """Improved sine transform; values are s(1)..s(N/2-1) (improved.py:124-128)."""
+    return _real(values, table, counter, "dst0")
 
 
 # keep the reference's names importable from this module as well

@@ -110,6 +110,54 @@ static void emu_one(const vec2<T> *x, vec2<T> *y, const T *U) {
     for (int t = 0; t < P::DT; ++t) Chain<LOG2N, T>::unit(w, y, t);
 }
 
+// real modes (1 rdft, 2 dct0, 3 dst0) on one pair of rows (xa, xb)
+template <int LOG2N, typename T, int MODE>
+static void emu_real_one(const T *xa, const T *xb, T *ya, T *yb, const T *U) {
+    using P = SPlan<LOG2N>;
+    std::vector<vec2<T>> Wv(P::PADDED);
+    vec2<T> *w = Wv.data();
+    for (int n = 0; n <= P::m; ++n) a0_item_real<LOG2N, T, MODE>(xa, xb, w, n);
+    emu_f<LOG2N, T, 0>(w, U);
+    for (int k = 0; k < P::NL32; ++k) {
+        b_l32<false, T>(w, 32 * k, U);
+        b_l32<true, T>(w, P::S0 + 32 * k, U);
+    }
+    b_small<LOG2N, false, T>(w, U);
+    b_small<LOG2N, true, T>(w, U);
+    emu_c<LOG2N, T, 0>(w);
+    auto emit = [&](int k, vec2<T> cv, vec2<T> sv) {
+        if constexpr (MODE == 1) {
+            const bool edge = (k == 0) || (k == P::m);
+            ya[2 * k] = cv.x;
+            ya[2 * k + 1] = edge ? (T)0 : -sv.x;
+            yb[2 * k] = cv.y;
+            yb[2 * k + 1] = edge ? (T)0 : -sv.y;
+        } else if constexpr (MODE == 2) {
+            ya[k] = cv.x;
+            yb[k] = cv.y;
+        } else {
+            if (k == 0 || k == P::m) return;
+            ya[k - 1] = sv.x;
+            yb[k - 1] = sv.y;
+        }
+    };
+    for (int t = 0; t < P::DT; ++t) Chain<LOG2N, T>::unit_e(w, emit, t);
+}
+
+template <typename T, int MODE>
+static int emu_real_dispatch(int log2n, const T *xa, const T *xb, T *ya, T *yb, const T *U) {
+    switch (log2n) {
+        case 6: emu_real_one<6, T, MODE>(xa, xb, ya, yb, U); return 0;
+        case 7: emu_real_one<7, T, MODE>(xa, xb, ya, yb, U); return 0;
+        case 8: emu_real_one<8, T, MODE>(xa, xb, ya, yb, U); return 0;
+        case 9: emu_real_one<9, T, MODE>(xa, xb, ya, yb, U); return 0;
+        case 10: emu_real_one<10, T, MODE>(xa, xb, ya, yb, U); return 0;
+        case 11: emu_real_one<11, T, MODE>(xa, xb, ya, yb, U); return 0;
+        case 12: emu_real_one<12, T, MODE>(xa, xb, ya, yb, U); return 0;
+    }
+    return -1;
+}
+
 template <int NN, typename T>
 static void emu_reg(const vec2<T> *x, vec2<T> *y, const T *U) {
     cdft_reg<NN, T>(x, y, U);
@@ -235,7 +283,31 @@ static int emu_dispatch(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
     }
 }
 
+template <typename T>
+static int emu_real(int mode, int log2n, const T *x, T *y, long nrows, const T *Tnat) {
+    const int N = 1 << log2n, m = N / 2;
+    const int rl = mode == 1 ? N : (mode == 2 ? m + 1 : m - 1);
+    const int ol = mode == 1 ? 2 * (m + 1) : rl;
+    std::vector<T> U;
+    build_U(N, Tnat, U);
+    for (long r = 0; r + 1 < nrows; r += 2) {
+        const T *xa = x + r * rl, *xb = xa + rl;
+        T *ya = y + r * ol, *yb = ya + ol;
+        int rc = mode == 1 ? emu_real_dispatch<T, 1>(log2n, xa, xb, ya, yb, U.data())
+               : mode == 2 ? emu_real_dispatch<T, 2>(log2n, xa, xb, ya, yb, U.data())
+                           : emu_real_dispatch<T, 3>(log2n, xa, xb, ya, yb, U.data());
+        if (rc) return rc;
+    }
+    return 0;
+}
+
 extern "C" {
+int emu_real_f32(int mode, int log2n, const float *x, float *y, long nrows, const float *T) {
+    return emu_real<float>(mode, log2n, x, y, nrows, T);
+}
+int emu_real_f64(int mode, int log2n, const double *x, double *y, long nrows, const double *T) {
+    return emu_real<double>(mode, log2n, x, y, nrows, T);
+}
 // x, y: batch-major interleaved complex; Tnat: natural table for N (N >= 8)
 int emu_cdft_f64(int log2n, const double *x, double *y, long batch, const double *Tnat) {
     const int N = 1 << log2n;

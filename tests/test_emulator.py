@@ -44,3 +44,24 @@ def test_emulated_kernel_bitwise(emu, oracle_mod, dt, lg):
     fn = emu.emu_cdft_f32 if dt == np.complex64 else emu.emu_cdft_f64
     assert fn(lg, z.ctypes.data, y.ctypes.data, B, T.ctypes.data) == 0
     assert bit_equal(y, oracle_mod.cdft_rows(z))
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("lg", [6, 9, 12])
+@pytest.mark.parametrize("kind", ["rdft", "dct0", "dst0"])
+def test_emulated_real_modes_bitwise(emu, oracle_mod, dt, lg, kind):
+    """improved.rdft/dct0/dst0 through the same phase functions (two real rows per lane)."""
+    N, m = 1 << lg, 1 << (lg - 1)
+    rl = {"rdft": N, "dct0": m + 1, "dst0": m - 1}[kind]
+    rng = np.random.default_rng(lg)
+    x = rng.standard_normal((4, rl)).astype(dt)
+    fn = emu.emu_real_f32 if dt == np.float32 else emu.emu_real_f64
+    fn.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_long, ctypes.c_void_p]
+    T = oracle_mod.table(N, dt)
+    if kind == "rdft":
+        y = np.empty((4, m + 1), dtype=np.complex64 if dt == np.float32 else np.complex128)
+    else:
+        y = np.empty((4, rl), dtype=dt)
+    assert fn({"rdft": 1, "dct0": 2, "dst0": 3}[kind], lg, x.ctypes.data, y.ctypes.data, 4, T.ctypes.data) == 0
+    want = getattr(oracle_mod, kind)(np.ascontiguousarray(x.T)).T
+    assert bit_equal(y, np.ascontiguousarray(want))

@@ -211,3 +211,46 @@ def test_large_batch_properties(torch_cuda):
     ref = torch.fft.fft(x.to(torch.complex128), dim=1)
     rel = ((y.to(torch.complex128) - ref).abs().pow(2).sum(1).sqrt() / ref.abs().pow(2).sum(1).sqrt()).max()
     assert rel.item() < 1e-6 * 12
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("lg", list(range(1, 13)))
+@pytest.mark.parametrize("kind", ["rdft", "dct0", "dst0"])
+def test_real_entry_points_bitwise(torch_cuda, oracle_mod, dt, lg, kind):
+    """improved.rdft / dct0 / dst0 (improved.py:117-136) on the GPU, bit-identical."""
+    from paper_1301_0763_b200 import improved
+    N = 1 << lg
+    if kind == "dst0" and N < 4:
+        pytest.skip("the sine transform needs N >= 4")
+    n_vals = {"rdft": N, "dct0": N // 2 + 1, "dst0": N // 2 - 1}[kind]
+    rng = np.random.default_rng(lg * 7 + len(kind))
+    x = rng.standard_normal((n_vals, 5)).astype(dt)  # odd batch: the last lane pairs with nothing
+    got = getattr(improved, kind)(x)
+    want = getattr(oracle_mod, kind)(x)
+    assert got.dtype == want.dtype and got.shape == want.shape
+    assert bit_equal(got, want)
+    one = getattr(improved, kind)(x[:, 2])
+    assert bit_equal(one, want[:, 2])
+
+
+def test_real_entry_points_counts_and_errors(torch_cuda):
+    from paper_1301_0763_b200 import improved
+    from paper_1301_0763_b200.counting import OpCounter
+    c = OpCounter()
+    improved.rdft(np.random.default_rng(0).uniform(-0.5, 0.5, 16), counter=c)
+    assert (c.adds, c.muls) == (60, 10)   # the worked 16-point example (test_improved.py:81-87)
+    c = OpCounter()
+    improved.dct0(np.random.default_rng(0).uniform(-0.5, 0.5, 9), counter=c)
+    assert (c.adds, c.muls) == (27, 5)
+    c = OpCounter()
+    improved.dst0(np.random.default_rng(0).uniform(-0.5, 0.5, 7), counter=c)
+    assert (c.adds, c.muls) == (19, 5)
+    with pytest.raises(ValueError):
+        improved.rdft(np.zeros(12))
+    with pytest.raises(ValueError):
+        improved.dct0(np.zeros(4))
+    with pytest.raises(ValueError):
+        improved.dst0(np.zeros(2))
+    d = improved.dct0(np.array([1.0, 0, 0, 0, 0, 0, 0, 0, 1.0]))  # test_cli.py:10-16
+    assert np.array_equal(d, [2, 0, 2, 0, 2, 0, 2, 0, 2])
+    assert improved.rdft(np.zeros(8, dtype=np.int64)).dtype == np.complex128

@@ -78,7 +78,7 @@ def test_no_fused_multiply_add_in_transform_kernels():
 def test_sm100a_and_packed_fp32():
     funcs, out = sass_by_function()
     assert "sm_100a" in out
-    smem32 = [k for k in funcs if "qft_cdft_smem" in k and "ILi12EfE" in k]
+    smem32 = [k for k in funcs if "qft_cdft_smem" in k and "ILi12EfLi0E" in k]
     assert smem32, "fp32 N=4096 kernel missing"
     ops = funcs[smem32[0]]
     assert any(o.startswith("FADD2") for o, _, _ in ops), "fp32 adds should use the packed FADD2 pipe"
