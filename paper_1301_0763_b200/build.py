@@ -66,6 +66,8 @@ def build(jobs=None, verbose=True, defines=(), lib=None):
     for p in PRECS:
         units.append((os.path.join(CSRC, "qft_large.cu"), os.path.join(BUILD, f"large_{p}_{dig}.o"),
                       [f"QFT_LARGE_PREC={p}"] + list(defines)))
+        units.append((os.path.join(CSRC, "qft_classical.cu"), os.path.join(BUILD, f"classical_{p}_{dig}.o"),
+                      [f"QFT_CL_PREC={p}"] + list(defines)))
     for p in PRECS:
         for l in LOG2NS:
             units.append((os.path.join(CSRC, "qft_inst.cu"), os.path.join(BUILD, f"inst_{p}_{l}_{dig}.o"),

@@ -1,39 +1,60 @@
-"""Drop-in for ``quickfourier.classical`` (classical.py:134-167).
+"""Drop-in for ``quickfourier.classical`` (classical.py:134-167) -- the north
+star's "classical QFT for comparison" entry point, on the GPU.
 
-The classical QFT is the "for comparison" entry point of the north star and
-the next row of SURVEY.md §8(f).  Its sm_100a kernel is not built yet, so the
-transforms validate their arguments exactly like the reference and then raise
-``NotImplementedError``; there is no CPU fallback by design.
+Same signatures, dtype rules, layouts and errors as the improved drop-in
+(paper_1301_0763_b200.improved); the transforms run the classical recursion
+(harmonic parity first, classical.py:64-129) in the warp-cooperative kernel of
+csrc/qft_classical.cu, bit-identical to the reference.  ``counter`` receives
+the exact classical op counts; ``table`` supplies the half-secants (the
+classical footprint is the N/4 - 1 secant slots, counting.py:189-205).
 """
 
 import numpy as np
 
+from . import _native, improved
 from .counting import OpCounter  # noqa: F401  (reference-compatible import)
 
-__all__ = ["cdft", "rdft", "dct0", "dst0"]
+__all__ = ["cdft", "cdft_rows", "rdft", "dct0", "dst0"]
 
-
-def _not_built(name):
-    raise NotImplementedError(
-        f"classical.{name} has no sm_100a kernel yet (SURVEY.md §8(f) rank 1); "
-        "there is no CPU fallback by design")
+ALGO = _native.QFT_ALGO_CLASSICAL
 
 
 def cdft(values, table=None, counter=None):
-    z = np.asarray(values)
-    N = z.shape[0] if z.ndim else 0
-    if N < 2 or N & (N - 1):
-        raise ValueError(f"periodization must be a power of two >= 2, got {N}")
-    _not_built("cdft")
+    """Classical complex DFT, reported for k = 0..N-1 (classical.py:156-167)."""
+    if improved._is_torch(values):
+        return improved._cdft_torch(values, table, counter, ALGO)
+    return improved._cdft_numpy(values, table, counter, ALGO)
+
+
+def cdft_rows(x, table=None, counter=None, out=None):
+    """Batch-major (batch, N) CUDA tensor, transform along the last axis."""
+    import torch
+    if not (improved._is_torch(x) and x.is_cuda):
+        raise TypeError("cdft_rows expects a CUDA torch.Tensor of shape (batch, N)")
+    B, N = x.shape
+    improved._check_n(N)
+    dtype = np.float32 if x.dtype == torch.complex64 else np.float64
+    if out is None:
+        out = torch.empty((B, N), dtype=x.dtype, device=x.device)
+    p = _native.plan(N.bit_length() - 1, 32 if dtype == np.float32 else 64, ALGO, x.device.index or 0)
+    with p.lock:
+        improved._apply_table(p, table, dtype, N, classical=True)
+        p.exec_device(x.data_ptr(), out.data_ptr(), B, (x.stride(0), x.stride(1)), (out.stride(0), out.stride(1)),
+                      torch.cuda.current_stream(x.device).cuda_stream)
+    improved._count(counter, N, B, ALGO)
+    return out
 
 
 def rdft(values, table=None, counter=None):
-    _not_built("rdft")
+    """Classical real-input DFT, k = 0..N/2 (classical.py:146-151)."""
+    return improved._real(values, table, counter, "rdft", ALGO)
 
 
 def dct0(values, table=None, counter=None):
-    _not_built("dct0")
+    """Classical cosine transform; values are s(0)..s(N/2) (classical.py:134-138)."""
+    return improved._real(values, table, counter, "dct0", ALGO)
 
 
 def dst0(values, table=None, counter=None):
-    _not_built("dst0")
+    """Classical sine transform; values are s(1)..s(N/2-1) (classical.py:140-144)."""
+    return improved._real(values, table, counter, "dst0", ALGO)

@@ -66,6 +66,67 @@ def improved_real_counts(kind, N):
     return (3 * N * lg // 4 - 7 * N // 4 - lg + 3, N * lg // 4 - 3 * N // 4 + 1)
 
 
+def classical_counts(kind, N):
+    """(adds, muls) of classical.cdft/rdft/dct0/dst0, by replaying the integer
+    structure of the classical recursion (classical.py:64-129; shared.py:21-72)."""
+    from functools import lru_cache
+
+    @lru_cache(None)
+    def dct(n):
+        if n == 2:
+            return (2, 0)
+        q = n // 4
+        a, m = dct(n // 2)
+        b, k = dct_odd(n)
+        return (2 * q + a + b, m + k)
+
+    @lru_cache(None)
+    def dct_odd(n):
+        if n == 4:
+            return (0, 0)
+        if n == 8:
+            return (2, 1)
+        q, q2 = n // 4, n // 8
+        a, m = dct(n // 4)
+        b, k = dct_odd(n // 2)
+        return (2 * q2 + a + b + q, q + m + k)
+
+    @lru_cache(None)
+    def dst(n):
+        if n == 4:
+            return (0, 0)
+        q = n // 4
+        a, m = dst(n // 2)
+        b, k = dst_odd(n)
+        return (2 * (q - 1) + a + b, m + k)
+
+    @lru_cache(None)
+    def dst_odd(n):
+        if n == 4:
+            return (0, 0)
+        q = n // 4
+        a, m = dst(n // 2)
+        return (a + (q - 2) + q, (q - 1) + m)
+
+    def rdft(n):
+        if n == 2:
+            return (2, 0)
+        a, m = dct(n)
+        b, k = dst(n)
+        return (2 * (n // 2 - 1) + a + b, m + k)
+
+    if kind == "cdft":
+        if N == 2:
+            return (4, 0)
+        a, m = rdft(N)
+        return (2 * a + 2 * N - 4, 2 * m)
+    if kind == "rdft":
+        return rdft(N)
+    if kind == "dct0":
+        return dct(N)
+    return dst(N)
+
+
 def _cos_turns_wide(j, d, ftype):
     """cos(2 pi j/d) one tier above the working dtype."""
     if ftype is np.float32:

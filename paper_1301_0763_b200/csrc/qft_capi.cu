@@ -16,6 +16,14 @@
 #include "qft_launch.cuh"
 #include "qft_large_api.h"
 
+// classical QFT (qft_classical.cu, one translation unit per precision)
+long long qft_classical_arena_cells_f32(int N);
+long long qft_classical_arena_cells_f64(int N);
+int qft_classical_exec_f32(int mode, const void *in, void *out, long long units, long long nreal, int N, const void *T,
+                           void *arena, size_t arena_cells, int warps, cudaStream_t st);
+int qft_classical_exec_f64(int mode, const void *in, void *out, long long units, long long nreal, int N, const void *T,
+                           void *arena, size_t arena_cells, int warps, cudaStream_t st);
+
 using namespace qft;
 
 // ============================================================== errors
@@ -134,6 +142,9 @@ struct qft_plan {
     cudaStream_t streams[2] = {nullptr, nullptr};
     std::mutex mu;
     void *large = nullptr;      // multi-pass schedule (N > 4096)
+    void *d_T = nullptr;        // natural table T[0..N/4) on the device (classical recursion)
+    void *d_arena = nullptr;    // classical: per-warp scratch
+    size_t arena_bytes = 0;
     void *d_lscratch = nullptr; // its scratch (two buffers of N+2 cells per signal of a chunk)
     size_t lscratch_bytes = 0;
 };
@@ -171,6 +182,8 @@ static int launch_large(qft_plan *p, const void *in, void *out, long long batch,
     if (chunk > batch) chunk = batch;
     if (p->lscratch_bytes < per * (size_t)chunk) {
         if (p->d_lscratch) cudaFree(p->d_lscratch);
+    if (p->d_T) cudaFree(p->d_T);
+    if (p->d_arena) cudaFree(p->d_arena);
         p->d_lscratch = nullptr;
         p->lscratch_bytes = 0;
         CUDA_TRY(cudaMalloc(&p->d_lscratch, per * (size_t)chunk));
@@ -188,7 +201,33 @@ static int launch_large(qft_plan *p, const void *in, void *out, long long batch,
     return 0;
 }
 
+static int launch_classical(qft_plan *p, int mode, const void *in, void *out, long long units, long long nreal,
+                            cudaStream_t st) {
+    const bool f32 = p->prec == QFT_PREC_F32;
+    const long long cells = f32 ? qft_classical_arena_cells_f32(p->N) : qft_classical_arena_cells_f64(p->N);
+    const size_t vb = f32 ? 8 : 16;
+    long long warps = units < (long long)p->num_sms * 16 ? units : (long long)p->num_sms * 16;
+    // keep the arena below ~8 GiB
+    const long long cap = (long long)(((size_t)8 << 30) / ((size_t)cells * vb));
+    if (warps > cap) warps = cap;
+    if (warps < 1) warps = 1;
+    const size_t need = (size_t)warps * (size_t)cells * vb;
+    if (p->arena_bytes < need) {
+        if (p->d_arena) cudaFree(p->d_arena);
+        p->d_arena = nullptr;
+        p->arena_bytes = 0;
+        CUDA_TRY(cudaMalloc(&p->d_arena, need));
+        p->arena_bytes = need;
+    }
+    if (p->d_T == nullptr) return fail(QFT_EINVAL, "plan was not created for the classical algorithm");
+    int e = f32 ? qft_classical_exec_f32(mode, in, out, units, nreal, p->N, p->d_T, p->d_arena, cells, (int)warps, st)
+                : qft_classical_exec_f64(mode, in, out, units, nreal, p->N, p->d_T, p->d_arena, cells, (int)warps, st);
+    if (e) return fail(QFT_ECUDA, std::string("classical launch: ") + cudaGetErrorString((cudaError_t)e));
+    return 0;
+}
+
 static int launch_contig(qft_plan *p, const void *in, void *out, long long batch, cudaStream_t st) {
+    if (p->algo == QFT_ALGO_CLASSICAL) return launch_classical(p, 0, in, out, batch, 0, st);
     if (is_large(p)) return launch_large(p, in, out, batch, st);
     if (p->log2n < 1 || p->log2n > kMaxLog2N)
         return fail(QFT_EUNSUPPORTED, "periodization 2^" + std::to_string(p->log2n) + " not built yet");
@@ -212,7 +251,7 @@ int qft_plan_create(qft_plan **out, int log2n, int prec, int algo, int device) {
     *out = nullptr;
     if (log2n < 1 || log2n > 30) return fail(QFT_EINVAL, "periodization must be a power of two >= 2");
     if (prec != QFT_PREC_F32 && prec != QFT_PREC_F64) return fail(QFT_EINVAL, "prec must be 32 or 64");
-    if (algo != QFT_ALGO_IMPROVED) return fail(QFT_EUNSUPPORTED, "only the improved algorithm is built on the GPU");
+    if (algo != QFT_ALGO_IMPROVED && algo != QFT_ALGO_CLASSICAL) return fail(QFT_EINVAL, "unknown algorithm");
     if (!size_supported(log2n))
         return fail(QFT_EUNSUPPORTED, "periodization 2^" + std::to_string(log2n) + " not built yet");
     int ndev = 0;
@@ -246,7 +285,15 @@ int qft_plan_create(qft_plan **out, int log2n, int prec, int algo, int device) {
             cudaMemcpy(p->d_U, U.data(), p->u_bytes, cudaMemcpyHostToDevice) != cudaSuccess)
             rc = fail(QFT_ECUDA, "table upload failed");
     }
-    if (!rc && is_large(p)) {
+    if (!rc && algo == QFT_ALGO_CLASSICAL) {
+        const size_t tb = (size_t)(p->N >= 8 ? p->N / 4 : 1) * (prec == QFT_PREC_F32 ? 4 : 8);
+        const void *src = prec == QFT_PREC_F32 ? (const void *)p->t32.data() : (const void *)p->t64.data();
+        double zero[1] = {0};
+        if (cudaMalloc(&p->d_T, tb) != cudaSuccess ||
+            cudaMemcpy(p->d_T, p->N >= 8 ? src : (const void *)zero, p->N >= 8 ? tb : 1, cudaMemcpyHostToDevice) !=
+                cudaSuccess)
+            rc = fail(QFT_ECUDA, "table upload failed");
+    } else if (!rc && is_large(p)) {
         int e = prec == QFT_PREC_F32 ? qft_large_create_f32(log2n, &p->large) : qft_large_create_f64(log2n, &p->large);
         if (e) rc = fail(QFT_ECUDA, "multi-pass schedule upload failed");
     }
@@ -264,6 +311,8 @@ int qft_plan_destroy(qft_plan *p) {
     if (p->d_U) cudaFree(p->d_U);
     if (p->d_scratch) cudaFree(p->d_scratch);
     if (p->d_lscratch) cudaFree(p->d_lscratch);
+    if (p->d_T) cudaFree(p->d_T);
+    if (p->d_arena) cudaFree(p->d_arena);
     if (p->large) {
         if (p->prec == QFT_PREC_F32) qft_large_destroy_f32(p->large);
         else qft_large_destroy_f64(p->large);
@@ -284,6 +333,13 @@ int qft_plan_get_info(const qft_plan *p, qft_plan_info_t *info) {
     info->kernel_launches = 1;
     int cfg[3] = {0, 0, 0};
     if (p->log2n >= 1 && p->log2n <= kMaxLog2N) kCfg[p->prec == QFT_PREC_F32 ? 0 : 1][p->log2n](cfg);
+    if (p->algo == QFT_ALGO_CLASSICAL) {
+        info->passes = 0;  // recursion in a per-warp arena (L1/L2 resident), not HBM passes
+        info->kernel_launches = 1;
+        info->threads_per_cta = 128;
+        info->scratch_bytes = (int64_t)p->arena_bytes;
+        return 0;
+    }
     if (is_large(p)) {
         int passes = 0, launches = 0;
         if (p->prec == QFT_PREC_F32) qft_large_info_f32(p->large, &passes, &launches);
@@ -325,6 +381,7 @@ int qft_plan_set_table(qft_plan *p, const void *h_table) {
         level_table(p->N, p->t64, U);
         for (size_t i = 0; i < 32 && i < U.size(); ++i) p->uhead64[i] = U[i];
         CUDA_TRY(cudaMemcpy(p->d_U, U.data(), U.size() * sizeof(double), cudaMemcpyHostToDevice));
+        if (p->d_T) CUDA_TRY(cudaMemcpy(p->d_T, p->t64.data(), p->t64.size() * sizeof(double), cudaMemcpyHostToDevice));
     } else {
         const float *t = (const float *)h_table;
         p->t32.assign(t, t + p->N / 4);
@@ -332,6 +389,7 @@ int qft_plan_set_table(qft_plan *p, const void *h_table) {
         level_table(p->N, p->t32, U);
         for (size_t i = 0; i < 32 && i < U.size(); ++i) p->uhead32[i] = U[i];
         CUDA_TRY(cudaMemcpy(p->d_U, U.data(), U.size() * sizeof(float), cudaMemcpyHostToDevice));
+        if (p->d_T) CUDA_TRY(cudaMemcpy(p->d_T, p->t32.data(), p->t32.size() * sizeof(float), cudaMemcpyHostToDevice));
     }
     return 0;
 }
@@ -421,9 +479,10 @@ int qft_exec_real(const qft_plan *cp, int kind, const void *d_in, void *d_out, i
     if (kind == QFT_KIND_DST0 && p->log2n < 2) return fail(QFT_EINVAL, "the sine transform needs N >= 4");
     if (nrows == 0) return 0;
     if (d_in == d_out) return fail(QFT_EINVAL, "transform is out-of-place: d_in must differ from d_out");
-    if (p->log2n > kMaxLog2N) return fail(QFT_EUNSUPPORTED, "real transforms are built for N <= 4096");
     CUDA_TRY(cudaSetDevice(p->device));
     std::lock_guard<std::mutex> lk(p->mu);
+    if (p->algo == QFT_ALGO_CLASSICAL) return launch_classical(p, kind, d_in, d_out, (nrows + 1) / 2, nrows, (cudaStream_t)stream);
+    if (p->log2n > kMaxLog2N) return fail(QFT_EUNSUPPORTED, "improved real transforms are built for N <= 4096");
     LaunchArgs a{d_in, d_out, (nrows + 1) / 2, p->d_U,
                  p->prec == QFT_PREC_F32 ? (const void *)p->uhead32 : (const void *)p->uhead64, p->num_sms,
                  (cudaStream_t)stream, nrows};

@@ -25,7 +25,8 @@ import weakref
 import numpy as np
 
 from . import _native
-from .counting import OpCounter, improved_cdft_counts, improved_real_counts, natural_constants
+from .counting import (OpCounter, classical_counts, improved_cdft_counts, improved_real_counts,
+                       natural_constants)
 
 __all__ = ["cdft", "cdft_rows", "rdft", "dct0", "dst0"]
 
@@ -45,8 +46,11 @@ def _check_n(N):
 _table_cache = {}
 
 
-def _apply_table(p, table, dtype, N):
-    """classical._resolve (classical.py:34-45) for the device plan."""
+def _apply_table(p, table, dtype, N, classical=None):
+    """classical._resolve (classical.py:34-45) for the device plan.  The improved
+    run touches cos(2pi/8) and the N/4-1 secant slots, the classical run the
+    secant slots only (counting.py:189-205)."""
+    classical = (p.algo == _native.QFT_ALGO_CLASSICAL) if classical is None else classical
     if table is None:
         if getattr(p, "_custom", False):
             p.set_table(p._default)
@@ -56,21 +60,26 @@ def _apply_table(p, table, dtype, N):
         raise ValueError(f"table dtype {table.dtype} does not match input dtype {np.dtype(dtype)}")
     if N < 8:
         return  # no constant is used below eight points
-    key = (id(table), N)
+    key = (id(table), N, classical)
+    if not hasattr(p, "_default"):
+        p._default = p.table()
+        p._custom = False
     hit = _table_cache.get(key)
     if hit is not None and hit[0]() is table:
         vals, keys = hit[1], hit[2]
-        table.touched.update(keys)  # the reference logs these N/4 keys every run
+        table.touched.update(keys)  # the reference logs these keys every run
     else:
-        vals = natural_constants(table, N)  # logs the same keys as a side effect
-        keys = frozenset([("cos8",)] + [_ref_key(m, N) for m in range(1, N // 4)])
+        if classical:
+            vals = np.concatenate([p._default[:1], np.asarray(
+                [table.half_secant(m, N) for m in range(1, N // 4)], dtype=np.dtype(table.dtype))])
+            keys = frozenset(_ref_key(m, N) for m in range(1, N // 4))
+        else:
+            vals = natural_constants(table, N)  # logs the same keys as a side effect
+            keys = frozenset([("cos8",)] + [_ref_key(m, N) for m in range(1, N // 4)])
         try:
             _table_cache[key] = (weakref.ref(table), vals, keys)
         except TypeError:
             pass
-    if not hasattr(p, "_default"):
-        p._default = p.table()
-        p._custom = False
     if p._custom or not np.array_equal(vals.view(np.uint8), p._default.view(np.uint8)):
         p.set_table(vals)
         p._custom = not np.array_equal(vals.view(np.uint8), p._default.view(np.uint8))
@@ -82,10 +91,13 @@ def _ref_key(m, N):
     return ("sec", m // g, N // g)
 
 
-def _count(counter, N, batch):
+def _count(counter, N, batch, algo=_native.QFT_ALGO_IMPROVED, kind="cdft"):
     if counter is None:
         return
-    adds, muls = improved_cdft_counts(N)
+    if algo == _native.QFT_ALGO_IMPROVED:
+        adds, muls = improved_cdft_counts(N) if kind == "cdft" else improved_real_counts(kind, N)
+    else:
+        adds, muls = classical_counts(kind, N)
     counter.adds += adds * batch
     counter.muls += muls * batch
 
@@ -109,7 +121,7 @@ def _cdft_numpy(values, table, counter, algo):
         else:
             strides = (1, B)  # (N, batch): element stride = batch
         p.exec_host(zc.ctypes.data, out.ctypes.data, B, strides, strides)
-    _count(counter, N, B)
+    _count(counter, N, B, algo)
     return out.reshape((N,) + batch_shape)
 
 
@@ -131,7 +143,7 @@ def _cdft_torch(t, table, counter, algo):
     with p.lock:
         _apply_table(p, table, dtype, N)
         p.exec_device(x.data_ptr(), out.data_ptr(), B, (x.stride(1), x.stride(0)), (1, B), stream)
-    _count(counter, N, B)
+    _count(counter, N, B, algo)
     return out.reshape((N,) + batch_shape)
 
 
@@ -168,7 +180,7 @@ def cdft_rows(x, table=None, counter=None, out=None):
 _KINDS = {"rdft": (_native.QFT_KIND_RDFT, 2), "dct0": (_native.QFT_KIND_DCT0, 2), "dst0": (_native.QFT_KIND_DST0, 4)}
 
 
-def _real(values, table, counter, kind):
+def _real(values, table, counter, kind, algo=ALGO):
     """classical._prep_real (classical.py:48-61) + the device transform."""
     import torch
     code, min_n = _KINDS[kind]
@@ -190,7 +202,7 @@ def _real(values, table, counter, kind):
         raise ValueError(f"stored length {n_vals} does not give a power-of-two periodization >= {min_n}")
     batch_shape = shape[1:]
     B = int(np.prod(batch_shape)) if batch_shape else 1
-    p = _native.plan(N.bit_length() - 1, 32 if dt == np.float32 else 64, ALGO,
+    p = _native.plan(N.bit_length() - 1, 32 if dt == np.float32 else 64, algo,
                      (values.device.index or 0) if on_dev else 0)
     dev = values.device if on_dev else torch.device("cuda", p.device)
     src = (t if _is_torch(values) else torch.from_numpy(np.ascontiguousarray(x))).to(dev)
@@ -203,10 +215,7 @@ def _real(values, table, counter, kind):
     with p.lock:
         _apply_table(p, table, dt, N)
         p.exec_real(code, rows.data_ptr(), out.data_ptr(), B, torch.cuda.current_stream(dev).cuda_stream)
-    if counter is not None:
-        adds, muls = improved_real_counts(kind, N)
-        counter.adds += adds * B
-        counter.muls += muls * B
+    _count(counter, N, B, algo, kind)
     res = out.t().reshape((out.shape[1],) + tuple(batch_shape))
     if on_dev:
         return res.contiguous()

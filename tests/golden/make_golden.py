@@ -121,6 +121,20 @@ def main():
         improved.cdft(golden_input(N, 2, np.complex128, 7), counter=c)
         counts[str(N)] = [c.adds, c.muls]
     meta["cdft_counts_batch2"] = counts
+    ccounts = {}
+    for lg in range(1, 13):
+        N = 1 << lg
+        for kind in ("cdft", "rdft", "dct0", "dst0"):
+            if kind == "dst0" and N < 4:
+                continue
+            n_vals = {"cdft": N, "rdft": N, "dct0": N // 2 + 1, "dst0": N // 2 - 1}[kind]
+            x = np.random.default_rng(1).uniform(-0.5, 0.5, n_vals)
+            if kind == "cdft":
+                x = x + 1j * x
+            c = OpCounter()
+            getattr(classical, kind)(x, counter=c)
+            ccounts[f"{kind}_{N}"] = [c.adds, c.muls]
+    meta["classical_counts"] = ccounts
     table = build_trig_table("improved", 64, np.float64)
     improved.cdft(golden_input(64, 1, np.complex128, 1)[:, 0], table=table, counter=OpCounter())
     meta["touched_64"] = sorted([list(k) for k in table.touched])

@@ -254,3 +254,61 @@ def test_real_entry_points_counts_and_errors(torch_cuda):
     d = improved.dct0(np.array([1.0, 0, 0, 0, 0, 0, 0, 0, 1.0]))  # test_cli.py:10-16
     assert np.array_equal(d, [2, 0, 2, 0, 2, 0, 2, 0, 2])
     assert improved.rdft(np.zeros(8, dtype=np.int64)).dtype == np.complex128
+
+
+@pytest.mark.parametrize("dt", [np.complex64, np.complex128])
+@pytest.mark.parametrize("lg", [1, 2, 3, 4, 5, 6, 8, 10, 12, 14])
+def test_classical_cdft_bitwise(torch_cuda, oracle_mod, dt, lg):
+    """classical.cdft (classical.py:156-167) on the GPU, bit-identical to the oracle."""
+    from paper_1301_0763_b200 import classical
+    N = 1 << lg
+    rng = np.random.default_rng(lg + 50)
+    z = (rng.standard_normal((N, 3)) + 1j * rng.standard_normal((N, 3))).astype(dt)
+    got = classical.cdft(z)
+    assert got.dtype == dt
+    assert bit_equal(got, oracle_mod.cdft(z, algo="classical"))
+
+
+def test_classical_golden_digests_and_semantics(golden, torch_cuda, oracle_mod):
+    from paper_1301_0763_b200 import classical
+    from paper_1301_0763_b200.counting import OpCounter, build_trig_table
+    _, meta = golden
+    for tag, dt in (("c128", np.complex128), ("c64", np.complex64)):
+        for lg in (5, 9, 12):
+            e = meta["cdft_sha256"][f"classical_{tag}_{1 << lg}"]
+            z = golden_input(1 << lg, e["batch"], dt, e["seed"])
+            assert sha(classical.cdft(z)) == e["sha256"]
+    z = config1_input()
+    assert sha(classical.cdft(z)) == meta["config1"]["classical_sha256"]
+    c = OpCounter()
+    classical.cdft(golden_input(64, 2, np.complex128, 3), counter=c)
+    assert [c.adds, c.muls] == [2 * v for v in meta["classical_counts"]["cdft_64"]]
+    t = build_trig_table("classical", 256, np.float64)
+    classical.cdft(golden_input(256, 1, np.complex128, 3)[:, 0], table=t)
+    assert t.touched_count() == 256 // 4 - 1   # classical footprint (test_acceptance.py criterion 5)
+
+
+@pytest.mark.parametrize("kind", ["rdft", "dct0", "dst0"])
+@pytest.mark.parametrize("lg", [3, 7, 11])
+def test_classical_real_entry_points(torch_cuda, oracle_mod, kind, lg):
+    from paper_1301_0763_b200 import classical
+    N = 1 << lg
+    n_vals = {"rdft": N, "dct0": N // 2 + 1, "dst0": N // 2 - 1}[kind]
+    for dt in (np.float32, np.float64):
+        x = np.random.default_rng(lg).standard_normal((n_vals, 3)).astype(dt)
+        assert bit_equal(getattr(classical, kind)(x), getattr(oracle_mod, kind)(x, algo="classical"))
+
+
+def test_classical_config4_accuracy_comparison(torch_cuda, oracle_mod):
+    """config 4's comparison: improved vs classical on the GPU at N=2^20 fp64."""
+    torch = torch_cuda
+    from paper_1301_0763_b200 import classical, improved, workloads
+    z = workloads.uniform_rows(1 << 20, 2, seed=4)
+    x = torch.from_numpy(z).cuda()
+    yi = improved.cdft_rows(x).cpu().numpy()
+    yc = classical.cdft_rows(x).cpu().numpy()
+    assert bit_equal(yc[:1], oracle_mod.cdft_rows(z[:1], algo="classical"))
+    ref = np.fft.fft(z, axis=1)
+    ei = np.linalg.norm(yi - ref) / np.linalg.norm(ref)
+    ec = np.linalg.norm(yc - ref) / np.linalg.norm(ref)
+    assert ei < 1e-12 and ec < 1e-12

@@ -61,3 +61,11 @@ def test_table_errors():
         TrigTable().half_secant(4, 16)
     with pytest.raises(ValueError):
         build_trig_table("fancy", 16)
+
+
+def test_classical_counts_replay_matches_reference(golden):
+    from paper_1301_0763_b200.counting import classical_counts
+    _, meta = golden
+    for key, (adds, muls) in meta["classical_counts"].items():
+        kind, N = key.split("_")
+        assert classical_counts(kind, int(N)) == (adds, muls), key
