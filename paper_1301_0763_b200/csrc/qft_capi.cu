@@ -220,6 +220,14 @@ static int launch_classical(qft_plan *p, int mode, const void *in, void *out, lo
         p->arena_bytes = need;
     }
     if (p->d_T == nullptr) return fail(QFT_EINVAL, "plan was not created for the classical algorithm");
+    // the recursion is ~2 lg N calls deep with ~128-byte frames: raise the
+    // per-thread stack once (the default 1 KB overflows from N = 64)
+    {
+        size_t cur = 0;
+        const size_t need = (size_t)(2 * p->log2n + 16) * 192;
+        CUDA_TRY(cudaDeviceGetLimit(&cur, cudaLimitStackSize));
+        if (cur < need) CUDA_TRY(cudaDeviceSetLimit(cudaLimitStackSize, need));
+    }
     int e = f32 ? qft_classical_exec_f32(mode, in, out, units, nreal, p->N, p->d_T, p->d_arena, cells, (int)warps, st)
                 : qft_classical_exec_f64(mode, in, out, units, nreal, p->N, p->d_T, p->d_arena, cells, (int)warps, st);
     if (e) return fail(QFT_ECUDA, std::string("classical launch: ") + cudaGetErrorString((cudaError_t)e));
