@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 PRECS = (32, 64)
-LOG2NS = range(1, 13)
+LOG2NS = range(1, 15)
 
 
 def nvcc():

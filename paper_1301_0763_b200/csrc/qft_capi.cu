@@ -7,6 +7,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -141,7 +142,8 @@ struct qft_plan {
     size_t scratch_bytes = 0;
     cudaStream_t streams[2] = {nullptr, nullptr};
     std::mutex mu;
-    void *large = nullptr;      // multi-pass schedule (N > 4096)
+    void *large = nullptr;      // multi-pass schedule
+    bool multipass = false;     // served by the multi-pass schedule
     void *d_T = nullptr;        // natural table T[0..N/4) on the device (classical recursion)
     void *d_arena = nullptr;    // classical: per-warp scratch
     size_t arena_bytes = 0;
@@ -153,25 +155,37 @@ struct qft_plan {
 #define QFT_DECL(P, L) int qft_inst_launch_##P##_##L(const LaunchArgs *, int); void qft_inst_cfg_##P##_##L(int *);
 #define QFT_DECL_ALL(P) \
     QFT_DECL(P, 1) QFT_DECL(P, 2) QFT_DECL(P, 3) QFT_DECL(P, 4) QFT_DECL(P, 5) QFT_DECL(P, 6) QFT_DECL(P, 7) \
-    QFT_DECL(P, 8) QFT_DECL(P, 9) QFT_DECL(P, 10) QFT_DECL(P, 11) QFT_DECL(P, 12)
+    QFT_DECL(P, 8) QFT_DECL(P, 9) QFT_DECL(P, 10) QFT_DECL(P, 11) QFT_DECL(P, 12) QFT_DECL(P, 13) QFT_DECL(P, 14)
 QFT_DECL_ALL(32)
 QFT_DECL_ALL(64)
 typedef int (*launch_fn)(const LaunchArgs *, int);
 #define QFT_ROW(P)                                                                                              \
     {nullptr, qft_inst_launch_##P##_1, qft_inst_launch_##P##_2, qft_inst_launch_##P##_3, qft_inst_launch_##P##_4, \
      qft_inst_launch_##P##_5, qft_inst_launch_##P##_6, qft_inst_launch_##P##_7, qft_inst_launch_##P##_8,         \
-     qft_inst_launch_##P##_9, qft_inst_launch_##P##_10, qft_inst_launch_##P##_11, qft_inst_launch_##P##_12}
-static const launch_fn kLaunch[2][13] = {QFT_ROW(32), QFT_ROW(64)};
+     qft_inst_launch_##P##_9, qft_inst_launch_##P##_10, qft_inst_launch_##P##_11, qft_inst_launch_##P##_12,     \
+     qft_inst_launch_##P##_13, qft_inst_launch_##P##_14}
+static const launch_fn kLaunch[2][15] = {QFT_ROW(32), QFT_ROW(64)};
 typedef void (*cfg_fn)(int *);
 #define QFT_CROW(P)                                                                                   \
     {nullptr, qft_inst_cfg_##P##_1, qft_inst_cfg_##P##_2, qft_inst_cfg_##P##_3, qft_inst_cfg_##P##_4,   \
      qft_inst_cfg_##P##_5, qft_inst_cfg_##P##_6, qft_inst_cfg_##P##_7, qft_inst_cfg_##P##_8,             \
-     qft_inst_cfg_##P##_9, qft_inst_cfg_##P##_10, qft_inst_cfg_##P##_11, qft_inst_cfg_##P##_12}
-static const cfg_fn kCfg[2][13] = {QFT_CROW(32), QFT_CROW(64)};
-static constexpr int kMaxLog2N = 12;
+     qft_inst_cfg_##P##_9, qft_inst_cfg_##P##_10, qft_inst_cfg_##P##_11, qft_inst_cfg_##P##_12,         \
+     qft_inst_cfg_##P##_13, qft_inst_cfg_##P##_14}
+static const cfg_fn kCfg[2][15] = {QFT_CROW(32), QFT_CROW(64)};
+static constexpr int kMaxLog2N = 14;  // largest single-pass instance (fp32; fp64 up to 13)
 
 static constexpr int kMaxLargeLog2N = 20;
-static bool is_large(const qft_plan *p) { return p->log2n > kMaxLog2N; }
+// single-pass shared-memory kernel built for (log2n, prec)
+static bool smem_available(int log2n, int prec) {
+    if (log2n < 1 || log2n > kMaxLog2N) return false;
+    if (log2n <= 12) return true;
+    int cfg[3] = {0, 0, 0};
+    kCfg[prec == QFT_PREC_F32 ? 0 : 1][log2n](cfg);
+    return cfg[0] > 0;
+}
+// multi-pass path: N beyond the single-pass kernels, or forced for N >= 2^13
+// by QFT_MULTIPASS=1 at plan creation (A/B comparisons and tests)
+static bool is_large(const qft_plan *p) { return p->multipass; }
 
 static int launch_large(qft_plan *p, const void *in, void *out, long long batch, cudaStream_t st) {
     // bound the scratch (two buffers of N+2 cells per signal) to ~2 GiB: chunk the batch
@@ -182,8 +196,6 @@ static int launch_large(qft_plan *p, const void *in, void *out, long long batch,
     if (chunk > batch) chunk = batch;
     if (p->lscratch_bytes < per * (size_t)chunk) {
         if (p->d_lscratch) cudaFree(p->d_lscratch);
-    if (p->d_T) cudaFree(p->d_T);
-    if (p->d_arena) cudaFree(p->d_arena);
         p->d_lscratch = nullptr;
         p->lscratch_bytes = 0;
         CUDA_TRY(cudaMalloc(&p->d_lscratch, per * (size_t)chunk));
@@ -237,7 +249,7 @@ static int launch_classical(qft_plan *p, int mode, const void *in, void *out, lo
 static int launch_contig(qft_plan *p, const void *in, void *out, long long batch, cudaStream_t st) {
     if (p->algo == QFT_ALGO_CLASSICAL) return launch_classical(p, 0, in, out, batch, 0, st);
     if (is_large(p)) return launch_large(p, in, out, batch, st);
-    if (p->log2n < 1 || p->log2n > kMaxLog2N)
+    if (!smem_available(p->log2n, p->prec))
         return fail(QFT_EUNSUPPORTED, "periodization 2^" + std::to_string(p->log2n) + " not built yet");
     LaunchArgs a{in, out, batch, p->d_U, p->prec == QFT_PREC_F32 ? (const void *)p->uhead32 : (const void *)p->uhead64,
                  p->num_sms, st};
@@ -272,6 +284,11 @@ int qft_plan_create(qft_plan **out, int log2n, int prec, int algo, int device) {
     p->prec = prec;
     p->algo = algo;
     p->device = device;
+    if (algo == QFT_ALGO_IMPROVED) {
+        const char *fm = getenv("QFT_MULTIPASS");
+        const bool force = fm && fm[0] == '1' && log2n >= 13;
+        p->multipass = force || !smem_available(log2n, prec);
+    }
     cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
     int rc = 0;
     if (prec == QFT_PREC_F64) {
@@ -340,7 +357,7 @@ int qft_plan_get_info(const qft_plan *p, qft_plan_info_t *info) {
     info->passes = 1;
     info->kernel_launches = 1;
     int cfg[3] = {0, 0, 0};
-    if (p->log2n >= 1 && p->log2n <= kMaxLog2N) kCfg[p->prec == QFT_PREC_F32 ? 0 : 1][p->log2n](cfg);
+    if (smem_available(p->log2n, p->prec)) kCfg[p->prec == QFT_PREC_F32 ? 0 : 1][p->log2n](cfg);
     if (p->algo == QFT_ALGO_CLASSICAL) {
         info->passes = 0;  // recursion in a per-warp arena (L1/L2 resident), not HBM passes
         info->kernel_launches = 1;
@@ -490,7 +507,8 @@ int qft_exec_real(const qft_plan *cp, int kind, const void *d_in, void *d_out, i
     CUDA_TRY(cudaSetDevice(p->device));
     std::lock_guard<std::mutex> lk(p->mu);
     if (p->algo == QFT_ALGO_CLASSICAL) return launch_classical(p, kind, d_in, d_out, (nrows + 1) / 2, nrows, (cudaStream_t)stream);
-    if (p->log2n > kMaxLog2N) return fail(QFT_EUNSUPPORTED, "improved real transforms are built for N <= 4096");
+    if (p->multipass || !smem_available(p->log2n, p->prec))
+        return fail(QFT_EUNSUPPORTED, "improved real transforms are built for N <= 16384 (fp32) / 8192 (fp64)");
     LaunchArgs a{d_in, d_out, (nrows + 1) / 2, p->d_U,
                  p->prec == QFT_PREC_F32 ? (const void *)p->uhead32 : (const void *)p->uhead64, p->num_sms,
                  (cudaStream_t)stream, nrows};

@@ -1,9 +1,11 @@
 // qft_inst.cu -- one (precision, N) instance of the transform kernels.
-// Compiled once per instance with -DQFT_INST_PREC={32,64} -DQFT_INST_LOG2N={1..12}.
+// Compiled once per instance with -DQFT_INST_PREC={32,64} -DQFT_INST_LOG2N={1..14}.
+// An instance whose working area does not fit in shared memory (fp64 N = 2^14)
+// reports cfg[0] = 0 and is served by the multi-pass path.
 #include "qft_launch.cuh"
 
 #if !defined(QFT_INST_PREC) || !defined(QFT_INST_LOG2N)
-#error "compile with -DQFT_INST_PREC=<32|64> -DQFT_INST_LOG2N=<1..12>"
+#error "compile with -DQFT_INST_PREC=<32|64> -DQFT_INST_LOG2N=<1..14>"
 #endif
 
 #define QFT_CAT3(a, b, c) a##_##b##_##c
@@ -19,6 +21,33 @@ using Real = double;
 
 #define QFT_CFGNAME(P, L) QFT_CAT3(qft_inst_cfg, P, L)
 
+namespace {
+// templates, so that the branch of an instance that does not fit is discarded
+template <int L, typename R>
+void smem_cfg(int *cfg) {
+    if constexpr (qft::smem_fits<L, R>()) {
+        using K = qft::KCfg<L, R>;
+        cfg[0] = K::SMEM;
+        cfg[1] = K::NT;
+        cfg[2] = K::TT;
+    } else {
+        cfg[0] = cfg[1] = cfg[2] = 0;
+    }
+}
+template <int L, typename R>
+int smem_launch(const qft::LaunchArgs *a, int mode) {
+    if constexpr (qft::smem_fits<L, R>()) {
+        switch (mode) {
+            case 0: return (int)qft::launch_smem<L, R, 0>(*a);
+            case 1: return (int)qft::launch_smem<L, R, 1>(*a);
+            case 2: return (int)qft::launch_smem<L, R, 2>(*a);
+            case 3: return (int)qft::launch_smem<L, R, 3>(*a);
+        }
+    }
+    return (int)cudaErrorInvalidValue;
+}
+}  // namespace
+
 // cfg[0] dynamic smem bytes, cfg[1] threads per CTA, cfg[2] signals per CTA iteration
 void QFT_CFGNAME(QFT_INST_PREC, QFT_INST_LOG2N)(int *cfg) {
 #if QFT_INST_LOG2N <= 5
@@ -26,10 +55,7 @@ void QFT_CFGNAME(QFT_INST_PREC, QFT_INST_LOG2N)(int *cfg) {
     cfg[1] = 128;
     cfg[2] = 1;
 #else
-    using K = qft::KCfg<QFT_INST_LOG2N, Real>;
-    cfg[0] = K::SMEM;
-    cfg[1] = K::NT;
-    cfg[2] = K::TT;
+    smem_cfg<QFT_INST_LOG2N, Real>(cfg);
 #endif
 }
 
@@ -46,12 +72,7 @@ int QFT_NAME(QFT_INST_PREC, QFT_INST_LOG2N)(const qft::LaunchArgs *a, int mode) 
             return (int)cudaErrorInvalidValue;
     }
 #else
-    switch (mode) {
-        case 0: return (int)qft::launch_smem<L, Real, 0>(*a);
-        case 1: return (int)qft::launch_smem<L, Real, 1>(*a);
-        case 2: return (int)qft::launch_smem<L, Real, 2>(*a);
-        case 3: return (int)qft::launch_smem<L, Real, 3>(*a);
-    }
+    return smem_launch<L, Real>(a, mode);
 #endif
     return (int)cudaErrorInvalidValue;
 }

@@ -1,9 +1,10 @@
 // qft_launch.cuh -- the batched transform kernels and their launchers.
 //   qft_cdft_reg   N <= 32     : one thread per signal, whole transform in registers
-//   qft_cdft_smem  N = 64..4096: persistent CTAs (1 per SM); each CTA transforms
+//   qft_cdft_smem  N = 64..16384: persistent CTAs (1 per SM); each CTA transforms
 //                                TT signals per iteration through the phases of
 //                                qft_smem.cuh while a TMA bulk copy prefetches the
-//                                next TT signals into a staging buffer
+//                                next TT signals into a staging buffer (or, when
+//                                the staging buffer does not fit, an L2 prefetch)
 // Each (precision, N) instance is compiled in its own translation unit
 // (qft_inst.cu) so the build parallelises.
 #pragma once
@@ -15,22 +16,10 @@
 #define QFT_CTAS_PER_SM 1  // shared-memory budget split: CTAs resident per SM
 #endif
 #ifndef QFT_A0_TMA
-#define QFT_A0_TMA 1       // A0 input: TMA bulk copy into a staging buffer (1) or L2-prefetched global loads (0)
+#define QFT_A0_TMA 1       // A0 input: TMA bulk copy into a staging buffer when it fits (1), else L2-prefetched global loads
 #endif
 #ifndef QFT_TT_MAX
 #define QFT_TT_MAX 4       // cap on signals per CTA iteration
-#endif
-#ifndef QFT_A0_64
-#define QFT_A0_64 1        // A0 by 64-sample chunks (conflict-free block-0 stores, paired loads)
-#endif
-#ifndef QFT_FUSED_ABC
-#define QFT_FUSED_ABC 1    // phases A, B, C fused per warp (no CTA barriers between them)
-#endif
-#ifndef QFT_HALO_SHFL
-#define QFT_HALO_SHFL 0    // phase-C halo by warp shuffle (1) or by a shared-memory read (0)
-#endif
-#ifndef QFT_A0_UNIT8
-#define QFT_A0_UNIT8 0     // A0 with 8 pairs per thread (fewer instructions, more bank conflicts)
 #endif
 
 namespace qft {
@@ -88,30 +77,43 @@ template <int LOG2N, typename T>
 struct KCfg {
     using P = SPlan<LOG2N>;
     static constexpr int VB = (int)sizeof(vec2<T>);
-    static constexpr int PER = (QFT_A0_TMA ? P::N * VB : 0) + P::PADDED * VB;  // (staging +) working per signal
     static constexpr int UB = P::UCELLS * (int)sizeof(T);
     static constexpr int BUDGET = (226 * 1024) / QFT_CTAS_PER_SM - UB - 64;
-    static constexpr int TT0 = BUDGET / PER;
+    static constexpr int PER_W = P::PADDED * VB;        // working area per signal
+    static constexpr int PER_S = P::N * VB + PER_W;     // + TMA staging
     static constexpr int TTC = P::n >= 12 ? QFT_TT_MAX : 64;
-    static constexpr int TT = TT0 < 1 ? 1 : (TT0 > TTC ? TTC : TT0);  // signals per CTA iteration
-    static constexpr int rup32(int x) { return (x + 31) / 32 * 32; }
-    static constexpr int NB32 = rup32(TT * P::NL32);                 // phase-B Lee-32 lanes per side
-    static constexpr int W_B = (2 * NB32 + rup32(2 * TT)) / 32;
-    static constexpr int W_D = (TT * P::DT + 31) / 32;
-    static constexpr int W_AC = TT * P::NWU + QFT_CHAIN_MID;  // + the chain-mid warp
+    static constexpr int clampt(int t) { return t < 1 ? 1 : (t > TTC ? TTC : t); }
+    // stage through TMA when the staging buffer still leaves room for 2 signals
+    // (fp32) / 1 signal (fp64, whose global A0 path spills)
+    static constexpr int TMA_MIN = sizeof(T) == 8 ? 1 : (TTC < 2 ? TTC : 2);
+    static constexpr bool TMA = QFT_A0_TMA && BUDGET / PER_S >= TMA_MIN;
+    static constexpr int TT = clampt(BUDGET / (TMA ? PER_S : PER_W));  // signals per CTA iteration
+    static_assert(TT * PER_W <= BUDGET, "working area exceeds shared memory");
     static constexpr int mx(int a, int b) { return a > b ? a : b; }
-    static constexpr int NU = P::JF >= 1 ? 4 : 2;  // fused warp units per signal
+    static constexpr int NU = 2 * (P::NU1 + 1);  // fused warp units per signal
     static constexpr int W_U = TT * NU;
-    static constexpr int NW0 = QFT_FUSED_ABC ? mx(W_U, W_D) : mx(mx(W_B, W_D), W_AC);
-    static constexpr int NWMAX = sizeof(T) == 8 ? 12 : 17;  // keep >= 168 (fp64) / 120 (fp32) registers
+    static constexpr int W_D = (TT * P::DT + 31) / 32;
+    static constexpr int NW0 = mx(W_U, W_D);
+    // warps are spread over 4 SM sub-partitions of 16K registers each: 12 warps
+    // keep 168 registers (fp64), 16 keep 128; 17 (fp32, N <= 4096) drop to 96
+    static constexpr int NWMAX = sizeof(T) == 8 ? 12 : (P::n >= 13 ? 16 : 17);
     static constexpr int NW = NW0 < 4 ? 4 : (NW0 > NWMAX ? NWMAX : NW0);
     static constexpr int NT = NW * 32;
     static constexpr int STAGE_OFF = 0;
-    static constexpr int W_OFF = QFT_A0_TMA ? TT * P::N * VB : 0;
-    static constexpr int U_OFF = W_OFF + TT * P::PADDED * VB;
+    static constexpr int W_OFF = TMA ? TT * P::N * VB : 0;
+    static constexpr int U_OFF = W_OFF + TT * PER_W;
     static constexpr int BAR_OFF = (U_OFF + UB + 15) / 16 * 16;
     static constexpr int SMEM = BAR_OFF + 16;
+    // top levels (N > 4096): items per thread of one huge block side
+    static constexpr int TIT = (1024 + NT - 1) / NT;
 };
+
+// smem kernel available for (LOG2N, T)
+template <int LOG2N, typename T>
+constexpr bool smem_fits() {
+    using P = SPlan<LOG2N>;
+    return (P::PADDED * (int)sizeof(vec2<T>) + P::UCELLS * (int)sizeof(T) + 64) <= (226 * 1024) / QFT_CTAS_PER_SM;
+}
 
 // ------------------------------------------------------------ small N
 template <int NN, typename T, int MODE = 0>
@@ -223,95 +225,172 @@ QFT_DEV vec2<T> shfl_vec(vec2<T> v, bool down) {
     return r;
 }
 
-template <int LOG2N, typename T, int J, bool DST>
-QFT_DEV void run_c_block(vec2<T> *w, int lane) {
-    CBlock<LOG2N, J, DST, T> c;
-    c.load(w, lane);
-    constexpr int G = CBlock<LOG2N, J, DST, T>::G;
-    vec2<T> out[G];
-#if QFT_HALO_SHFL
-    auto halo = [&](int p) { return shfl_vec(c.own[p], !DST); };
-#else
-    const vec2<T> *hc = CBlock<LOG2N, J, DST, T>::halo_col(w, lane);
+// backward levels of one big block (padded pointer wb), one warp
+template <int R, bool DST, typename T>
+QFT_DEV void run_c_blockp(vec2<T> *wb, int lane) {
+    CBlockP<R, DST, T> c;
+    c.load(wb, lane);
+    vec2<T> out[1 << R];
+    const vec2<T> *hc = CBlockP<R, DST, T>::halo_colp(wb, lane);
     auto halo = [&](int p) { return hc[33 * p]; };  // read before the __syncwarp below
-#endif
     c.compute(lane, halo, out);
     __syncwarp();
-    c.store(w, lane, out);
+    CBlockP<R, DST, T>::storep(wb, lane, out);
     __syncwarp();
 }
 
 template <int LOG2N, typename T, int J>
 QFT_DEV void run_c_blocks(vec2<T> *w, bool dst, int lane) {
-    if constexpr (J < SPlan<LOG2N>::JF) {
-        if (dst) run_c_block<LOG2N, T, J, true>(w, lane);
-        else run_c_block<LOG2N, T, J, false>(w, lane);
-        run_c_blocks<LOG2N, T, J + 1>(w, dst, lane);
-    }
-}
-
-// chain-mid: one warp computes C_JM / S_JM of all signals, level by level
-template <int LOG2N, typename T, int TT>
-QFT_DEV void run_chain_mid(vec2<T> *W, int ntr, int lane) {
     using P = SPlan<LOG2N>;
-    using C = Chain<LOG2N, T>;
-    for (int it = lane; it < ntr; it += 32) C::mid_base(W + it * P::PADDED);
-    __syncwarp();
-    constexpr int RK = (P::MJM + 1 + 31) / 32;  // rounds of 32 lanes per signal and level
-    for (int j = P::n - 2; j >= P::JM; --j) {
-        const int cnt = 2 * C::qj(j) + 1;  // k in [0, m_j]
-        vec2<T> cv[TT][RK], sv[TT][RK];
-#pragma unroll
-        for (int tau = 0; tau < TT; ++tau)
-#pragma unroll
-            for (int r = 0; r < RK; ++r) {
-                const int k = lane + 32 * r;
-                if (tau < ntr && k < cnt) C::mid_level_load(W + tau * P::PADDED, j, k, cv[tau][r], sv[tau][r]);
-            }
-        __syncwarp();
-#pragma unroll
-        for (int tau = 0; tau < TT; ++tau)
-#pragma unroll
-            for (int r = 0; r < RK; ++r) {
-                const int k = lane + 32 * r;
-                if (tau < ntr && k < cnt) C::mid_level_store(W + tau * P::PADDED, j, k, cv[tau][r], sv[tau][r]);
-            }
-        __syncwarp();
+    if constexpr (J < P::JF) {
+        constexpr int b = P::off(J);
+        if (dst) run_c_blockp<P::RF(J), true, T>(w + padx(P::S0 + b), lane);
+        else run_c_blockp<P::RF(J), false, T>(w + padx(b), lane);
+        run_c_blocks<LOG2N, T, J + 1>(w, dst, lane);
     }
 }
 
 // ---- fused forward / Lee-32 / backward work of one side of one signal, one warp.
 // The F -> Lee-32 -> B work of a Lee block depends on no other block, so a warp
 // runs it start to finish with __syncwarp only (no CTA barrier).
-// unit 0: block 0 (its 2^RF(0) sub-blocks = one Lee-32 per lane)
-template <int LOG2N, typename T, bool DST>
-QFT_DEV void unit_block0(vec2<T> *w, const T *U, const T *kcu, int lane) {
-    using P = SPlan<LOG2N>;
-    if constexpr (P::JF >= 1) {
-        constexpr int sb = DST ? P::S0 : 0;
-        FBlock<LOG2N, 0, DST, T> f;
-        f.load(w, U, lane);
-        __syncwarp();
-        f.store(w, lane);
-        __syncwarp();
-        if (lane < (1 << P::RF(0))) b_l32<DST, T>(w, sb + 32 * lane, kcu);
-        __syncwarp();
-        run_c_block<LOG2N, T, 0, DST>(w, lane);
-    }
+// big unit: a block of L = 32 << R cells at padded pointer wb (block 0 for
+// N <= 4096, a 1024-cell (sub-)block for N > 4096): one Lee-32 per lane
+template <int L, int R, typename T, bool DST>
+QFT_DEV void unit_big(vec2<T> *wb, const T *U, const T *kcu, int lane) {
+    FBlockP<L, R, DST, T> f;
+    f.load(wb, U, lane);
+    __syncwarp();
+    f.store(wb, lane);
+    __syncwarp();
+    if (lane < (1 << R)) b_l32p<DST, T>(wb + 33 * lane, kcu);
+    __syncwarp();
+    run_c_blockp<R, DST, T>(wb, lane);
 }
-// unit 1: blocks 1..JF-1, the L = 32 block and the blocks with L <= 16
+// rest unit: blocks JR..JF-1, the L = 32 block and the blocks with L <= 16
 template <int LOG2N, typename T, bool DST>
 QFT_DEV void unit_rest(vec2<T> *w, const T *U, const T *kcu, int lane) {
     using P = SPlan<LOG2N>;
     constexpr int sb = DST ? P::S0 : 0;
-    constexpr int K0 = P::JF >= 1 ? (1 << P::RF(0)) : 0;  // first chunk after block 0
-    constexpr int CNT = P::NL32 - K0;
-    run_f_blocks<LOG2N, T, 1>(w, U, DST, lane);
+    constexpr int CNT = P::NL32 - P::K0;
+    run_f_blocks<LOG2N, T, P::JR>(w, U, DST, lane);
     __syncwarp();
-    if (lane < CNT) b_l32<DST, T>(w, sb + 32 * (K0 + lane), kcu);
+    if (lane < CNT) b_l32<DST, T>(w, sb + 32 * (P::K0 + lane), kcu);
     else if (lane == CNT) b_small<LOG2N, DST, T>(w, kcu);
     __syncwarp();
-    run_c_blocks<LOG2N, T, 1>(w, DST, lane);
+    run_c_blocks<LOG2N, T, P::JR>(w, DST, lane);
+}
+
+// ---- top levels of the huge blocks (N > 4096), whole CTA.  For one signal at
+// a time, every thread holds its items of every huge block (both sides) in
+// registers across one CTA barrier, because the levels permute cells across the
+// whole block.  The next signal's loads touch other cells, so they need no
+// barrier after the previous signal's stores.
+template <int LOG2N, typename T, int MODE, int J>
+QFT_DEV void top_f_sig(vec2<T> *w, const T *U, int tid) {
+    using P = SPlan<LOG2N>;
+    using K = KCfg<LOG2N, T>;
+    if constexpr (J >= P::JH) {
+        __syncthreads();
+    } else {
+        using TC = Top<LOG2N, J, false, T>;
+        using TS = Top<LOG2N, J, true, T>;
+        constexpr int G = TC::G, IT = K::TIT, NT = K::NT;
+        constexpr bool DOC = MODE != 3, DOS = MODE != 2;
+        vec2<T> vc[IT][G], vs[IT][G];
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            const int t = tid + k * NT;
+            if (t < 1024) {
+                if (DOC) TC::f_load(w, U, t, vc[k]);
+                if (DOS) TS::f_load(w, U, t, vs[k]);
+            }
+        }
+        top_f_sig<LOG2N, T, MODE, J + 1>(w, U, tid);
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            const int t = tid + k * NT;
+            if (t < 1024) {
+                if (DOC) TC::f_store(w, t, vc[k]);
+                if (DOS) TS::f_store(w, t, vs[k]);
+            }
+        }
+    }
+}
+template <int LOG2N, typename T, int MODE, int J>
+QFT_DEV void top_b_sig(vec2<T> *w, int tid) {
+    using P = SPlan<LOG2N>;
+    using K = KCfg<LOG2N, T>;
+    if constexpr (J >= P::JH) {
+        __syncthreads();
+    } else {
+        using TC = Top<LOG2N, J, false, T>;
+        using TS = Top<LOG2N, J, true, T>;
+        constexpr int G = TC::G, IT = K::TIT, NT = K::NT;
+        constexpr bool DOC = MODE != 3, DOS = MODE != 2;
+        vec2<T> oc[IT][G], os[IT][G];
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            const int i = tid + k * NT;
+            if (i < 1024) {
+                if (DOC) TC::b_compute(w, i, oc[k]);
+                if (DOS) TS::b_compute(w, i, os[k]);
+            }
+        }
+        top_b_sig<LOG2N, T, MODE, J + 1>(w, tid);
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            const int i = tid + k * NT;
+            if (i < 1024) {
+                if (DOC) TC::b_store(w, i, oc[k]);
+                if (DOS) TS::b_store(w, i, os[k]);
+            }
+        }
+    }
+}
+// all signals; ends with a CTA barrier (ntr is CTA-uniform)
+template <int LOG2N, typename T, int MODE>
+QFT_DEV void top_f(vec2<T> *W, const T *U, int ntr, int tid) {
+    for (int tau = 0; tau < ntr; ++tau) top_f_sig<LOG2N, T, MODE, 0>(W + tau * SPlan<LOG2N>::PADDED, U, tid);
+    __syncthreads();
+}
+template <int LOG2N, typename T, int MODE>
+QFT_DEV void top_b(vec2<T> *W, int ntr, int tid) {
+    for (int tau = 0; tau < ntr; ++tau) top_b_sig<LOG2N, T, MODE, 0>(W + tau * SPlan<LOG2N>::PADDED, tid);
+    __syncthreads();
+}
+
+// A0 of TT complex signals from src (staging buffer or global memory): chunks
+// of 64 consecutive n per warp, UNR chunks in flight; then the multiples of 64.
+template <int LOG2N, typename T, int UNR>
+QFT_DEV void a0_complex(const vec2<T> *src, vec2<T> *W, int ntr, int TTn, int tid, int NT, int NW,
+                        const A0Lane64 &a0l64) {
+    using P = SPlan<LOG2N>;
+    const int lane = tid & 31, warp = tid >> 5;
+    if constexpr (P::m >= 64) {
+        constexpr int NC64 = P::m / 64;
+        auto shfl_up = [](vec2<T> v) { return shfl_vec(v, false); };
+        for (int u0 = warp; u0 < TTn * NC64; u0 += NW * UNR) {
+            A0Chunk64<T> ch[UNR];
+#pragma unroll
+            for (int r = 0; r < UNR; ++r) {
+                const int u = u0 + r * NW, tau = u / NC64, c = u - tau * NC64;
+                if (u < TTn * NC64 && tau < ntr) ch[r].template load<LOG2N>(src + tau * P::N, c, lane);
+            }
+#pragma unroll
+            for (int r = 0; r < UNR; ++r) {
+                const int u = u0 + r * NW, tau = u / NC64, c = u - tau * NC64;
+                // the shuffle inside store is warp-uniform (u, tau do not depend on the lane)
+                if (u < TTn * NC64 && tau < ntr) ch[r].template store<LOG2N>(W + tau * P::PADDED, c, lane, a0l64, shfl_up);
+            }
+        }
+        for (int it = tid; it < TTn * NC64; it += NT) {
+            const int tau = it / NC64, c = it - tau * NC64;
+            if (tau < ntr) a0_item<LOG2N, T>(src + tau * P::N, W + tau * P::PADDED, 64 * c);
+        }
+    } else {
+        for (int tau = 0; tau < ntr; ++tau)
+            for (int nn = tid; nn < P::m; nn += NT) a0_item<LOG2N, T>(src + tau * P::N, W + tau * P::PADDED, nn);
+    }
 }
 
 // MODE 0: complex cdft on (batch, N) complex rows.  MODE 1/2/3: rdft / dct0 /
@@ -324,50 +403,39 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
     using P = SPlan<LOG2N>;
     using K = KCfg<LOG2N, T>;
     constexpr int TT = K::TT, NT = K::NT, NW = K::NW;
+    constexpr bool TMA = K::TMA && MODE == 0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-#if QFT_A0_TMA
     vec2<T> *stage = reinterpret_cast<vec2<T> *>(smem_raw + K::STAGE_OFF);
-#endif
     vec2<T> *W = reinterpret_cast<vec2<T> *>(smem_raw + K::W_OFF);
     T *U = reinterpret_cast<T *>(smem_raw + K::U_OFF);
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + K::BAR_OFF);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
     const long long nbatch = (batch + TT - 1) / TT;
-    const A0Lane a0l = a0_lane<LOG2N>(lane);
     const A0Lane64 a0l64 = a0_lane64<LOG2N>(lane);
     for (int i = tid; i < P::UCELLS; i += NT) U[i] = Ug[i];
-#if QFT_A0_TMA
-    if (tid == 0) mbar_init(bar, 1);
-#else
-    (void)bar;
-#endif
+    if (TMA && tid == 0) mbar_init(bar, 1);
     __syncthreads();
     long long bt = blockIdx.x;
-#if QFT_A0_TMA
-    if (MODE == 0 && tid == 0 && bt < nbatch) {
+    if (TMA && tid == 0 && bt < nbatch) {
         const long long nt = (batch - bt * TT) < TT ? (batch - bt * TT) : TT;
         tma_bulk_load(stage, in + bt * TT * P::N, (uint32_t)(nt * P::N * K::VB), bar);
     }
     uint32_t parity = 0;
-#endif
     for (; bt < nbatch; bt += gridDim.x) {
         const int ntr = (int)((batch - bt * TT) < TT ? (batch - bt * TT) : TT);
-#if QFT_A0_TMA
-        if constexpr (MODE == 0) {
+        if constexpr (TMA) {
             mbar_wait(bar, parity);
             parity ^= 1u;
-        }
-#else
-        // pull the next batch into L2 while this one is transformed
-        if (tid == 0 && bt + gridDim.x < nbatch) {
+        } else if (tid == 0 && bt + gridDim.x < nbatch) {
+            // pull the next batch into L2 while this one is transformed
             const long long nb = bt + gridDim.x;
-            const long long nt = (batch - nb * TT) < TT ? (batch - nb * TT) : TT;
-            l2_prefetch(in + nb * TT * P::N, (uint32_t)(nt * P::N * K::VB));
+            if constexpr (MODE == 0) {
+                const long long nt = (batch - nb * TT) < TT ? (batch - nb * TT) : TT;
+                l2_prefetch(in + nb * TT * P::N, (uint32_t)(nt * P::N * K::VB));
+            }
         }
-        const vec2<T> *stage = in + bt * TT * P::N;  // A0 reads global memory directly
-#endif
-        // A0: fold + route, staging -> W
+        // A0: fold + route -> W
         if constexpr (MODE != 0) {
             // real modes: rows of the mode's stored length straight from global memory
             constexpr int RL = MODE == 1 ? P::N : (MODE == 2 ? P::m + 1 : P::m - 1);
@@ -377,90 +445,20 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
                 for (int nn = tid; nn <= P::m; nn += NT)
                     a0_item_real<LOG2N, T, MODE>(xr + ra * RL, xr + rb * RL, W + tau * P::PADDED, nn);
             }
+        } else if constexpr (TMA) {
+            a0_complex<LOG2N, T, 1>(stage, W, ntr, TT, tid, NT, NW, a0l64);
         } else {
-#if QFT_A0_UNIT8
-        for (int it = tid; it < TT * (P::m / 8); it += NT) {
-            const int tau = it / (P::m / 8), k = it - tau * (P::m / 8);
-            if (tau < ntr) a0_unit8<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, k);
-        }
-#else
-        {
-            // warps take chunks of 32 consecutive n; lane 0's multiples of 32 afterwards
-            constexpr int NCH = P::m / 32;
-#if !QFT_A0_TMA
-            // global loads: 8 chunks in flight per lane (memory-level parallelism)
-            constexpr int UNR = 8;
-            for (int u0 = warp; u0 < TT * NCH; u0 += NW * UNR) {
-                vec2<T> xa[UNR], xb[UNR];
-#pragma unroll
-                for (int r = 0; r < UNR; ++r) {
-                    const int u = u0 + r * NW, tau = u / NCH, c = u - tau * NCH, n = 32 * c + lane;
-                    if (u < TT * NCH && tau < ntr && lane) {
-                        xa[r] = stage[tau * P::N + n];
-                        xb[r] = stage[tau * P::N + P::N - n];
-                    }
-                }
-#pragma unroll
-                for (int r = 0; r < UNR; ++r) {
-                    const int u = u0 + r * NW, tau = u / NCH, c = u - tau * NCH;
-                    if (u < TT * NCH && tau < ntr && lane) {
-                        vec2<T> *w = W + tau * P::PADDED;
-                        const int cell = a0l.A + c * a0l.B;
-                        w[padx(cell)] = vadd(xa[r], xb[r]);
-                        w[padx(cell) + padx(P::S0)] = vsub(xa[r], xb[r]);
-                    }
-                }
-            }
-#else
-#if QFT_A0_64
-            // chunks of 64 consecutive n; the multiples of 64 (and n = 0) afterwards
-            // (N = 64 has a single 32-sample half: one chunk of lanes 0..15 suffices
-            //  only for m >= 64, so small N keep the 32-sample chunks below)
-            if constexpr (P::m >= 64) {
-            constexpr int NC64 = P::m / 64;
-            auto shfl_up = [](vec2<T> v) { return shfl_vec(v, false); };
-            for (int u = warp; u < TT * NC64; u += NW) {
-                const int tau = u / NC64, c = u - tau * NC64;
-                if (tau < ntr) a0_chunk64<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, c, lane, a0l64, shfl_up);
-            }
-            for (int it = tid; it < TT * NC64; it += NT) {
-                const int tau = it / NC64, c = it - tau * NC64;
-                if (tau < ntr) a0_item<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, 64 * c);
-            }
-            } else {
-                for (int tau = 0; tau < ntr; ++tau)
-                    for (int nn = tid; nn < P::m; nn += NT)
-                        a0_item<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, nn);
-            }
-#else
-            // the warp walks its chunks of each signal with fixed per-lane constants
-            for (int tau = 0; tau < ntr; ++tau) {
-                const vec2<T> *xs = stage + tau * P::N;
-                vec2<T> *ws = W + tau * P::PADDED;
-                if (lane) {
-#pragma unroll 4
-                    for (int c = warp; c < NCH; c += NW) a0_chunk<LOG2N, T>(xs, ws, c, lane, a0l);
-                }
-            }
-            for (int it = tid; it < TT * NCH; it += NT) {
-                const int tau = it / NCH, c = it - tau * NCH;
-                if (tau < ntr) a0_item<LOG2N, T>(stage + tau * P::N, W + tau * P::PADDED, 32 * c);
-            }
-#endif
-#endif  // QFT_A0_TMA
-        }
-#endif  // QFT_A0_UNIT8
+            a0_complex<LOG2N, T, sizeof(T) == 8 ? 1 : 4>(in + bt * TT * P::N, W, ntr, TT, tid, NT, NW, a0l64);
         }
         __syncthreads();
-#if QFT_A0_TMA
         // the staging buffer is free: prefetch the next batch while we compute
-        if (MODE == 0 && tid == 0 && bt + gridDim.x < nbatch) {
+        if (TMA && tid == 0 && bt + gridDim.x < nbatch) {
             const long long nb = bt + gridDim.x;
             const long long nt = (batch - nb * TT) < TT ? (batch - nb * TT) : TT;
             tma_bulk_load(stage, in + nb * TT * P::N, (uint32_t)(nt * P::N * K::VB), bar);
         }
-#endif
-#if QFT_FUSED_ABC
+        // TF: top forward levels of the huge blocks (N > 4096; ends with a barrier)
+        if constexpr (P::JH > 0) top_f<LOG2N, T, MODE>(W, U, ntr, tid);
         // A+B+C fused: one warp per (signal, side, unit) -- no CTA barrier inside
         for (int u = warp; u < TT * K::NU; u += NW) {
             const int tau = u / K::NU, kind = u - tau * K::NU;
@@ -468,9 +466,11 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
             vec2<T> *w = W + tau * P::PADDED;
             const bool dst = kind & 1;
             if ((MODE == 2 && dst) || (MODE == 3 && !dst)) continue;  // side not needed
-            if (K::NU == 4 && kind < 2) {
-                if (dst) unit_block0<LOG2N, T, true>(w, U, kc.u, lane);
-                else unit_block0<LOG2N, T, false>(w, U, kc.u, lane);
+            const int bu = kind >> 1;
+            if (bu < P::NU1) {
+                vec2<T> *wb = w + padx((dst ? P::S0 : 0) + P::big_cell(bu));
+                if (dst) unit_big<P::LB, P::RB, T, true>(wb, U, kc.u, lane);
+                else unit_big<P::LB, P::RB, T, false>(wb, U, kc.u, lane);
             } else {
                 if (dst) unit_rest<LOG2N, T, true>(w, U, kc.u, lane);
                 else unit_rest<LOG2N, T, false>(w, U, kc.u, lane);
@@ -478,79 +478,8 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
             __syncwarp();
         }
         __syncthreads();
-#else
-        // A: forward levels of the big blocks (warp units: side x {block 0, blocks 1..})
-        if constexpr (P::NWU > 0) {
-            for (int u = warp; u < TT * P::NWU; u += NW) {
-                const int tau = u / P::NWU, kind = u - tau * P::NWU;
-                if (tau >= ntr) continue;
-                vec2<T> *w = W + tau * P::PADDED;
-                const bool dst = kind & 1;
-                if (kind < 2) {
-                    if (dst) {
-                        FBlock<LOG2N, 0, true, T> f;
-                        f.load(w, U, lane);
-                        __syncwarp();
-                        f.store(w, lane);
-                    } else {
-                        FBlock<LOG2N, 0, false, T> f;
-                        f.load(w, U, lane);
-                        __syncwarp();
-                        f.store(w, lane);
-                    }
-                } else {
-                    run_f_blocks<LOG2N, T, 1>(w, U, dst, lane);
-                }
-                __syncwarp();
-            }
-            __syncthreads();
-        }
-        // B: Lee-32 on every 32-cell chunk (warp-uniform side), then the small blocks
-        for (int u = tid; u < 2 * K::NB32 + 2 * TT; u += NT) {
-            if (u < 2 * K::NB32) {
-                const bool dst = u >= K::NB32;
-                const int v = dst ? u - K::NB32 : u;
-                const int tau = v / (P::NL32 > 0 ? P::NL32 : 1), k = v - tau * P::NL32;
-                if (P::NL32 > 0 && tau < ntr) {
-                    vec2<T> *w = W + tau * P::PADDED;
-                    if (dst) b_l32<true, T>(w, P::S0 + 32 * k, kc.u);
-                    else b_l32<false, T>(w, 32 * k, kc.u);
-                }
-            } else {
-                const int v = u - 2 * K::NB32;
-                const int tau = v >> 1;
-                if (tau < ntr) {
-                    vec2<T> *w = W + tau * P::PADDED;
-                    if (v & 1) b_small<LOG2N, true, T>(w, kc.u);
-                    else b_small<LOG2N, false, T>(w, kc.u);
-                }
-            }
-        }
-        __syncthreads();
-        // C: backward levels of the big blocks; one more warp unit computes the
-        // lower chain levels C_JM, S_JM of all signals (chain-mid)
-        {
-            for (int u = warp; u < TT * P::NWU + QFT_CHAIN_MID; u += NW) {
-                if (QFT_CHAIN_MID && u == TT * P::NWU) {
-                    run_chain_mid<LOG2N, T, TT>(W, ntr, lane);
-                    continue;
-                }
-                if constexpr (P::NWU > 0) {
-                    const int tau = u / P::NWU, kind = u - tau * P::NWU;
-                    if (tau >= ntr) continue;
-                    vec2<T> *w = W + tau * P::PADDED;
-                    const bool dst = kind & 1;
-                    if (kind < 2) {
-                        if (dst) run_c_block<LOG2N, T, 0, true>(w, lane);
-                        else run_c_block<LOG2N, T, 0, false>(w, lane);
-                    } else {
-                        run_c_blocks<LOG2N, T, 1>(w, dst, lane);
-                    }
-                }
-            }
-            __syncthreads();
-        }
-#endif
+        // TB: top backward levels of the huge blocks (ends with a barrier)
+        if constexpr (P::JH > 0) top_b<LOG2N, T, MODE>(W, ntr, tid);
         // D: chain + recombination -> global
         for (int it = tid; it < TT * P::DT; it += NT) {
             const int tau = it / P::DT, t = it - tau * P::DT;

@@ -1,4 +1,4 @@
-// qft_smem.cuh -- improved-QFT of length-N complex signals (N = 2^6 .. 2^12)
+// qft_smem.cuh -- improved-QFT of length-N complex signals (N = 2^6 .. 2^14)
 // held in shared memory; a CTA works on T signals at a time.
 //
 // Working layout W of one signal (vec2 cells, padded address p + p/32 so that
@@ -18,14 +18,12 @@
 //   C   backward levels of the big blocks (halo = neighbour lane)   W -> W
 //   D   time-split chain (elaborations.py:329-340) + complex
 //       recombination (shared.py:58-72)                          W -> global
+// N > 4096: the "huge" Lee blocks (L > 1024) first get RT = n-12-j top fold
+// levels from the whole CTA (TF, W -> W, 1024-cell sub-blocks written
+// sub-block-major), then every 1024-cell sub-block is a warp unit exactly like
+// block 0 of N = 4096, then the whole CTA runs the RT top backward levels (TB).
 #pragma once
 #include "qft_lee.cuh"
-
-// QFT_CHAIN_MID = k > 0: the bottom k chain levels are computed once by one warp
-// in phase C (the rest by each phase-D thread's descent); 0: all by descent
-#ifndef QFT_CHAIN_MID
-#define QFT_CHAIN_MID 0
-#endif
 
 namespace qft {
 
@@ -42,19 +40,33 @@ struct SPlan {
     static constexpr int RF(int j) { return n - 7 - j; }  // big block: L = 32 << RF
     static constexpr int S0 = m;                     // sine region
     static constexpr int BASE = N - 1;               // s(0) at N-1, s(m) at N
-    static constexpr int JM0 = n - 1 - QFT_CHAIN_MID;
-    static constexpr int JM = QFT_CHAIN_MID ? (JM0 > RC + 1 ? JM0 : RC + 1) : n - 1;  // chain-mid level
-    static constexpr int MJM = N >> (JM + 1);        // m_JM: C_JM has MJM+1 cells, S_JM MJM-1
-    static constexpr int CHC = N + 1;                // C_JM cells [CHC, CHC + MJM]
-    static constexpr int CHS = CHC + MJM + 1;        // S_JM harmonic h at CHS + h - 1
-    static constexpr int CELLS = CHS + MJM;
-    static_assert(JM > n - 2 || (1 << (n - 2 - JM)) <= 32, "chain-mid blocks must be finished by phase B");
+    static constexpr int CELLS = N + 1;
     static constexpr int PADDED = CELLS + CELLS / 32 + 1;
     static constexpr int NL32 = n >= 7 ? m / 32 - 1 : 0;  // Lee-32 chunks per side
-    static constexpr int NWU = 2 * ((JF >= 1) + (JF >= 2)); // phase A/C warp units
     static constexpr int MRC = N >> (RC + 1);        // m_RC: phase-D thread t in [0, MRC]
     static constexpr int DT = MRC + 1;               // phase D threads per signal
     static constexpr int UCELLS = N / 4;             // level-table entries
+    // huge blocks (L > 1024): j < JH, RT(j) top levels leave 1024-cell sub-blocks
+    static constexpr int JH = n > 12 ? n - 12 : 0;
+    static constexpr int RT(int j) { return n - 12 - j; }
+    // "big" warp units per side: block 0 (n <= 12), or every 1024-cell
+    // (sub-)block of the blocks j <= n-12 (n > 12); the "rest" unit does the
+    // blocks j >= JR, the L = 32 block and the small blocks
+    static constexpr int NU1 = n <= 12 ? (JF >= 1 ? 1 : 0) : (1 << (n - 11)) - 1;
+    static constexpr int JR = n <= 12 ? 1 : n - 11;
+    static constexpr int K0 = JF >= 1 ? off(JR) / 32 : 0;  // first Lee-32 chunk of the rest unit
+    static constexpr int LB = n <= 12 ? (JF >= 1 ? L(0) : 32) : 1024;  // big unit length
+    static constexpr int RB = n <= 12 ? (JF >= 1 ? RF(0) : 0) : 5;
+    // first cell of big unit u (one side)
+    static QFT_HD int big_cell(int u) {
+        if (n <= 12) return 0;
+        int j = 0;
+        while (u >= (1 << RT(j))) {
+            u -= 1 << RT(j);
+            ++j;
+        }
+        return off(j) + 1024 * u;
+    }
 };
 
 // ---------------------------------------------------------------- phase A0
@@ -90,35 +102,6 @@ QFT_HD void a0_item(const vec2<T> *x, vec2<T> *w, int n) {
     }
 }
 
-// A0 by chunks of 32 consecutive n: lane l (1..31) handles n = 32c + l, whose
-// class j = ctz(l) and cell off_j + (n >> (j+1)) = A_l + c * B_l do not depend
-// on c except through B_l; lane 0's n = 32c (c >= 1) are done by a0_item.
-struct A0Lane {
-    int A, B, sh;  // padded cosine cell of chunk c: A + c*B + (c >> sh)
-};
-template <int LOG2N>
-QFT_HD A0Lane a0_lane(int l) {
-    using P = SPlan<LOG2N>;
-    A0Lane r;
-    const int j = ctz32((uint32_t)(l | 32));
-    // cell = off_j + (n >> (j+1)) with off_j a multiple of 32 and (l >> (j+1)) + c*B mod 32 < 32,
-    // so padx(cell) = off_j + off_j/32 + (l >> (j+1)) + c*B + (c >> (j+1))
-    const int off = P::m - (1 << (LOG2N - 1 - j));
-    r.A = off + (off >> 5) + (l >> (j + 1));
-    r.B = 32 >> (j + 1);
-    r.sh = j + 1;
-    return r;
-}
-template <int LOG2N, typename T>
-QFT_HD void a0_chunk(const vec2<T> *x, vec2<T> *w, int c, int l, A0Lane a) {
-    using P = SPlan<LOG2N>;
-    const int n = 32 * c + l;
-    vec2<T> u = x[n], v = x[P::N - n];
-    const int pc = a.A + c * a.B + (c >> a.sh);
-    w[pc] = vadd(u, v);                      // dc[n]   = x[n] + x[N-n]
-    w[pc + padx(P::S0)] = vsub(u, v);        // ds[n-1] = x[n] - x[N-n]  (S0 is a multiple of 32)
-}
-
 // A0 by chunks of 64 consecutive n (n = 64c + 2l and 64c + 2l + 1 for lane l):
 // one aligned pair load per side, the odd samples (Lee block 0) go to 32
 // consecutive cells, the even ones to block 1 + ctz(l); lane l's even mirror
@@ -137,21 +120,33 @@ QFT_HD A0Lane64 a0_lane64(int l) {
     r.sh = j;
     return r;
 }
+template <typename T>
+struct A0Chunk64 {
+    vec2<T> xe, xo, mn, mo;
+    template <int LOG2N>
+    QFT_HD void load(const vec2<T> *x, int c, int l) {
+        ld2(x + 64 * c + 2 * l, xe, xo);                          // x[n_e], x[n_o]
+        ld2(x + (1 << LOG2N) - 64 * c - 2 * l - 2, mn, mo);       // x[N - n_e - 2], x[N - n_o]
+    }
+    template <int LOG2N, class ShflUp>
+    QFT_HD void store(vec2<T> *w, int c, int l, const A0Lane64 &a, ShflUp &&shfl_up) const {
+        constexpr int PS = padx(SPlan<LOG2N>::S0);
+        const vec2<T> me = shfl_up(mn);                  // x[N - n_e] from lane l-1
+        const int po = 33 * c + l;                       // block 0 cell 32c + l, padded
+        w[po] = vadd(xo, mo);
+        w[po + PS] = vsub(xo, mo);
+        if (l) {
+            const int pe = a.A + c * a.B + (c >> a.sh);
+            w[pe] = vadd(xe, me);
+            w[pe + PS] = vsub(xe, me);
+        }
+    }
+};
 template <int LOG2N, typename T, class ShflUp>
 QFT_HD void a0_chunk64(const vec2<T> *x, vec2<T> *w, int c, int l, A0Lane64 a, ShflUp &&shfl_up) {
-    using P = SPlan<LOG2N>;
-    vec2<T> xe, xo, mn, mo;
-    ld2(x + 64 * c + 2 * l, xe, xo);                // x[n_e], x[n_o]
-    ld2(x + P::N - 64 * c - 2 * l - 2, mn, mo);     // x[N - n_e - 2], x[N - n_o]
-    const vec2<T> me = shfl_up(mn);                  // x[N - n_e] from lane l-1
-    const int po = 33 * c + l;                       // block 0 cell 32c + l, padded
-    w[po] = vadd(xo, mo);
-    w[po + padx(P::S0)] = vsub(xo, mo);
-    if (l) {
-        const int pe = a.A + c * a.B + (c >> a.sh);
-        w[pe] = vadd(xe, me);
-        w[pe + padx(P::S0)] = vsub(xe, me);
-    }
+    A0Chunk64<T> ch;
+    ch.template load<LOG2N>(x, c, l);
+    ch.template store<LOG2N>(w, c, l, a, shfl_up);
 }
 
 // ---------------------------------------------------------------- modes
@@ -185,55 +180,17 @@ QFT_HD void a0_item_real(const T *xa, const T *xb, vec2<T> *w, int n) {
     }
 }
 
-template <int LOG2N, typename T>
-QFT_HD void a0_unit8(const vec2<T> *x, vec2<T> *w, int k) {
-    using P = SPlan<LOG2N>;
-    vec2<T> f[9], r[8];
-#pragma unroll
-    for (int e = 0; e < 8; e += 2) ld2(x + 8 * k + e, f[e], f[e + 1]);
-    f[8] = x[8 * k + 8];
-#pragma unroll
-    for (int e = 0; e < 8; e += 2) ld2(x + P::N - 8 * k - 8 + e, r[e], r[e + 1]);
-    // r[e] = x[N - n] for n = 8k + 8 - e
-    constexpr int off0 = P::off(0), off1 = P::off(1), off2 = P::off(2);
-    vec2<T> *c0 = w + padx(off0 + 4 * k), *s0 = w + padx(P::S0 + off0 + 4 * k);
-#pragma unroll
-    for (int d = 1; d < 8; d += 2) {  // odd n: block 0, i = 4k + (d-1)/2
-        c0[(d - 1) / 2] = vadd(f[d], r[8 - d]);
-        s0[(d - 1) / 2] = vsub(f[d], r[8 - d]);
-    }
-    vec2<T> *c1 = w + padx(off1 + 2 * k), *s1 = w + padx(P::S0 + off1 + 2 * k);
-    c1[0] = vadd(f[2], r[6]);  // n = 8k+2: block 1, i = 2k
-    s1[0] = vsub(f[2], r[6]);
-    c1[1] = vadd(f[6], r[2]);  // n = 8k+6: i = 2k+1
-    s1[1] = vsub(f[6], r[2]);
-    w[padx(off2 + k)] = vadd(f[4], r[4]);  // n = 8k+4: block 2, i = k
-    w[padx(P::S0 + off2 + k)] = vsub(f[4], r[4]);
-    const int n8 = 8 * k + 8;
-    if (n8 == P::m) {
-        w[padx(P::BASE + 1)] = f[8];  // dc[m] = x[m]
-    } else {
-        const int j = ctz32((uint32_t)n8);
-        const int cell = P::m - (1 << (LOG2N - 1 - j)) + (n8 >> (j + 1));
-        w[padx(cell)] = vadd(f[8], r[0]);
-        w[padx(P::S0 + cell)] = vsub(f[8], r[0]);
-    }
-    if (k == 0) w[padx(P::BASE)] = f[0];  // dc[0] = x[0]
-}
-
 // ---------------------------------------------------------------- phase A
-// Lane t of the warp owning big block J of one side: loads its reflection group,
-// folds RF levels, and (after __syncwarp) writes element t of sub-block p to
-// cell 32p + t of the block.
-template <int LOG2N, int J, bool DST, typename T>
-struct FBlock {
-    using P = SPlan<LOG2N>;
-    static constexpr int L = P::L(J), R = P::RF(J), G = 1 << R;
-    static constexpr int base = (DST ? P::S0 : 0) + P::off(J);  // multiple of 32
+// Lane t of the warp owning a big block of L = 32 << R cells (padded pointer wb
+// to its first cell, a multiple of 32): loads its reflection group, folds R
+// levels, and (after __syncwarp) writes element t of sub-block p to cell 32p + t.
+template <int L, int R, bool DST, typename T>
+struct FBlockP {
+    static constexpr int G = 1 << R;
     vec2<T> v[G];
-    QFT_HD void load(const vec2<T> *w, const T *U, int t) {
-        const vec2<T> *bf = w + padx(base) + t;       // forward runs
-        const vec2<T> *br = w + padx(base) + 31 - t;  // reversed runs
+    QFT_HD void load(const vec2<T> *wb, const T *U, int t) {
+        const vec2<T> *bf = wb + t;       // forward runs
+        const vec2<T> *br = wb + 31 - t;  // reversed runs
 #pragma unroll
         for (int s = 0; s < G; ++s) {
             int c, sg;
@@ -243,24 +200,76 @@ struct FBlock {
         }
         lee_fwd<R, L, DST, T>(v, t, U);
     }
-    QFT_HD void store(vec2<T> *w, int t) const {
-        vec2<T> *o = w + padx(base) + t;
+    QFT_HD void store(vec2<T> *wb, int t) const {
+        vec2<T> *o = wb + t;
 #pragma unroll
         for (int p = 0; p < G; ++p) o[33 * p] = v[p];
     }
 };
+// Lee block J of one side of a signal at w
+template <int LOG2N, int J, bool DST, typename T>
+struct FBlock : FBlockP<SPlan<LOG2N>::L(J), SPlan<LOG2N>::RF(J), DST, T> {
+    using P = SPlan<LOG2N>;
+    using Base = FBlockP<P::L(J), P::RF(J), DST, T>;
+    static constexpr int base = (DST ? P::S0 : 0) + P::off(J);  // multiple of 32
+    QFT_HD void load(const vec2<T> *w, const T *U, int t) { Base::load(w + padx(base), U, t); }
+    QFT_HD void store(vec2<T> *w, int t) const { Base::store(w + padx(base), t); }
+};
+
+// ---------------------------------------------------------------- top levels (N > 4096)
+// Huge block J of one side (L > 1024, RT = n-12-J top levels).  TF item t in
+// [0, 1024): the reflection group t, RT forward levels, element t of sub-block p
+// -> cell 1024p + t.  TB item i in [0, 1024): column i of the 2^RT sub-block
+// spectra (+ halo column) -> block spectrum slots [i 2^RT, (i+1) 2^RT).
+template <int LOG2N, int J, bool DST, typename T>
+struct Top {
+    using P = SPlan<LOG2N>;
+    static constexpr int L = P::L(J), R = P::RT(J), G = 1 << R;
+    static constexpr int base = (DST ? P::S0 : 0) + P::off(J);
+    static_assert(L >> R == 1024, "top levels leave 1024-cell sub-blocks");
+    QFT_HD static void f_load(const vec2<T> *w, const T *U, int t, vec2<T> *v) {
+#pragma unroll
+        for (int s = 0; s < G; ++s) {
+            int c, sg;
+            run_of(R, L, s, c, sg);
+            v[s] = w[padx(base + c + sg * t)];
+        }
+        lee_fwd<R, L, DST, T>(v, t, U);
+    }
+    QFT_HD static void f_store(vec2<T> *w, int t, const vec2<T> *v) {
+#pragma unroll
+        for (int p = 0; p < G; ++p) w[padx(base + 1024 * p + t)] = v[p];
+    }
+    QFT_HD static void b_compute(const vec2<T> *w, int i, vec2<T> *out) {
+        const int ih = DST ? (i > 0 ? i - 1 : i) : (i < 1023 ? i + 1 : i);
+        vec2<T> own[G];
+#pragma unroll
+        for (int p = 0; p < G; ++p) own[p] = w[padx(base + 1024 * p + i)];
+        auto halo = [&](int p) { return w[padx(base + 1024 * p + ih)]; };
+        const bool edge = DST ? (i == 0) : (i == 1023);
+        lee_bwd_fn<R, DST, T>(own, 0, halo, edge, out);
+    }
+    QFT_HD static void b_store(vec2<T> *w, int i, const vec2<T> *out) {
+        vec2<T> *o = w + padx(base + i * G);  // G <= 32 slots inside one 32-cell chunk
+#pragma unroll
+        for (int s = 0; s < G; ++s) o[s] = out[s];
+    }
+};
 
 // ---------------------------------------------------------------- phase B
-// Lee-32 on the 32-cell chunk starting at (padded) cell p0; in place.
+// Lee-32 on the 32-cell chunk at padded pointer c; in place.
 template <bool DST, typename T>
-QFT_HD void b_l32(vec2<T> *w, int chunk_base, const T *U) {
-    vec2<T> *c = w + padx(chunk_base);
+QFT_HD void b_l32p(vec2<T> *c, const T *U) {
     vec2<T> v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = c[e];
     lee_full<32, DST, T>(v, U);
 #pragma unroll
     for (int e = 0; e < 32; ++e) c[e] = v[e];
+}
+template <bool DST, typename T>
+QFT_HD void b_l32(vec2<T> *w, int chunk_base, const T *U) {
+    b_l32p<DST, T>(w + padx(chunk_base), U);
 }
 
 template <int LOG2N, bool DST, typename T, int J>
@@ -286,24 +295,23 @@ QFT_HD void b_small(vec2<T> *w, const T *U) {
 }
 
 // ---------------------------------------------------------------- phase C
-// Lane i of the warp owning big block J of one side: column i of the 2^R
-// sub-block spectra -> block spectrum slots [i*2^R, (i+1)*2^R), natural order.
-// The halo Z_p[i+1] (DCT) / Z_p[i-1] (DST) is the neighbour lane's own value.
-template <int LOG2N, int J, bool DST, typename T>
-struct CBlock {
-    using P = SPlan<LOG2N>;
-    static constexpr int R = P::RF(J), G = 1 << R;
-    static constexpr int base = (DST ? P::S0 : 0) + P::off(J);
+// Lane i of the warp owning a big block (2^R sub-blocks of 32, padded pointer
+// wb): column i of the sub-block spectra -> block spectrum slots
+// [i*2^R, (i+1)*2^R), natural order.  The halo Z_p[i+1] (DCT) / Z_p[i-1] (DST)
+// is the neighbour lane's own value.
+template <int R, bool DST, typename T>
+struct CBlockP {
+    static constexpr int G = 1 << R;
     vec2<T> own[G];
-    QFT_HD void load(const vec2<T> *w, int i) {
-        const vec2<T> *c = w + padx(base) + i;
+    QFT_HD void load(const vec2<T> *wb, int i) {
+        const vec2<T> *c = wb + i;
 #pragma unroll
         for (int p = 0; p < G; ++p) own[p] = c[33 * p];
     }
     // halo column (i+1 for DCT, i-1 for DST; the edge lane re-reads its own column)
-    QFT_HD static const vec2<T> *halo_col(const vec2<T> *w, int i) {
+    QFT_HD static const vec2<T> *halo_colp(const vec2<T> *wb, int i) {
         const int ih = DST ? (i > 0 ? i - 1 : i) : (i < 31 ? i + 1 : i);
-        return w + padx(base) + ih;
+        return wb + ih;
     }
     // halo(p) must return the neighbour lane's own[p]
     template <class Halo>
@@ -311,12 +319,21 @@ struct CBlock {
         const bool edge = DST ? (i == 0) : (i == 31);
         lee_bwd_fn<R, DST, T>(own, 0, halo, edge, out);
     }
-    QFT_HD static void store(vec2<T> *w, int i, const vec2<T> *out) {
+    QFT_HD static void storep(vec2<T> *wb, int i, const vec2<T> *out) {
         // slots i*G .. i*G+G-1 lie inside one 32-cell chunk: contiguous when padded
-        vec2<T> *o = w + padx(base + i * G);
+        vec2<T> *o = wb + i * G + ((i * G) >> 5);
 #pragma unroll
         for (int s = 0; s < G; ++s) o[s] = out[s];
     }
+};
+template <int LOG2N, int J, bool DST, typename T>
+struct CBlock : CBlockP<SPlan<LOG2N>::RF(J), DST, T> {
+    using P = SPlan<LOG2N>;
+    using Base = CBlockP<P::RF(J), DST, T>;
+    static constexpr int base = (DST ? P::S0 : 0) + P::off(J);
+    QFT_HD void load(const vec2<T> *w, int i) { Base::load(w + padx(base), i); }
+    QFT_HD static const vec2<T> *halo_col(const vec2<T> *w, int i) { return Base::halo_colp(w + padx(base), i); }
+    QFT_HD static void store(vec2<T> *w, int i, const vec2<T> *out) { Base::storep(w + padx(base), i, out); }
 };
 
 // ---------------------------------------------------------------- phase D
@@ -330,126 +347,6 @@ struct Chain {
     // sine spectrum of Lee block j, harmonic h (slot h-1)
     static QFT_HD vec2<T> OS(const vec2<T> *w, int j, int h) { return w[padx(P::S0 + P::off(j) + h - 1)]; }
 
-    // ---- chain-mid (phase C, one warp per signal): C_j, S_j for j = n-1 .. JM,
-    // bottom-up, in place in the chain cells (elaborations.py:329-340).
-    // C_j[k] = E[k]+O[k], C_j[m_j-k] = E[k]-O[k] (k < q_j), C_j[q_j] = E[q_j];
-    // S_j[h] = O[h]+E[h], S_j[m_j-h] = O[h]-E[h] (h < q_j), S_j[q_j] = O[q_j].
-    static QFT_HD void mid_level_load(const vec2<T> *w, int j, int k, vec2<T> &c, vec2<T> &s) {
-        const int q = qj(j), mm = 2 * q;
-        if (k <= mm) {  // C_j[k]
-            const int kk = k <= q ? k : mm - k;
-            vec2<T> e = w[padx(P::CHC + kk)];
-            if (k == q) c = e;
-            else {
-                vec2<T> o = OC(w, j, kk);
-                c = k < q ? vadd(e, o) : vsub(e, o);
-            }
-        }
-        if (k >= 1 && k < mm) {  // S_j[k]
-            if (k == q) s = OS(w, j, q);
-            else {
-                const int kk = k < q ? k : mm - k;
-                vec2<T> o = OS(w, j, kk);
-                vec2<T> e = w[padx(P::CHS + kk - 1)];
-                s = k < q ? vadd(o, e) : vsub(o, e);
-            }
-        }
-    }
-    static QFT_HD void mid_level_store(vec2<T> *w, int j, int k, vec2<T> c, vec2<T> s) {
-        const int mm = 2 * qj(j);
-        if (k <= mm) w[padx(P::CHC + k)] = c;
-        if (k >= 1 && k < mm) w[padx(P::CHS + k - 1)] = s;
-    }
-    static QFT_HD void mid_base(vec2<T> *w) {  // C_{n-1} = DCT-0 of two points
-        vec2<T> s0 = w[padx(P::BASE)], sm = w[padx(P::BASE + 1)];
-        w[padx(P::CHC)] = vadd(s0, sm);
-        w[padx(P::CHC + 1)] = vsub(s0, sm);
-    }
-
-    // C_J[k], 0 <= k <= m_J: descend the time-split chain to the DCT base (or to
-    // the chain-mid level JM computed in phase C)
-    template <int J>
-    static QFT_HD vec2<T> descCJ(const vec2<T> *w, int k) {
-        if constexpr (QFT_CHAIN_MID && J == P::JM) {
-            return w[padx(P::CHC + k)];
-        } else if constexpr (J == n - 1) {  // DCT-0 of two points: [s0 + sm, s0 - sm]
-            vec2<T> s0 = w[padx(P::BASE)], sm = w[padx(P::BASE + 1)];
-            return k == 0 ? vadd(s0, sm) : vsub(s0, sm);
-        } else {
-            constexpr int q = qj(J), mm = 2 * q;
-            const int kk = k <= q ? k : mm - k;
-            vec2<T> e = descCJ<J + 1>(w, kk);
-            if (k == q) return e;                       // out[q] = E[q]
-            vec2<T> o = OC(w, J, kk);
-            return k < q ? vadd(e, o) : vsub(e, o);     // E+O / E-O
-        }
-    }
-    // S_J[k], 1 <= k <= m_J - 1 (k = 0, m_J: unused value, in-bounds reads)
-    template <int J>
-    static QFT_HD vec2<T> descSJ(const vec2<T> *w, int k) {
-        constexpr int q = qj(J), mm = 2 * q;
-        if constexpr (QFT_CHAIN_MID && J == P::JM) {
-            return w[padx(P::CHS + (k > 0 ? k - 1 : 0))];
-        } else if constexpr (J == n - 2) {
-            return OS(w, J, 1);                         // _dst base: copy
-        } else {
-            if (k == q) return OS(w, J, q);             // out[q-1] = O[q-1]
-            const int kk = k < q ? k : mm - k;
-            vec2<T> e = descSJ<J + 1>(w, kk);
-            vec2<T> o = OS(w, J, kk);
-            return k < q ? vadd(o, e) : vsub(o, e);     // O+E / O-E
-        }
-    }
-    static QFT_HD vec2<T> descC(const vec2<T> *w, int k) { return descCJ<P::RC>(w, k); }
-    static QFT_HD vec2<T> descS(const vec2<T> *w, int k) { return descSJ<P::RC>(w, k); }
-
-    static QFT_HD void emit(vec2<T> *y, int k, vec2<T> cv, vec2<T> sv) {
-        // S(k) = (C1 + S2, C2 - S1), S(N-k) = (C1 - S2, C2 + S1) (shared.py:218-221):
-        // with u = (S2, -S1): S(k) = cv + u, S(N-k) = cv - u, bit for bit
-        // (x - (-y) == x + y and x + (-y) == x - y in IEEE arithmetic).
-        const vec2<T> u = {sv.y, -sv.x};
-        y[k] = vadd(cv, u);
-        y[P::N - k] = vsub(cv, u);
-    }
-
-    // regular thread: every index stays strictly inside (0, q_j) at every level
-    template <int J>
-    static QFT_HD void up(const vec2<T> *w, vec2<T> *y, int k, vec2<T> cv, vec2<T> sv) {
-        if constexpr (J == 0) {
-            emit(y, k, cv, sv);
-        } else {
-            constexpr int mm = 2 * qj(J - 1);
-            vec2<T> o = OC(w, J - 1, k), os = OS(w, J - 1, k);
-            up<J - 1>(w, y, k, vadd(cv, o), vadd(os, sv));
-            up<J - 1>(w, y, mm - k, vsub(cv, o), vsub(os, sv));
-        }
-    }
-
-    // special thread: groups of t = 0 and t = m_RC; every index is compile-time
-    template <int J, int K>
-    static QFT_HD void up_s(const vec2<T> *w, vec2<T> *y, vec2<T> cv, vec2<T> sv) {
-        if constexpr (J == 0) {
-            if constexpr (K == 0 || K == P::m) y[K] = cv;  // harmonics 0, N/2: copies
-            else emit(y, K, cv, sv);
-        } else {
-            constexpr int q = qj(J - 1), mm = 2 * q;
-            if constexpr (K == q) {                        // C copy, S leaf
-                up_s<J - 1, q>(w, y, cv, OS(w, J - 1, q));
-            } else {
-                vec2<T> o = OC(w, J - 1, K);
-                if constexpr (K == 0) {                    // no sine harmonic 0
-                    up_s<J - 1, 0>(w, y, vadd(cv, o), sv);
-                    up_s<J - 1, mm>(w, y, vsub(cv, o), sv);
-                } else {
-                    vec2<T> os = OS(w, J - 1, K);
-                    up_s<J - 1, K>(w, y, vadd(cv, o), vadd(os, sv));
-                    up_s<J - 1, mm - K>(w, y, vsub(cv, o), vsub(os, sv));
-                }
-            }
-        }
-    }
-
-    // t in [0, MRC): t = 0 is the special thread (groups 0 and MRC)
     // ---- uniform phase-D thread (t in [0, MRC], no special path) ----------
     // index of thread t's chain value at level J > RC: the distance of t to the
     // nearest multiple of m_{J-1} (composition of the folds k -> min(k, m_j - k))

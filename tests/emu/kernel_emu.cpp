@@ -24,47 +24,99 @@ static void build_U(int N, const T *Tnat, std::vector<T> &U) {
         for (int i = 0; i < S / 2; ++i) U[S / 2 + i] = Tnat[(2 * i + 1) * (N / (4 * S))];
 }
 
+// big warp unit (unit_big in qft_launch.cuh) on the block at padded pointer wb
+template <int L, int R, typename T, bool DST>
+static void emu_unit_big(vec2<T> *wb, const T *U) {
+    std::vector<FBlockP<L, R, DST, T>> f(32);
+    for (int t = 0; t < 32; ++t) f[t].load(wb, U, t);   // all lanes load ...
+    for (int t = 0; t < 32; ++t) f[t].store(wb, t);     // ... __syncwarp ... store
+    for (int p = 0; p < (1 << R); ++p) b_l32p<DST, T>(wb + 33 * p, U);
+    using CB = CBlockP<R, DST, T>;
+    std::vector<CB> c(32);
+    std::vector<std::vector<vec2<T>>> outs(32, std::vector<vec2<T>>(CB::G));
+    for (int i = 0; i < 32; ++i) c[i].load(wb, i);
+    for (int i = 0; i < 32; ++i) {
+        const vec2<T> *hc = CB::halo_colp(wb, i);  // the device reads the halo column before any store
+        auto halo = [&](int p) { return hc[33 * p]; };
+        c[i].compute(i, halo, outs[i].data());
+    }
+    for (int i = 0; i < 32; ++i) CB::storep(wb, i, outs[i].data());
+}
+
 template <int LOG2N, typename T, int J, bool DST>
 static void emu_f_side(vec2<T> *w, const T *U) {
     std::vector<FBlock<LOG2N, J, DST, T>> lanes(32);
-    for (int t = 0; t < 32; ++t) lanes[t].load(w, U, t);   // all lanes load ...
-    for (int t = 0; t < 32; ++t) lanes[t].store(w, t);     // ... __syncwarp ... store
+    for (int t = 0; t < 32; ++t) lanes[t].load(w, U, t);
+    for (int t = 0; t < 32; ++t) lanes[t].store(w, t);
 }
-
-template <int LOG2N, typename T, int J>
-static void emu_f(vec2<T> *w, const T *U) {
-    using P = SPlan<LOG2N>;
-    if constexpr (J < P::JF) {
-        emu_f_side<LOG2N, T, J, false>(w, U);
-        emu_f_side<LOG2N, T, J, true>(w, U);
-        emu_f<LOG2N, T, J + 1>(w, U);
-    }
-}
-
 template <int LOG2N, typename T, int J, bool DST>
 static void emu_c_side(vec2<T> *w) {
-    using CB = CBlock<LOG2N, J, DST, T>;
+    using P = SPlan<LOG2N>;
+    using CB = CBlockP<P::RF(J), DST, T>;
+    vec2<T> *wb = w + padx((DST ? P::S0 : 0) + P::off(J));
     std::vector<CB> lanes(32);
     std::vector<std::vector<vec2<T>>> outs(32, std::vector<vec2<T>>(CB::G));
-    for (int i = 0; i < 32; ++i) lanes[i].load(w, i);
+    for (int i = 0; i < 32; ++i) lanes[i].load(wb, i);
     for (int i = 0; i < 32; ++i) {
-        // the device gets the halo with a shuffle from lane i+1 (DCT) / i-1 (DST)
-        const int nb = DST ? i - 1 : i + 1;
-        const vec2<T> *hc = CB::halo_col(w, i);  // the device reads the halo column before any store
-        auto halo = [&](int p) { (void)nb; return hc[33 * p]; };
+        const vec2<T> *hc = CB::halo_colp(wb, i);
+        auto halo = [&](int p) { return hc[33 * p]; };
         lanes[i].compute(i, halo, outs[i].data());
     }
-    for (int i = 0; i < 32; ++i) CB::store(w, i, outs[i].data());
+    for (int i = 0; i < 32; ++i) CB::storep(wb, i, outs[i].data());
 }
-
-template <int LOG2N, typename T, int J>
-static void emu_c(vec2<T> *w) {
-    using P = SPlan<LOG2N>;
-    if constexpr (J < P::JF) {
-        emu_c_side<LOG2N, T, J, false>(w);
-        emu_c_side<LOG2N, T, J, true>(w);
-        emu_c<LOG2N, T, J + 1>(w);
+// rest unit (unit_rest): blocks JR..JF-1, Lee-32 chunks from K0, small blocks
+template <int LOG2N, typename T, int J, bool DST>
+static void emu_rest_f(vec2<T> *w, const T *U) {
+    if constexpr (J < SPlan<LOG2N>::JF) {
+        emu_f_side<LOG2N, T, J, DST>(w, U);
+        emu_rest_f<LOG2N, T, J + 1, DST>(w, U);
     }
+}
+template <int LOG2N, typename T, int J, bool DST>
+static void emu_rest_c(vec2<T> *w) {
+    if constexpr (J < SPlan<LOG2N>::JF) {
+        emu_c_side<LOG2N, T, J, DST>(w);
+        emu_rest_c<LOG2N, T, J + 1, DST>(w);
+    }
+}
+template <int LOG2N, typename T, bool DST>
+static void emu_unit_rest(vec2<T> *w, const T *U) {
+    using P = SPlan<LOG2N>;
+    emu_rest_f<LOG2N, T, P::JR, DST>(w, U);
+    for (int k = P::K0; k < P::NL32; ++k) b_l32<DST, T>(w, (DST ? P::S0 : 0) + 32 * k, U);
+    b_small<LOG2N, DST, T>(w, U);
+    emu_rest_c<LOG2N, T, P::JR, DST>(w);
+}
+// top levels (top_f / top_b): every item loads before any store
+template <int LOG2N, typename T, int J, bool DST>
+static void emu_top_f(vec2<T> *w, const T *U) {
+    if constexpr (J < SPlan<LOG2N>::JH) {
+        using TP = Top<LOG2N, J, DST, T>;
+        std::vector<vec2<T>> v(1024 * TP::G);
+        for (int t = 0; t < 1024; ++t) TP::f_load(w, U, t, &v[t * TP::G]);
+        for (int t = 0; t < 1024; ++t) TP::f_store(w, t, &v[t * TP::G]);
+        emu_top_f<LOG2N, T, J + 1, DST>(w, U);
+    }
+}
+template <int LOG2N, typename T, int J, bool DST>
+static void emu_top_b(vec2<T> *w) {
+    if constexpr (J < SPlan<LOG2N>::JH) {
+        using TP = Top<LOG2N, J, DST, T>;
+        std::vector<vec2<T>> o(1024 * TP::G);
+        for (int i = 0; i < 1024; ++i) TP::b_compute(w, i, &o[i * TP::G]);
+        for (int i = 0; i < 1024; ++i) TP::b_store(w, i, &o[i * TP::G]);
+        emu_top_b<LOG2N, T, J + 1, DST>(w);
+    }
+}
+// TF -> fused units -> TB of one side, in the kernel's order
+template <int LOG2N, typename T, bool DST>
+static void emu_side(vec2<T> *w, const T *U) {
+    using P = SPlan<LOG2N>;
+    emu_top_f<LOG2N, T, 0, DST>(w, U);
+    for (int bu = 0; bu < P::NU1; ++bu)
+        emu_unit_big<P::LB, P::RB, T, DST>(w + padx((DST ? P::S0 : 0) + P::big_cell(bu)), U);
+    emu_unit_rest<LOG2N, T, DST>(w, U);
+    emu_top_b<LOG2N, T, 0, DST>(w);
 }
 
 template <int LOG2N, typename T>
@@ -86,27 +138,8 @@ static void emu_one(const vec2<T> *x, vec2<T> *y, const T *U) {
         }
         a0_item<LOG2N, T>(x, w, 64 * c);
     }
-    // the kernel fuses F -> Lee-32 -> B per warp; blocks are independent, so the
-    // emulator may run the three stages block-set by block-set in any order
-    emu_f<LOG2N, T, 0>(w, U);
-    for (int k = 0; k < P::NL32; ++k) {
-        b_l32<false, T>(w, 32 * k, U);
-        b_l32<true, T>(w, P::S0 + 32 * k, U);
-    }
-    b_small<LOG2N, false, T>(w, U);
-    b_small<LOG2N, true, T>(w, U);
-    emu_c<LOG2N, T, 0>(w);
-#if QFT_CHAIN_MID
-    // chain-mid: level by level, all loads of a level before its stores (__syncwarp)
-    using C = Chain<LOG2N, T>;
-    C::mid_base(w);
-    for (int j = P::n - 2; j >= P::JM; --j) {
-        const int cnt = 2 * C::qj(j) + 1;
-        std::vector<vec2<T>> cv(cnt), sv(cnt);
-        for (int k = 0; k < cnt; ++k) C::mid_level_load(w, j, k, cv[k], sv[k]);
-        for (int k = 0; k < cnt; ++k) C::mid_level_store(w, j, k, cv[k], sv[k]);
-    }
-#endif
+    emu_side<LOG2N, T, false>(w, U);
+    emu_side<LOG2N, T, true>(w, U);
     for (int t = 0; t < P::DT; ++t) Chain<LOG2N, T>::unit(w, y, t);
 }
 
@@ -117,14 +150,8 @@ static void emu_real_one(const T *xa, const T *xb, T *ya, T *yb, const T *U) {
     std::vector<vec2<T>> Wv(P::PADDED);
     vec2<T> *w = Wv.data();
     for (int n = 0; n <= P::m; ++n) a0_item_real<LOG2N, T, MODE>(xa, xb, w, n);
-    emu_f<LOG2N, T, 0>(w, U);
-    for (int k = 0; k < P::NL32; ++k) {
-        b_l32<false, T>(w, 32 * k, U);
-        b_l32<true, T>(w, P::S0 + 32 * k, U);
-    }
-    b_small<LOG2N, false, T>(w, U);
-    b_small<LOG2N, true, T>(w, U);
-    emu_c<LOG2N, T, 0>(w);
+    if (MODE != 3) emu_side<LOG2N, T, false>(w, U);
+    if (MODE != 2) emu_side<LOG2N, T, true>(w, U);
     auto emit = [&](int k, vec2<T> cv, vec2<T> sv) {
         if constexpr (MODE == 1) {
             const bool edge = (k == 0) || (k == P::m);
@@ -154,6 +181,8 @@ static int emu_real_dispatch(int log2n, const T *xa, const T *xb, T *ya, T *yb, 
         case 10: emu_real_one<10, T, MODE>(xa, xb, ya, yb, U); return 0;
         case 11: emu_real_one<11, T, MODE>(xa, xb, ya, yb, U); return 0;
         case 12: emu_real_one<12, T, MODE>(xa, xb, ya, yb, U); return 0;
+        case 13: emu_real_one<13, T, MODE>(xa, xb, ya, yb, U); return 0;
+        case 14: emu_real_one<14, T, MODE>(xa, xb, ya, yb, U); return 0;
     }
     return -1;
 }
@@ -277,6 +306,8 @@ static int emu_dispatch(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
         case 10: emu_one<10, T>(x, y, U); return 0;
         case 11: emu_one<11, T>(x, y, U); return 0;
         case 12: emu_one<12, T>(x, y, U); return 0;
+        case 13: emu_one<13, T>(x, y, U); return 0;
+        case 14: emu_one<14, T>(x, y, U); return 0;
         default:
             if (log2n < 13 || log2n > 20) return -1;
             return sizeof(T) == 4 ? emu_large<T, 10, 5>(log2n, x, y, U) : emu_large<T, 9, 4>(log2n, x, y, U);
@@ -302,6 +333,27 @@ static int emu_real(int mode, int log2n, const T *x, T *y, long nrows, const T *
 }
 
 extern "C" {
+// multi-pass schedule emulation for any N = 2^13 .. 2^20
+int emu_large_f64(int log2n, const double *x, double *y, long batch, const double *Tnat) {
+    std::vector<double> U;
+    build_U(1 << log2n, Tnat, U);
+    for (long b = 0; b < batch; ++b) {
+        const long o = 2L * (1L << log2n) * b;
+        int rc = emu_large<double, 9, 4>(log2n, (const vec2<double> *)(x + o), (vec2<double> *)(y + o), U.data());
+        if (rc) return rc;
+    }
+    return 0;
+}
+int emu_large_f32(int log2n, const float *x, float *y, long batch, const float *Tnat) {
+    std::vector<float> U;
+    build_U(1 << log2n, Tnat, U);
+    for (long b = 0; b < batch; ++b) {
+        const long o = 2L * (1L << log2n) * b;
+        int rc = emu_large<float, 10, 5>(log2n, (const vec2<float> *)(x + o), (vec2<float> *)(y + o), U.data());
+        if (rc) return rc;
+    }
+    return 0;
+}
 int emu_real_f32(int mode, int log2n, const float *x, float *y, long nrows, const float *T) {
     return emu_real<float>(mode, log2n, x, y, nrows, T);
 }

@@ -25,15 +25,16 @@ def emu():
         subprocess.check_call([cxx, "-O1", "-std=c++17", "-fPIC", "-shared", "-ffp-contract=off",
                                "-o", EMU_LIB, src])
     lib = ctypes.CDLL(EMU_LIB)
-    for name in ("emu_cdft_f64", "emu_cdft_f32"):
+    for name in ("emu_cdft_f64", "emu_cdft_f32", "emu_large_f64", "emu_large_f32"):
         getattr(lib, name).argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_long,
                                        ctypes.c_void_p]
     return lib
 
 
 @pytest.mark.parametrize("dt", [np.complex128, np.complex64])
-@pytest.mark.parametrize("lg", list(range(1, 13)))
+@pytest.mark.parametrize("lg", list(range(1, 15)))
 def test_emulated_kernel_bitwise(emu, oracle_mod, dt, lg):
+    """Single-pass kernel phases (N <= 2^14: top levels + 1024-cell units above 4096)."""
     N = 1 << lg
     rt = np.float32 if dt == np.complex64 else np.float64
     rng = np.random.default_rng(100 + lg)
@@ -47,7 +48,7 @@ def test_emulated_kernel_bitwise(emu, oracle_mod, dt, lg):
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
-@pytest.mark.parametrize("lg", [6, 9, 12])
+@pytest.mark.parametrize("lg", [6, 9, 12, 13, 14])
 @pytest.mark.parametrize("kind", ["rdft", "dct0", "dst0"])
 def test_emulated_real_modes_bitwise(emu, oracle_mod, dt, lg, kind):
     """improved.rdft/dct0/dst0 through the same phase functions (two real rows per lane)."""
@@ -65,3 +66,18 @@ def test_emulated_real_modes_bitwise(emu, oracle_mod, dt, lg, kind):
     assert fn({"rdft": 1, "dct0": 2, "dst0": 3}[kind], lg, x.ctypes.data, y.ctypes.data, 4, T.ctypes.data) == 0
     want = getattr(oracle_mod, kind)(np.ascontiguousarray(x.T)).T
     assert bit_equal(y, np.ascontiguousarray(want))
+
+
+@pytest.mark.parametrize("dt", [np.complex128, np.complex64])
+@pytest.mark.parametrize("lg", [13, 14, 16])
+def test_emulated_multipass_bitwise(emu, oracle_mod, dt, lg):
+    """The multi-pass schedule (qft_large_plan.h task lists + qft_large.cuh phases)."""
+    N = 1 << lg
+    rt = np.float32 if dt == np.complex64 else np.float64
+    rng = np.random.default_rng(200 + lg)
+    z = (rng.standard_normal((1, N)) + 1j * rng.standard_normal((1, N))).astype(dt)
+    y = np.empty_like(z)
+    T = oracle_mod.table(N, rt)
+    fn = emu.emu_large_f32 if dt == np.complex64 else emu.emu_large_f64
+    assert fn(lg, z.ctypes.data, y.ctypes.data, 1, T.ctypes.data) == 0
+    assert bit_equal(y, oracle_mod.cdft_rows(z))

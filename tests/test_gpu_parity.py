@@ -214,12 +214,16 @@ def test_large_batch_properties(torch_cuda):
 
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
-@pytest.mark.parametrize("lg", list(range(1, 13)))
+@pytest.mark.parametrize("lg", list(range(1, 15)))
 @pytest.mark.parametrize("kind", ["rdft", "dct0", "dst0"])
 def test_real_entry_points_bitwise(torch_cuda, oracle_mod, dt, lg, kind):
     """improved.rdft / dct0 / dst0 (improved.py:117-136) on the GPU, bit-identical."""
     from paper_1301_0763_b200 import improved
     N = 1 << lg
+    if lg == 14 and dt == np.float64:
+        with pytest.raises(NotImplementedError):   # working area exceeds shared memory
+            getattr(improved, kind)(np.zeros(({"rdft": N, "dct0": N // 2 + 1, "dst0": N // 2 - 1}[kind], 2)))
+        return
     if kind == "dst0" and N < 4:
         pytest.skip("the sine transform needs N >= 4")
     n_vals = {"rdft": N, "dct0": N // 2 + 1, "dst0": N // 2 - 1}[kind]
@@ -312,3 +316,31 @@ def test_classical_config4_accuracy_comparison(torch_cuda, oracle_mod):
     ei = np.linalg.norm(yi - ref) / np.linalg.norm(ref)
     ec = np.linalg.norm(yc - ref) / np.linalg.norm(ref)
     assert ei < 1e-12 and ec < 1e-12
+
+
+@pytest.mark.parametrize("dt", [np.complex64, np.complex128])
+@pytest.mark.parametrize("lg", [13, 14])
+def test_single_pass_and_multipass_agree(torch_cuda, oracle_mod, dt, lg, monkeypatch):
+    """N = 2^13 / 2^14 run single-pass (top levels + 1024-cell units) where the
+    working area fits; QFT_MULTIPASS=1 forces the multi-pass schedule.  Both are
+    bit-identical to the oracle."""
+    import torch
+    from paper_1301_0763_b200 import _native
+    N = 1 << lg
+    prec = 32 if dt == np.complex64 else 64
+    rng = np.random.default_rng(lg + prec)
+    z = (rng.standard_normal((5, N)) + 1j * rng.standard_normal((5, N))).astype(dt)
+    want = oracle_mod.cdft_rows(z)
+    outs = {}
+    for mp in ("0", "1"):
+        monkeypatch.setenv("QFT_MULTIPASS", mp)
+        p = _native.Plan(lg, prec)           # uncached: the variable is read at plan creation
+        info = p.info()
+        single = not (prec == 64 and lg == 14) and mp == "0"
+        assert (info.passes == 1) == single, (mp, info.passes)
+        x = torch.from_numpy(z).cuda()
+        y = torch.empty_like(x)
+        p.exec_device(x.data_ptr(), y.data_ptr(), 5, (N, 1), (N, 1))
+        torch.cuda.synchronize()
+        outs[mp] = y.cpu().numpy()
+        assert bit_equal(outs[mp], want), mp
