@@ -16,6 +16,8 @@
 
 #include "qft_large_api.h"
 #include "qft_large_plan.h"
+#include "qft_launch.cuh"
+#include "qft_leaf.cuh"
 
 #if !defined(QFT_LARGE_PREC)
 #error "compile with -DQFT_LARGE_PREC=32|64"
@@ -32,7 +34,8 @@ using namespace qft;
 
 namespace {
 
-constexpr int kLeafLog = QFT_LARGE_PREC == 32 ? 10 : 9;  // warp leaf: L <= 1024 (fp32) / 512 (fp64)
+// largest single-pass sub-signal / leaf: 2^14 cells fp32, 2^13 fp64 (128 KiB)
+constexpr int kSubLogMax = QFT_LARGE_PREC == 32 ? 14 : 13;
 constexpr int kRG = QFT_LARGE_PREC == 32 ? 5 : 4;         // fold levels per F/B pass
 constexpr int kRC = 4;                                    // chain levels unfolded per thread
 constexpr int kChunk = 256;
@@ -53,16 +56,22 @@ struct TaskSet {  // one launch: tasks of one kind and one R (or log2 L for leav
     int ntasks = 0, nchunks = 0;
 };
 
-using Sched = LargeSchedule<kLeafLog, kRG>;
+using Sched = LargeSchedule;
 
 }  // namespace
 
+// N = 2^n: the sub-signal has 2^sublog points, J0 = n - sublog
+static int sublog_for(int log2n) { return log2n - 1 < kSubLogMax ? log2n - 1 : kSubLogMax; }
+
 struct QFT_LG(LargePlan) {
+    int sublog, J0;
     Sched s;
     std::vector<std::vector<TaskSet>> fset, bset;
-    std::vector<TaskSet> lset;
+    void *d_items = nullptr, *d_leaves = nullptr;
+    int nitems = 0;
     int launches = 0;
-    explicit QFT_LG(LargePlan)(int log2n) : s(log2n) {}
+    explicit QFT_LG(LargePlan)(int log2n)
+        : sublog(sublog_for(log2n)), J0(log2n - sublog_for(log2n)), s(log2n, sublog_for(log2n), kRG, J0) {}
 };
 
 template <typename TT>
@@ -73,14 +82,6 @@ static int upload(const std::vector<TT> &v, void **d) {
 }
 
 // ------------------------------------------------------------------ kernels
-template <typename T>
-__global__ void lg_fold_kernel(const vec2<T> *__restrict__ x, vec2<T> *__restrict__ W0, int N, int log2n,
-                               long long batch, long long Ws) {
-    const int n = blockIdx.x * blockDim.x + threadIdx.x;
-    if (n >= N / 2) return;
-    for (long long b = blockIdx.y; b < batch; b += gridDim.y) lg_fold_item<T>(x + b * N, W0 + b * Ws, n, N, log2n);
-}
-
 template <int R, typename T>
 __device__ __forceinline__ void lg_f_dispatch_r(vec2<T> *w, const FTask &tk, int t, bool dst, const T *U,
                                                 const vec2<T> *x, int N) {
@@ -149,82 +150,155 @@ __global__ void __launch_bounds__(kBChunk) lg_b_kernel(vec2<T> *W0, vec2<T> *W1,
     }
 }
 
-template <int L, typename T>
-__global__ void lg_leaf_thread_kernel(vec2<T> *W0, const LeafTask *__restrict__ tasks, int ntasks, long long batch,
-                                      long long Ws, const __grid_constant__ LeeConstL<T> kc,
-                                      const vec2<T> *__restrict__ x, int N) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= ntasks) return;
-    const LeafTask tk = tasks[k];
-    for (long long b = blockIdx.y; b < batch; b += gridDim.y) {
-        if (tk.dst) lg_leaf_thread<L, T, true>(W0 + b * Ws, tk, kc.u, x + b * N, N);
-        else lg_leaf_thread<L, T, false>(W0 + b * Ws, tk, kc.u, x + b * N, N);
-    }
-}
+// ------------------------------------------------------------------ item kernel
+// One persistent kernel runs every CTA-resident work item of every signal,
+// signal-major (the items of a signal run concurrently, so the strided input
+// gathers of its sub-signal and leaves share L2-resident sectors):
+//   SUB  the 2^SUBLOG-point improved transform of the sub-signal x[k 2^J0]
+//        (blocks j >= J0 of the time-parity chain) through the single-pass
+//        phases of qft_launch.cuh; phase D emits C_J0 / S_J0 instead of y
+//   LEAF one Lee block (or two of half the size) of 2^SUBLOG cells: whole
+//        blocks fold x on load, sub-blocks of the F passes come from W0;
+//        TF / warp units / TB (qft_leaf.cuh), spectrum written along the run
+struct Item {
+    int kind, k0;  // kind 0: SUB, 1: leaf task k0, 2: leaf tasks k0 and k0+1
+};
 
-template <int R, typename T>
-__global__ void __launch_bounds__(128) lg_leaf_warp_kernel(vec2<T> *W0, const LeafTask *__restrict__ tasks, int ntasks,
-                                                           long long batch, long long Ws, const T *__restrict__ U,
-                                                           const __grid_constant__ LeeConstL<T> kc,
-                                                           const vec2<T> *__restrict__ x, int N) {
-    constexpr int L = 32 << R, PADL = L + L / 32 + 1;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    vec2<T> *s = reinterpret_cast<vec2<T> *>(smem_raw) + warp * PADL;
-    const int k = blockIdx.x * 4 + warp;
-    if (k >= ntasks) return;
-    const LeafTask tk = tasks[k];
-    for (long long b = blockIdx.y; b < batch; b += gridDim.y) {
-        vec2<T> *w = W0 + b * Ws;
+template <int SUBLOG, typename T>
+struct ItemCfg {
+    using K = KCfg<SUBLOG, T>;
+    using P = SPlan<SUBLOG>;
+    static constexpr int NT = K::NT, NW = K::NW, L = 1 << SUBLOG;
+    static constexpr int VB = (int)sizeof(vec2<T>);
+    static constexpr int LPAD = L + L / 32 + 1;
+    static constexpr int WCELLS = P::PADDED > LPAD ? P::PADDED : LPAD;
+    static constexpr int UCELLS = L;  // level constants of every block size <= L
+    static constexpr int U_OFF = WCELLS * VB;
+    static constexpr int SMEM = U_OFF + UCELLS * (int)sizeof(T);
+};
+
+template <int A, typename T, int NT, int NW>
+QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const T *kcu, const vec2<T> *xb,
+                       vec2<T> *wb, int N, int tid) {
+    constexpr int L = 1 << A;
+    const int warp = tid >> 5, lane = tid & 31;
+    // load (fold on load for whole blocks)
+    for (int k = 0; k < K; ++k) {
+        const LeafTask tk = tks[k];
+        vec2<T> *s = S + padx(k * L);
         if (tk.j >= 0) {
-            const vec2<T> *xb = x + b * N;
 #pragma unroll 4
-            for (int e = lane; e < L; e += 32)
-                s[e + (e >> 5)] = tk.dst ? fold_load<T, true>(xb, N, tk.j, e) : fold_load<T, false>(xb, N, tk.j, e);
+            for (int e = tid; e < L; e += NT)
+                s[padx(e)] = tk.dst ? fold_load<T, true>(xb, N, tk.j, e) : fold_load<T, false>(xb, N, tk.j, e);
         } else {
 #pragma unroll 8
-            for (int e = lane; e < L; e += 32) s[e + (e >> 5)] = w[tk.c + tk.sg * e];
+            for (int e = tid; e < L; e += NT) s[padx(e)] = wb[tk.c + tk.sg * e];
         }
-        __syncwarp();
-        if (tk.dst) {
-            using WL = WarpLee<R, T, true>;
-            typename WL::F f;
-            f.load(s, lane, U);
-            __syncwarp();
-            f.store(s, lane);
-            __syncwarp();
-            if (lane < (1 << R)) WL::lee32(s, lane, kc.u);
-            __syncwarp();
-            typename WL::B bb;
-            bb.compute(s, lane);
-            __syncwarp();
-            bb.store(s, lane);
+    }
+    __syncthreads();
+    // TF: top fold levels in place
+    for (int it = tid; it < K * 1024; it += NT) {
+        const int k = it >> 10, t = it & 1023;
+        vec2<T> *s = S + padx(k * L);
+        if (tks[k].dst) LeafTop<A, true, T>::tf(s, U, t);
+        else LeafTop<A, false, T>::tf(s, U, t);
+    }
+    __syncthreads();
+    // 1024-cell warp units on the (possibly reversed) sub-block runs
+    constexpr int NSUB = L / 1024;
+    for (int u = warp; u < K * NSUB; u += NW) {
+        const int k = u / NSUB, p = u - k * NSUB;
+        int lo;
+        bool rev;
+        LeafTop<A, false, T>::sub(p, lo, rev);
+        vec2<T> *ws = S + padx(k * L) + padx(lo);
+        const bool dst = tks[k].dst;
+        if (dst) {
+            if (rev) unit_big<1024, 5, T, true, true>(ws, U, kcu, lane);
+            else unit_big<1024, 5, T, true, false>(ws, U, kcu, lane);
         } else {
-            using WL = WarpLee<R, T, false>;
-            typename WL::F f;
-            f.load(s, lane, U);
-            __syncwarp();
-            f.store(s, lane);
-            __syncwarp();
-            if (lane < (1 << R)) WL::lee32(s, lane, kc.u);
-            __syncwarp();
-            typename WL::B bb;
-            bb.compute(s, lane);
-            __syncwarp();
-            bb.store(s, lane);
+            if (rev) unit_big<1024, 5, T, false, true>(ws, U, kcu, lane);
+            else unit_big<1024, 5, T, false, false>(ws, U, kcu, lane);
         }
         __syncwarp();
-        for (int e = lane; e < L; e += 32) w[tk.c + tk.sg * e] = s[e + (e >> 5)];
-        __syncwarp();
+    }
+    __syncthreads();
+    // TB: block spectrum straight to the leaf's run in W0
+    constexpr int G = LeafTop<A, false, T>::G;
+    for (int it = tid; it < K * 1024; it += NT) {
+        const int k = it >> 10, i = it & 1023;
+        const LeafTask tk = tks[k];
+        const vec2<T> *s = S + padx(k * L);
+        vec2<T> out[G];
+        if (tk.dst) LeafTop<A, true, T>::tb(s, i, out);
+        else LeafTop<A, false, T>::tb(s, i, out);
+        vec2<T> *o = wb + tk.c + tk.sg * (i * G);
+#pragma unroll
+        for (int q = 0; q < G; ++q) o[tk.sg * q] = out[q];
     }
 }
 
-template <typename T, int LOG2N>
+template <int SUBLOG, typename T>
+QFT_DEV void sub_item(const vec2<T> *xb, long long stride, vec2<T> *W, const T *U, const T *kcu, vec2<T> *cbuf,
+                      vec2<T> *sbuf, int tid) {
+    using P = SPlan<SUBLOG>;
+    using C = ItemCfg<SUBLOG, T>;
+    constexpr int NT = C::NT, NW = C::NW;
+    const int warp = tid >> 5, lane = tid & 31;
+#pragma unroll 4
+    for (int nn = tid; nn < P::m; nn += NT) a0_item_s<SUBLOG, T>(xb, stride, W, nn);
+    __syncthreads();
+    if constexpr (P::JH > 0) top_f<SUBLOG, T, 0>(W, U, 1, tid);
+    fused_units<SUBLOG, T, 0, 1, NW>(W, U, kcu, 1, warp, lane);
+    __syncthreads();
+    if constexpr (P::JH > 0) top_b<SUBLOG, T, 0>(W, 1, tid);
+    // C_J0[k] = cv, S_J0[k] = sv for k in [0, m'] (S_J0 at 0 and m' unused)
+    auto emit = [&](int k, vec2<T> cv, vec2<T> sv) {
+        cbuf[k] = cv;
+        sbuf[k] = sv;
+    };
+    for (int t = tid; t < P::DT; t += NT) Chain<SUBLOG, T>::unit_e(W, emit, t);
+}
+
+template <int SUBLOG, typename T>
+__global__ void __launch_bounds__(ItemCfg<SUBLOG, T>::NT, 1)
+    lg_item_kernel(const vec2<T> *__restrict__ x, vec2<T> *W0, long long Ws, int log2n, int J0,
+                   const Item *__restrict__ items, int ni, const LeafTask *__restrict__ tasks, long long batch,
+                   const T *__restrict__ Ug, const __grid_constant__ LeeConstL<T> kc) {
+    using C = ItemCfg<SUBLOG, T>;
+    constexpr int NT = C::NT, NW = C::NW;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    vec2<T> *S = reinterpret_cast<vec2<T> *>(smem_raw);
+    T *U = reinterpret_cast<T *>(smem_raw + C::U_OFF);
+    const int tid = threadIdx.x;
+    const int N = 1 << log2n;
+    const int nu = C::UCELLS < N / 4 ? C::UCELLS : N / 4;
+    for (int i = tid; i < nu; i += NT) U[i] = Ug[i];
+    __syncthreads();
+    for (long long g = blockIdx.x; g < batch * ni; g += gridDim.x) {
+        const long long b = g / ni;
+        const Item it = items[g - b * ni];
+        const vec2<T> *xb = x + b * N;
+        vec2<T> *wb = W0 + b * Ws;
+        if (it.kind == 0) {
+            vec2<T> *cbuf = wb + (N + 2);
+            sub_item<SUBLOG, T>(xb, 1ll << J0, S, U, kc.u, cbuf, cbuf + SPlan<SUBLOG>::m + 1, tid);
+        } else if (it.kind == 1) {
+            leaf_item<SUBLOG, T, NT, NW>(tasks + it.k0, 1, S, U, kc.u, xb, wb, N, tid);
+        } else {
+            leaf_item<SUBLOG - 1, T, NT, NW>(tasks + it.k0, 2, S, U, kc.u, xb, wb, N, tid);
+        }
+        __syncthreads();
+    }
+}
+
+template <typename T, int LOG2N, int RC>
 __global__ void lg_chain_kernel(const vec2<T> *W0, const vec2<T> *W1, const vec2<T> *__restrict__ x,
-                                vec2<T> *__restrict__ y, uint32_t cmask, uint32_t smask, long long batch, long long Ws) {
+                                vec2<T> *__restrict__ y, uint32_t cmask, uint32_t smask, long long batch, long long Ws,
+                                int J0, int mj0) {
     constexpr int N = 1 << LOG2N;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t > (N >> (kRC + 1))) return;
+    if (t > (N >> (RC + 1))) return;
     for (long long b = blockIdx.y; b < batch; b += gridDim.y) {
         GChain<T> g;
         g.n = LOG2N;
@@ -235,7 +309,10 @@ __global__ void lg_chain_kernel(const vec2<T> *W0, const vec2<T> *W1, const vec2
         g.x = x + (long long)b * N;
         g.cmask = cmask;
         g.smask = smask;
-        g.template unit<kRC>(y + b * N, t);
+        g.J0 = J0;
+        g.cb = g.w0 + (N + 2);
+        g.sb = g.cb + mj0 + 1;
+        g.template unit<RC>(y + b * N, t);
     }
 }
 
@@ -290,14 +367,24 @@ int QFT_LG(qft_large_create)(int log2n, void **out) {
             p->bset[d].push_back(ts);
         }
     }
-    for (auto &kv : S.leaf) {
-        TaskSet ts;
-        ts.R = kv.first;  // log2 L
-        ts.ntasks = (int)kv.second.size();
-        rc |= upload(kv.second, &ts.d_tasks);
-        p->lset.push_back(ts);
+    // work items per signal: the sub-signal, every 2^sublog leaf, pairs of 2^(sublog-1) leaves
+    {
+        std::vector<Item> items{{0, 0}};
+        std::vector<LeafTask> leaves;
+        for (auto &kv : S.leaf) {
+            if (kv.first != p->sublog && kv.first != p->sublog - 1) return -1;  // schedule invariant
+            const bool pair = kv.first == p->sublog - 1;
+            if (pair && kv.second.size() % 2) return -1;
+            for (size_t i = 0; i < kv.second.size(); i += pair ? 2 : 1) {
+                items.push_back({pair ? 2 : 1, (int)leaves.size()});
+                leaves.push_back(kv.second[i]);
+                if (pair) leaves.push_back(kv.second[i + 1]);
+            }
+        }
+        p->nitems = (int)items.size();
+        rc |= upload(items, &p->d_items) | upload(leaves, &p->d_leaves);
     }
-    p->launches = 2 + (int)p->lset.size();
+    p->launches = 2;
     for (auto &v : p->fset) p->launches += (int)v.size();
     for (auto &v : p->bset) p->launches += (int)v.size();
     *out = p;
@@ -315,7 +402,8 @@ void QFT_LG(qft_large_destroy)(void *pp) {
                 cudaFree(t.d_chunks);
                 cudaFree(t.d_rs);
             }
-    for (auto &t : p->lset) cudaFree(t.d_tasks);
+    cudaFree(p->d_items);
+    cudaFree(p->d_leaves);
     delete p;
 }
 
@@ -327,7 +415,8 @@ void QFT_LG(qft_large_info)(void *pp, int *passes, int *launches) {
 
 long long QFT_LG(qft_large_scratch_cells)(void *pp) {
     auto *p = (QFT_LG(LargePlan) *)pp;
-    return (long long)p->s.N + 2;  // per signal and buffer
+    // per signal and buffer: N+2 cells + C_J0 / S_J0 of the sub-signal
+    return (long long)p->s.N + 2 + 2 * ((1ll << (p->sublog - 1)) + 1);
 }
 
 int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long batch, const void *d_U,
@@ -335,7 +424,7 @@ int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long ba
     auto *p = (QFT_LG(LargePlan) *)pp;
     using T = Real;
     const Sched &S = p->s;
-    const long long Ws = (long long)S.N + 2;
+    const long long Ws = QFT_LG(qft_large_scratch_cells)(pp);
     vec2<T> *W0 = (vec2<T> *)scratch, *W1 = W0 + batch * Ws;
     const vec2<T> *x = (const vec2<T> *)d_in;
     vec2<T> *y = (vec2<T> *)d_out;
@@ -354,34 +443,30 @@ int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long ba
                        Ws, x, S.N);
             if (e) return (int)e;
         }
-    // leaves
-    for (auto &ts : p->lset) {
-        const LeafTask *tk = (const LeafTask *)ts.d_tasks;
-        const int lg = ts.R;
-        if (lg <= 5) {
-            dim3 g((ts.ntasks + 127) / 128, yb);
-            switch (lg) {
-                case 0: e = launch(lg_leaf_thread_kernel<1, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc, x, S.N); break;
-                case 1: e = launch(lg_leaf_thread_kernel<2, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc, x, S.N); break;
-                case 2: e = launch(lg_leaf_thread_kernel<4, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc, x, S.N); break;
-                case 3: e = launch(lg_leaf_thread_kernel<8, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc, x, S.N); break;
-                case 4: e = launch(lg_leaf_thread_kernel<16, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc, x, S.N); break;
-                case 5: e = launch(lg_leaf_thread_kernel<32, T>, g, dim3(128), 0, st, W0, tk, ts.ntasks, batch, Ws, kc, x, S.N); break;
-            }
-        } else {
-            const int R = lg - 5, L = 32 << R;
-            const size_t smem = 4 * (size_t)(L + L / 32 + 1) * sizeof(vec2<T>);
-            dim3 g((ts.ntasks + 3) / 4, yb);
-            switch (R) {
-                case 1: e = launch(lg_leaf_warp_kernel<1, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc, x, S.N); break;
-                case 2: e = launch(lg_leaf_warp_kernel<2, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc, x, S.N); break;
-                case 3: e = launch(lg_leaf_warp_kernel<3, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc, x, S.N); break;
-                case 4: e = launch(lg_leaf_warp_kernel<4, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc, x, S.N); break;
+    // sub-signal + leaves (one persistent launch)
+    {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const long long work = batch * p->nitems;
+        const unsigned grid = (unsigned)std::min<long long>(work, sms);
+        const Item *it = (const Item *)p->d_items;
+        const LeafTask *lv = (const LeafTask *)p->d_leaves;
+        auto run = [&](auto kern, int nt, int smem) -> cudaError_t {
+            cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e2) return e2;
+            return launch(kern, dim3(grid), dim3(nt), (size_t)smem, st, x, W0, Ws, S.n, p->J0, it, p->nitems, lv,
+                          batch, U, kc);
+        };
+        switch (p->sublog) {
+#define QFT_IT(SL) \
+    case SL: e = run(lg_item_kernel<SL, T>, ItemCfg<SL, T>::NT, ItemCfg<SL, T>::SMEM); break;
+            QFT_IT(12) QFT_IT(13)
 #if QFT_LARGE_PREC == 32
-                case 5: e = launch(lg_leaf_warp_kernel<5, T>, g, dim3(128), smem, st, W0, tk, ts.ntasks, batch, Ws, U, kc, x, S.N); break;
+            QFT_IT(14)
 #endif
-                default: return (int)cudaErrorInvalidValue;
-            }
+#undef QFT_IT
+            default: return (int)cudaErrorInvalidValue;
         }
         if (e) return (int)e;
     }
@@ -404,16 +489,21 @@ int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long ba
             }
             if (e) return (int)e;
         }
-    // chain + recombination
-    const int threads = (S.N >> (kRC + 1)) + 1;
+    // chain levels J0-1 .. 0 + recombination
+    const int RC = p->J0 < kRC ? p->J0 : kRC;
+    const int threads = (S.N >> (RC + 1)) + 1;
     const dim3 cg((threads + 127) / 128, yb), cb(128);
     const vec2<T> *w0 = W0, *w1 = W1;
-    switch (S.n) {
-#define QFT_CH(LG) case LG: e = launch(lg_chain_kernel<T, LG>, cg, cb, 0, st, w0, w1, x, y, S.cmask, S.smask, batch, Ws); break;
-        QFT_CH(13) QFT_CH(14) QFT_CH(15) QFT_CH(16) QFT_CH(17) QFT_CH(18) QFT_CH(19) QFT_CH(20)
-#undef QFT_CH
+    const int mj0 = 1 << (p->sublog - 1);
+#define QFT_CH(LG, R) \
+    case LG * 8 + R: e = launch(lg_chain_kernel<T, LG, R>, cg, cb, 0, st, w0, w1, x, y, S.cmask, S.smask, batch, Ws, p->J0, mj0); break;
+#define QFT_CHR(LG) QFT_CH(LG, 1) QFT_CH(LG, 2) QFT_CH(LG, 3) QFT_CH(LG, 4)
+    switch (S.n * 8 + RC) {
+        QFT_CHR(13) QFT_CHR(14) QFT_CHR(15) QFT_CHR(16) QFT_CHR(17) QFT_CHR(18) QFT_CHR(19) QFT_CHR(20)
         default: return (int)cudaErrorInvalidValue;
     }
+#undef QFT_CHR
+#undef QFT_CH
     return (int)e;
 }
 

@@ -223,6 +223,10 @@ struct GChain {
     const vec2<T> *x;        // the input signal: base pair s(0) = x[0], s(m) = x[m]
     uint32_t cmask, smask;   // bit j: the cosine / sine spectrum of block j is in W1
     int n, N, m;
+    // J0 > 0: C_J0[k], S_J0[k] (k in [0, m_J0]) come from the sub-signal
+    // transform (cb, sb) instead of the descent from the DCT base
+    int J0 = 0;
+    const vec2<T> *cb = nullptr, *sb = nullptr;
 
     QFT_HD int off(int j) const { return m - (1 << (n - 1 - j)); }
     QFT_HD vec2<T> OC(int j, int k) const { return ((cmask >> j) & 1 ? w1 : w0)[off(j) + k]; }
@@ -239,13 +243,19 @@ struct GChain {
             const int r = t & (P - 1);
             return r < P - r ? r : P - r;
         };
-        {
+        int Jtop = n - 2;
+        if (J0 > 0) {
+            const int k0 = kk(J0);
+            cv = cb[k0];
+            sv = sb[k0];
+            Jtop = J0 - 1;
+        } else {
             const vec2<T> s0 = x[0], sm = x[m];
             cv = kk(n - 1) == 0 ? vadd(s0, sm) : vsub(s0, sm);
+            sv = vec2<T>{(T)0, (T)0};
         }
-        sv = vec2<T>{(T)0, (T)0};
 #pragma unroll 20
-        for (int J = n - 2; J >= RC; --J) {
+        for (int J = Jtop; J >= RC; --J) {
             const int k = kk(J), q = qj(J);
             const int k1 = k < q ? k : 2 * q - k;  // index at level J+1
             if (k != q) {

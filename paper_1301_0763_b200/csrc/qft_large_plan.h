@@ -19,9 +19,9 @@
 
 namespace qft {
 
-template <int LEAFLOG, int RG>
 struct LargeSchedule {
     int n = 0, N = 0, m = 0;
+    int LEAFLOG = 10, RG = 5;  // leaf size 2^LEAFLOG, fold levels per F/B pass
     std::vector<std::map<int, std::vector<std::pair<FTask, int>>>> f;  // [depth][R] -> (task, dst)
     std::vector<std::map<int, std::vector<BTask>>> b;                  // [depth][R]
     std::map<int, std::vector<LeafTask>> leaf;                         // [log2 L]
@@ -55,9 +55,13 @@ struct LargeSchedule {
         return {1 - sub.buf, 0};
     }
 
-    explicit LargeSchedule(int log2n) : n(log2n), N(1 << log2n), m(1 << (log2n - 1)) {
+    // jmax > 0: only the blocks j < jmax (the rest belong to the sub-signal
+    // transform of x[2^jmax k], see qft_large.cu)
+    LargeSchedule(int log2n, int leaflog, int rg, int jmax = -1)
+        : n(log2n), N(1 << log2n), m(1 << (log2n - 1)), LEAFLOG(leaflog), RG(rg) {
+        const int jend = jmax > 0 ? jmax : n - 1;
         for (int side = 0; side < 2; ++side)
-            for (int j = 0; j <= n - 2; ++j) {
+            for (int j = 0; j < jend; ++j) {
                 const int L = 1 << (n - 2 - j);
                 Loc l = decompose(side * m + m - 2 * L, 1, L, side, 0, j);  // first touch folds x
                 if (l.buf) (side ? smask : cmask) |= 1u << j;

@@ -255,10 +255,10 @@ QFT_DEV void run_c_blocks(vec2<T> *w, bool dst, int lane) {
 // runs it start to finish with __syncwarp only (no CTA barrier).
 // big unit: a block of L = 32 << R cells at padded pointer wb (block 0 for
 // N <= 4096, a 1024-cell (sub-)block for N > 4096): one Lee-32 per lane
-template <int L, int R, typename T, bool DST>
+template <int L, int R, typename T, bool DST, bool REV = false>
 QFT_DEV void unit_big(vec2<T> *wb, const T *U, const T *kcu, int lane) {
     FBlockP<L, R, DST, T> f;
-    f.load(wb, U, lane);
+    f.template load<REV>(wb, U, lane);
     __syncwarp();
     f.store(wb, lane);
     __syncwarp();
@@ -357,6 +357,30 @@ template <int LOG2N, typename T, int MODE>
 QFT_DEV void top_b(vec2<T> *W, int ntr, int tid) {
     for (int tau = 0; tau < ntr; ++tau) top_b_sig<LOG2N, T, MODE, 0>(W + tau * SPlan<LOG2N>::PADDED, tid);
     __syncthreads();
+}
+
+// A+B+C of TT signals, one warp per (signal, side, unit)
+template <int LOG2N, typename T, int MODE, int TT, int NW>
+QFT_DEV void fused_units(vec2<T> *W, const T *U, const T *kcu, int ntr, int warp, int lane) {
+    using P = SPlan<LOG2N>;
+    constexpr int NU = 2 * (P::NU1 + 1);
+    for (int u = warp; u < TT * NU; u += NW) {
+        const int tau = u / NU, kind = u - tau * NU;
+        if (tau >= ntr) continue;
+        vec2<T> *w = W + tau * P::PADDED;
+        const bool dst = kind & 1;
+        if ((MODE == 2 && dst) || (MODE == 3 && !dst)) continue;  // side not needed
+        const int bu = kind >> 1;
+        if (bu < P::NU1) {
+            vec2<T> *wb = w + padx((dst ? P::S0 : 0) + P::big_cell(bu));
+            if (dst) unit_big<P::LB, P::RB, T, true>(wb, U, kcu, lane);
+            else unit_big<P::LB, P::RB, T, false>(wb, U, kcu, lane);
+        } else {
+            if (dst) unit_rest<LOG2N, T, true>(w, U, kcu, lane);
+            else unit_rest<LOG2N, T, false>(w, U, kcu, lane);
+        }
+        __syncwarp();
+    }
 }
 
 // A0 of TT complex signals from src (staging buffer or global memory): chunks
@@ -460,23 +484,7 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
         // TF: top forward levels of the huge blocks (N > 4096; ends with a barrier)
         if constexpr (P::JH > 0) top_f<LOG2N, T, MODE>(W, U, ntr, tid);
         // A+B+C fused: one warp per (signal, side, unit) -- no CTA barrier inside
-        for (int u = warp; u < TT * K::NU; u += NW) {
-            const int tau = u / K::NU, kind = u - tau * K::NU;
-            if (tau >= ntr) continue;
-            vec2<T> *w = W + tau * P::PADDED;
-            const bool dst = kind & 1;
-            if ((MODE == 2 && dst) || (MODE == 3 && !dst)) continue;  // side not needed
-            const int bu = kind >> 1;
-            if (bu < P::NU1) {
-                vec2<T> *wb = w + padx((dst ? P::S0 : 0) + P::big_cell(bu));
-                if (dst) unit_big<P::LB, P::RB, T, true>(wb, U, kc.u, lane);
-                else unit_big<P::LB, P::RB, T, false>(wb, U, kc.u, lane);
-            } else {
-                if (dst) unit_rest<LOG2N, T, true>(w, U, kc.u, lane);
-                else unit_rest<LOG2N, T, false>(w, U, kc.u, lane);
-            }
-            __syncwarp();
-        }
+        fused_units<LOG2N, T, MODE, TT, NW>(W, U, kc.u, ntr, warp, lane);
         __syncthreads();
         // TB: top backward levels of the huge blocks (ends with a barrier)
         if constexpr (P::JH > 0) top_b<LOG2N, T, MODE>(W, ntr, tid);

@@ -102,6 +102,23 @@ QFT_HD void a0_item(const vec2<T> *x, vec2<T> *w, int n) {
     }
 }
 
+// A0 item of the strided sub-signal x'[i] = x[i*S] (the multi-pass path's
+// sub-transform of the blocks j >= J0, S = 2^J0)
+template <int LOG2N, typename T>
+QFT_HD void a0_item_s(const vec2<T> *x, long long S, vec2<T> *w, int n) {
+    using P = SPlan<LOG2N>;
+    if (n == 0) {
+        w[padx(P::BASE)] = x[0];
+        w[padx(P::BASE + 1)] = x[(long long)P::m * S];
+    } else {
+        const vec2<T> a = x[(long long)n * S], b = x[(long long)(P::N - n) * S];
+        const int j = ctz32((uint32_t)n);
+        const int cell = P::m - (1 << (LOG2N - 1 - j)) + (n >> (j + 1));
+        w[padx(cell)] = vadd(a, b);
+        w[padx(P::S0 + cell)] = vsub(a, b);
+    }
+}
+
 // A0 by chunks of 64 consecutive n (n = 64c + 2l and 64c + 2l + 1 for lane l):
 // one aligned pair load per side, the odd samples (Lee block 0) go to 32
 // consecutive cells, the even ones to block 1 + ctz(l); lane l's even mirror
@@ -186,8 +203,10 @@ QFT_HD void a0_item_real(const T *xa, const T *xb, vec2<T> *w, int n) {
 // levels, and (after __syncwarp) writes element t of sub-block p to cell 32p + t.
 template <int L, int R, bool DST, typename T>
 struct FBlockP {
-    static constexpr int G = 1 << R;
+    static constexpr int G = 1 << R, NCH = L / 32;
     vec2<T> v[G];
+    // REV: the block's element e is stored at cell L-1-e (a reversed run)
+    template <bool REV = false>
     QFT_HD void load(const vec2<T> *wb, const T *U, int t) {
         const vec2<T> *bf = wb + t;       // forward runs
         const vec2<T> *br = wb + 31 - t;  // reversed runs
@@ -196,7 +215,10 @@ struct FBlockP {
             int c, sg;
             run_of(R, L, s, c, sg);  // compile-time after unrolling
             const int u = c >> 5;    // the run is the 32-aligned chunk u
-            v[s] = sg > 0 ? bf[33 * u] : br[33 * u];
+            if constexpr (REV)       // chunk u is stored as chunk NCH-1-u, direction flipped
+                v[s] = sg > 0 ? br[33 * (NCH - 1 - u)] : bf[33 * (NCH - 1 - u)];
+            else
+                v[s] = sg > 0 ? bf[33 * u] : br[33 * u];
         }
         lee_fwd<R, L, DST, T>(v, t, U);
     }

@@ -12,6 +12,7 @@
 
 #include "../../paper_1301_0763_b200/csrc/qft_smem.cuh"
 #include "../../paper_1301_0763_b200/csrc/qft_large_plan.h"
+#include "../../paper_1301_0763_b200/csrc/qft_leaf.cuh"
 
 using namespace qft;
 
@@ -25,10 +26,10 @@ static void build_U(int N, const T *Tnat, std::vector<T> &U) {
 }
 
 // big warp unit (unit_big in qft_launch.cuh) on the block at padded pointer wb
-template <int L, int R, typename T, bool DST>
+template <int L, int R, typename T, bool DST, bool REV = false>
 static void emu_unit_big(vec2<T> *wb, const T *U) {
     std::vector<FBlockP<L, R, DST, T>> f(32);
-    for (int t = 0; t < 32; ++t) f[t].load(wb, U, t);   // all lanes load ...
+    for (int t = 0; t < 32; ++t) f[t].template load<REV>(wb, U, t);   // all lanes load ...
     for (int t = 0; t < 32; ++t) f[t].store(wb, t);     // ... __syncwarp ... store
     for (int p = 0; p < (1 << R); ++p) b_l32p<DST, T>(wb + 33 * p, U);
     using CB = CBlockP<R, DST, T>;
@@ -193,6 +194,8 @@ static void emu_reg(const vec2<T> *x, vec2<T> *y, const T *U) {
 }
 
 // ---------------------------------------------------------------- large N
+// the multi-pass path of qft_large.cu: F passes (blocks j < J0 above the leaf
+// size), the sub-signal transform of x[k 2^J0], CTA leaves, B passes, chain
 template <int R, typename T>
 static void emu_f_task(vec2<T> *w, const FTask &tk, int dst, const T *U, const vec2<T> *x, int N) {
     for (int t = 0; t < (tk.L >> R); ++t) {
@@ -207,38 +210,54 @@ static void emu_b_task(vec2<T> **W, const BTask &tk) {
         else lg_b_column<R, T, false>(W, tk, i);
     }
 }
-template <int L, typename T>
-static void emu_leaf_thread(vec2<T> *w, const LeafTask &tk, const T *U, const vec2<T> *x, int N) {
-    if (tk.dst) lg_leaf_thread<L, T, true>(w, tk, U, x, N);
-    else lg_leaf_thread<L, T, false>(w, tk, U, x, N);
+template <int A, typename T, bool DST>
+static void emu_leaf_dst(vec2<T> *w, const LeafTask &tk, const T *U, const vec2<T> *x, int N) {
+    using LT = LeafTop<A, DST, T>;
+    constexpr int L = 1 << A;
+    std::vector<vec2<T>> sv(L + L / 32 + 1);
+    vec2<T> *s = sv.data();
+    for (int e = 0; e < L; ++e) s[padx(e)] = tk.j >= 0 ? fold_load<T, DST>(x, N, tk.j, e) : w[tk.c + tk.sg * e];
+    for (int t = 0; t < 1024; ++t) LT::tf(s, U, t);  // groups are disjoint: any order
+    for (int p = 0; p < L / 1024; ++p) {
+        int lo;
+        bool rev;
+        LT::sub(p, lo, rev);
+        if (rev) emu_unit_big<1024, 5, T, DST, true>(s + padx(lo), U);
+        else emu_unit_big<1024, 5, T, DST, false>(s + padx(lo), U);
+    }
+    for (int i = 0; i < 1024; ++i) {  // TB reads shared memory only, writes the run
+        vec2<T> out[LT::G];
+        LT::tb(s, i, out);
+        for (int q = 0; q < LT::G; ++q) w[tk.c + tk.sg * (i * LT::G + q)] = out[q];
+    }
 }
-template <int R, typename T, bool DST>
-static void emu_leaf_warp_dst(vec2<T> *w, const LeafTask &tk, const T *U, const vec2<T> *x, int N) {
-    using WL = WarpLee<R, T, DST>;
-    constexpr int L = WL::L;
-    std::vector<vec2<T>> s(L + L / 32 + 1);
-    for (int e = 0; e < L; ++e)
-        s[e + (e >> 5)] = tk.j >= 0 ? fold_load<T, DST>(x, N, tk.j, e) : w[tk.c + tk.sg * e];
-    std::vector<typename WL::F> f(32);
-    for (int t = 0; t < 32; ++t) f[t].load(s.data(), t, U);
-    for (int t = 0; t < 32; ++t) f[t].store(s.data(), t);
-    for (int p = 0; p < (1 << R); ++p) WL::lee32(s.data(), p, U);
-    std::vector<typename WL::B> bb(32);
-    for (int i = 0; i < 32; ++i) bb[i].compute(s.data(), i);
-    for (int i = 0; i < 32; ++i) bb[i].store(s.data(), i);
-    for (int e = 0; e < L; ++e) w[tk.c + tk.sg * e] = s[e + (e >> 5)];
+template <int A, typename T>
+static void emu_leaf(vec2<T> *w, const LeafTask &tk, const T *U, const vec2<T> *x, int N) {
+    if (tk.dst) emu_leaf_dst<A, T, true>(w, tk, U, x, N);
+    else emu_leaf_dst<A, T, false>(w, tk, U, x, N);
 }
-template <int R, typename T>
-static void emu_leaf_warp(vec2<T> *w, const LeafTask &tk, const T *U, const vec2<T> *x, int N) {
-    if (tk.dst) emu_leaf_warp_dst<R, T, true>(w, tk, U, x, N);
-    else emu_leaf_warp_dst<R, T, false>(w, tk, U, x, N);
+template <int SUBLOG, typename T>
+static void emu_sub(const vec2<T> *x, long long stride, vec2<T> *cb, vec2<T> *sb, const T *U) {
+    using P = SPlan<SUBLOG>;
+    std::vector<vec2<T>> Wv(P::PADDED);
+    vec2<T> *w = Wv.data();
+    for (int n = 0; n < P::m; ++n) a0_item_s<SUBLOG, T>(x, stride, w, n);
+    emu_side<SUBLOG, T, false>(w, U);
+    emu_side<SUBLOG, T, true>(w, U);
+    auto emit = [&](int k, vec2<T> cv, vec2<T> sv) {
+        cb[k] = cv;
+        sb[k] = sv;
+    };
+    for (int t = 0; t < P::DT; ++t) Chain<SUBLOG, T>::unit_e(w, emit, t);
 }
 
-template <typename T, int LEAFLOG, int RG>
+template <typename T, int SUBLOG>
 static int emu_large(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
-    LargeSchedule<LEAFLOG, RG> S(log2n);
-    const int N = S.N;
-    std::vector<vec2<T>> W0(N + 2), W1(N + 2);
+    const int J0 = log2n - SUBLOG, RG = sizeof(T) == 4 ? 5 : 4;
+    LargeSchedule S(log2n, SUBLOG, RG, J0);
+    const int N = S.N, mj0 = 1 << (SUBLOG - 1);
+    const long long Ws = N + 2 + 2 * (mj0 + 1);
+    std::vector<vec2<T>> W0(Ws), W1(Ws);
     vec2<T> *W[2] = {W0.data(), W1.data()};
     for (auto &lvl : S.f)
         for (auto &kv : lvl)
@@ -251,22 +270,15 @@ static int emu_large(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
                     case 5: emu_f_task<5, T>(W[0], td.first, td.second, U, x, N); break;
                 }
             }
-    for (auto &kv : S.leaf)
+    vec2<T> *cb = W[0] + (N + 2), *sb = cb + mj0 + 1;
+    emu_sub<SUBLOG, T>(x, 1ll << J0, cb, sb, U);
+    for (auto &kv : S.leaf) {
+        if (kv.first != SUBLOG && kv.first != SUBLOG - 1) return -2;
         for (auto &tk : kv.second) {
-            switch (kv.first) {
-                case 0: emu_leaf_thread<1, T>(W[0], tk, U, x, N); break;
-                case 1: emu_leaf_thread<2, T>(W[0], tk, U, x, N); break;
-                case 2: emu_leaf_thread<4, T>(W[0], tk, U, x, N); break;
-                case 3: emu_leaf_thread<8, T>(W[0], tk, U, x, N); break;
-                case 4: emu_leaf_thread<16, T>(W[0], tk, U, x, N); break;
-                case 5: emu_leaf_thread<32, T>(W[0], tk, U, x, N); break;
-                case 6: emu_leaf_warp<1, T>(W[0], tk, U, x, N); break;
-                case 7: emu_leaf_warp<2, T>(W[0], tk, U, x, N); break;
-                case 8: emu_leaf_warp<3, T>(W[0], tk, U, x, N); break;
-                case 9: emu_leaf_warp<4, T>(W[0], tk, U, x, N); break;
-                case 10: emu_leaf_warp<5, T>(W[0], tk, U, x, N); break;
-            }
+            if (kv.first == SUBLOG) emu_leaf<SUBLOG, T>(W[0], tk, U, x, N);
+            else emu_leaf<SUBLOG - 1, T>(W[0], tk, U, x, N);
         }
+    }
     for (int d = (int)S.b.size() - 1; d >= 0; --d)
         for (auto &kv : S.b[d])
             for (auto &tk : kv.second) {
@@ -287,8 +299,31 @@ static int emu_large(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
     g.x = x;
     g.cmask = S.cmask;
     g.smask = S.smask;
-    for (int t = 0; t <= (N >> 5); ++t) g.template unit<4>(y, t);
+    g.J0 = J0;
+    g.cb = cb;
+    g.sb = sb;
+    const int RC = J0 < 4 ? J0 : 4;
+    for (int t = 0; t <= (N >> (RC + 1)); ++t) {
+        switch (RC) {
+            case 1: g.template unit<1>(y, t); break;
+            case 2: g.template unit<2>(y, t); break;
+            case 3: g.template unit<3>(y, t); break;
+            case 4: g.template unit<4>(y, t); break;
+        }
+    }
     return 0;
+}
+// sub-signal size of the device plan (qft_large.cu sublog_for)
+template <typename T>
+static int emu_large_any(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
+    const int cap = sizeof(T) == 4 ? 14 : 13;
+    const int sl = log2n - 1 < cap ? log2n - 1 : cap;
+    switch (sl) {
+        case 12: return emu_large<T, 12>(log2n, x, y, U);
+        case 13: return emu_large<T, 13>(log2n, x, y, U);
+        case 14: return emu_large<T, 14>(log2n, x, y, U);
+    }
+    return -1;
 }
 
 template <typename T>
@@ -310,7 +345,7 @@ static int emu_dispatch(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
         case 14: emu_one<14, T>(x, y, U); return 0;
         default:
             if (log2n < 13 || log2n > 20) return -1;
-            return sizeof(T) == 4 ? emu_large<T, 10, 5>(log2n, x, y, U) : emu_large<T, 9, 4>(log2n, x, y, U);
+            return emu_large_any<T>(log2n, x, y, U);
     }
 }
 
@@ -339,7 +374,7 @@ int emu_large_f64(int log2n, const double *x, double *y, long batch, const doubl
     build_U(1 << log2n, Tnat, U);
     for (long b = 0; b < batch; ++b) {
         const long o = 2L * (1L << log2n) * b;
-        int rc = emu_large<double, 9, 4>(log2n, (const vec2<double> *)(x + o), (vec2<double> *)(y + o), U.data());
+        int rc = emu_large_any<double>(log2n, (const vec2<double> *)(x + o), (vec2<double> *)(y + o), U.data());
         if (rc) return rc;
     }
     return 0;
@@ -349,7 +384,7 @@ int emu_large_f32(int log2n, const float *x, float *y, long batch, const float *
     build_U(1 << log2n, Tnat, U);
     for (long b = 0; b < batch; ++b) {
         const long o = 2L * (1L << log2n) * b;
-        int rc = emu_large<float, 10, 5>(log2n, (const vec2<float> *)(x + o), (vec2<float> *)(y + o), U.data());
+        int rc = emu_large_any<float>(log2n, (const vec2<float> *)(x + o), (vec2<float> *)(y + o), U.data());
         if (rc) return rc;
     }
     return 0;

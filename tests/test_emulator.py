@@ -69,7 +69,7 @@ def test_emulated_real_modes_bitwise(emu, oracle_mod, dt, lg, kind):
 
 
 @pytest.mark.parametrize("dt", [np.complex128, np.complex64])
-@pytest.mark.parametrize("lg", [13, 14, 16])
+@pytest.mark.parametrize("lg", [13, 14, 15, 16, 17, 20])
 def test_emulated_multipass_bitwise(emu, oracle_mod, dt, lg):
     """The multi-pass schedule (qft_large_plan.h task lists + qft_large.cuh phases)."""
     N = 1 << lg
