@@ -188,12 +188,12 @@ static bool smem_available(int log2n, int prec) {
 static bool is_large(const qft_plan *p) { return p->multipass; }
 
 static int launch_large(qft_plan *p, const void *in, void *out, long long batch, cudaStream_t st) {
-    // bound the scratch (two buffers per signal) to ~2 GiB: chunk the batch
+    // bound the scratch (two buffers per signal) to ~6 GiB: chunk the batch
     const size_t esz = p->prec == QFT_PREC_F32 ? 8 : 16;
     const long long cells = p->prec == QFT_PREC_F32 ? qft_large_scratch_cells_f32(p->large)
                                                     : qft_large_scratch_cells_f64(p->large);
     const size_t per = 2 * (size_t)cells * esz;
-    long long chunk = (long long)(((size_t)2 << 30) / per);
+    long long chunk = (long long)(((size_t)6 << 30) / per);
     if (chunk < 1) chunk = 1;
     if (chunk > batch) chunk = batch;
     if (p->lscratch_bytes < per * (size_t)chunk) {

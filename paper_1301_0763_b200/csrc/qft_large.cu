@@ -71,7 +71,7 @@ struct QFT_LG(LargePlan) {
     int nitems = 0;
     int launches = 0;
     explicit QFT_LG(LargePlan)(int log2n)
-        : sublog(sublog_for(log2n)), J0(log2n - sublog_for(log2n)), s(log2n, sublog_for(log2n), kRG, J0) {}
+        : sublog(sublog_for(log2n)), J0(log2n - sublog_for(log2n)), s(log2n, sublog_for(log2n), kRG, J0, true) {}
 };
 
 template <typename TT>
@@ -82,6 +82,45 @@ static int upload(const std::vector<TT> &v, void **d) {
 }
 
 // ------------------------------------------------------------------ kernels
+// fold pass: x -> W0 in the Lee-block cell layout (shared.py:28-35; the time-
+// parity routing of improved.py:43, :81).  A CTA folds 2048 consecutive n (and
+// their mirrors N-n), coalesced loads; the stores of one warp land in a few
+// contiguous segments (block j takes every 2^(j+1)-th n).
+constexpr int kFoldN = 2048, kFoldT = 256;
+template <typename T>
+__global__ void __launch_bounds__(kFoldT) lg_fold_kernel(const vec2<T> *__restrict__ x, vec2<T> *__restrict__ W0,
+                                                         int log2n, long long batch, long long Ws) {
+    const int N = 1 << log2n, m = N / 2;
+    const int nch = m / kFoldN;
+    for (long long g = blockIdx.x; g < batch * nch; g += gridDim.x) {
+        const long long b = g / nch;
+        const int a = (int)(g - b * nch) * kFoldN;
+        const vec2<T> *xb = x + b * N;
+        vec2<T> *w = W0 + b * Ws;
+        constexpr int UNR = kFoldN / kFoldT;
+        vec2<T> u[UNR], v[UNR];
+#pragma unroll
+        for (int r = 0; r < UNR; ++r) {
+            const int n = a + r * kFoldT + threadIdx.x;
+            u[r] = xb[n];
+            v[r] = xb[n == 0 ? m : N - n];
+        }
+#pragma unroll
+        for (int r = 0; r < UNR; ++r) {
+            const int n = a + r * kFoldT + threadIdx.x;
+            if (n == 0) {
+                w[N - 1] = u[r];  // s(0) = x[0], s(m) = x[m]
+                w[N] = v[r];
+            } else {
+                const int j = ctz32((uint32_t)n);
+                const int cell = m - (1 << (log2n - 1 - j)) + (n >> (j + 1));
+                w[cell] = vadd(u[r], v[r]);
+                w[m + cell] = vsub(u[r], v[r]);
+            }
+        }
+    }
+}
+
 template <int R, typename T>
 __device__ __forceinline__ void lg_f_dispatch_r(vec2<T> *w, const FTask &tk, int t, bool dst, const T *U,
                                                 const vec2<T> *x, int N) {
@@ -182,17 +221,58 @@ QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const
                        vec2<T> *wb, int N, int tid) {
     constexpr int L = 1 << A;
     const int warp = tid >> 5, lane = tid & 31;
-    // load (fold on load for whole blocks)
-    for (int k = 0; k < K; ++k) {
-        const LeafTask tk = tks[k];
-        vec2<T> *s = S + padx(k * L);
-        if (tk.j >= 0) {
-#pragma unroll 4
-            for (int e = tid; e < L; e += NT)
-                s[padx(e)] = tk.dst ? fold_load<T, true>(xb, N, tk.j, e) : fold_load<T, false>(xb, N, tk.j, e);
-        } else {
-#pragma unroll 8
-            for (int e = tid; e < L; e += NT) s[padx(e)] = wb[tk.c + tk.sg * e];
+    // load (fold on load for whole blocks); UNR loads per thread in flight
+    constexpr int UNR = sizeof(T) == 8 ? 1 : 4;
+    const bool both = K == 2 && tks[0].j >= 0 && tks[0].j == tks[1].j && tks[0].dst != tks[1].dst;
+    if (both) {
+        // the cosine and sine blocks of one j: one gather feeds both folds
+        vec2<T> *sc = S + padx((tks[0].dst ? 1 : 0) * L), *ss = S + padx((tks[0].dst ? 0 : 1) * L);
+        const int j = tks[0].j;
+        for (int e0 = tid; e0 < L; e0 += NT * UNR) {
+            vec2<T> a[UNR], b[UNR];
+#pragma unroll
+            for (int r = 0; r < UNR; ++r) {
+                const int e = e0 + r * NT;
+                if (e < L) {
+                    const int n = (2 * e + 1) << j;
+                    a[r] = xb[n];
+                    b[r] = xb[N - n];
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < UNR; ++r) {
+                const int e = e0 + r * NT;
+                if (e < L) {
+                    sc[padx(e)] = vadd(a[r], b[r]);
+                    ss[padx(e)] = vsub(a[r], b[r]);
+                }
+            }
+        }
+    } else {
+        for (int k = 0; k < K; ++k) {
+            const LeafTask tk = tks[k];
+            vec2<T> *s = S + padx(k * L);
+            for (int e0 = tid; e0 < L; e0 += NT * UNR) {
+                vec2<T> a[UNR], b[UNR];
+#pragma unroll
+                for (int r = 0; r < UNR; ++r) {
+                    const int e = e0 + r * NT;
+                    if (e < L) {
+                        if (tk.j >= 0) {
+                            const int n = (2 * e + 1) << tk.j;
+                            a[r] = xb[n];
+                            b[r] = xb[N - n];
+                        } else {
+                            a[r] = wb[tk.c + tk.sg * e];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < UNR; ++r) {
+                    const int e = e0 + r * NT;
+                    if (e < L) s[padx(e)] = tk.j < 0 ? a[r] : (tk.dst ? vsub(a[r], b[r]) : vadd(a[r], b[r]));
+                }
+            }
         }
     }
     __syncthreads();
@@ -233,20 +313,54 @@ QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const
         if (tk.dst) LeafTop<A, true, T>::tb(s, i, out);
         else LeafTop<A, false, T>::tb(s, i, out);
         vec2<T> *o = wb + tk.c + tk.sg * (i * G);
+        if (sizeof(T) == 4 && ((tk.c & 1) == (tk.sg < 0 ? 1 : 0))) {
+            // 16-byte pairs: (q, q+1) at (o+q, o+q+1) forward, (o-q-1, o-q) reversed
+            float4 *o4 = reinterpret_cast<float4 *>(tk.sg > 0 ? o : o - 1);
 #pragma unroll
-        for (int q = 0; q < G; ++q) o[tk.sg * q] = out[q];
+            for (int q = 0; q < G; q += 2) {
+                const vec2<T> lo = tk.sg > 0 ? out[q] : out[q + 1], hi = tk.sg > 0 ? out[q + 1] : out[q];
+                o4[tk.sg * (q >> 1)] = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < G; ++q) o[tk.sg * q] = out[q];
+        }
     }
 }
 
 template <int SUBLOG, typename T>
-QFT_DEV void sub_item(const vec2<T> *xb, long long stride, vec2<T> *W, const T *U, const T *kcu, vec2<T> *cbuf,
-                      vec2<T> *sbuf, int tid) {
+QFT_DEV void sub_item(const vec2<T> *w0b, int m, vec2<T> *W, const T *U, const T *kcu, vec2<T> *cbuf, vec2<T> *sbuf,
+                      int tid) {
     using P = SPlan<SUBLOG>;
     using C = ItemCfg<SUBLOG, T>;
     constexpr int NT = C::NT, NW = C::NW;
     const int warp = tid >> 5, lane = tid & 31;
-#pragma unroll 4
-    for (int nn = tid; nn < P::m; nn += NT) a0_item_s<SUBLOG, T>(xb, stride, W, nn);
+    // the folded blocks j >= J0 are contiguous in W0: cosine cells [m - m', m-1),
+    // sine cells [N - m', N-1), base pair N-1, N  ->  the sub-signal's layout
+    {
+        constexpr int MP = P::m, UNR = sizeof(T) == 8 ? 2 : 4;
+        const vec2<T> *wc = w0b + (m - MP), *ws = w0b + (2 * m - MP);
+        for (int c0 = tid; c0 < MP - 1; c0 += NT * UNR) {
+            vec2<T> a[UNR], b[UNR];
+#pragma unroll
+            for (int r = 0; r < UNR; ++r) {
+                const int c = c0 + r * NT;
+                if (c < MP - 1) {
+                    a[r] = wc[c];
+                    b[r] = ws[c];
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < UNR; ++r) {
+                const int c = c0 + r * NT;
+                if (c < MP - 1) {
+                    W[padx(c)] = a[r];
+                    W[padx(P::S0 + c)] = b[r];
+                }
+            }
+        }
+        if (tid < 2) W[padx(P::BASE + tid)] = w0b[2 * m - 1 + tid];
+    }
     __syncthreads();
     if constexpr (P::JH > 0) top_f<SUBLOG, T, 0>(W, U, 1, tid);
     fused_units<SUBLOG, T, 0, 1, NW>(W, U, kcu, 1, warp, lane);
@@ -282,7 +396,7 @@ __global__ void __launch_bounds__(ItemCfg<SUBLOG, T>::NT, 1)
         vec2<T> *wb = W0 + b * Ws;
         if (it.kind == 0) {
             vec2<T> *cbuf = wb + (N + 2);
-            sub_item<SUBLOG, T>(xb, 1ll << J0, S, U, kc.u, cbuf, cbuf + SPlan<SUBLOG>::m + 1, tid);
+            sub_item<SUBLOG, T>(wb, N / 2, S, U, kc.u, cbuf, cbuf + SPlan<SUBLOG>::m + 1, tid);
         } else if (it.kind == 1) {
             leaf_item<SUBLOG, T, NT, NW>(tasks + it.k0, 1, S, U, kc.u, xb, wb, N, tid);
         } else {
@@ -384,7 +498,7 @@ int QFT_LG(qft_large_create)(int log2n, void **out) {
         p->nitems = (int)items.size();
         rc |= upload(items, &p->d_items) | upload(leaves, &p->d_leaves);
     }
-    p->launches = 2;
+    p->launches = 3;
     for (auto &v : p->fset) p->launches += (int)v.size();
     for (auto &v : p->bset) p->launches += (int)v.size();
     *out = p;
@@ -433,6 +547,13 @@ int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long ba
     memcpy(kc.u, uhead, sizeof(kc.u));
     const unsigned yb = ybatch(batch);
     cudaError_t e;
+    // fold pass
+    {
+        const long long work = batch * (S.m / kFoldN);
+        const unsigned grid = (unsigned)std::min<long long>(work, 1 << 20);
+        e = launch(lg_fold_kernel<T>, dim3(grid), dim3(kFoldT), 0, st, x, W0, S.n, batch, Ws);
+        if (e) return (int)e;
+    }
     // forward passes: one launch per depth
     for (auto &v : p->fset)
         for (auto &ts : v) {

@@ -57,17 +57,20 @@ struct LargeSchedule {
 
     // jmax > 0: only the blocks j < jmax (the rest belong to the sub-signal
     // transform of x[2^jmax k], see qft_large.cu)
-    LargeSchedule(int log2n, int leaflog, int rg, int jmax = -1)
+    // fold_pass: a separate pass folds x into W0 first (no fold on first touch)
+    LargeSchedule(int log2n, int leaflog, int rg, int jmax = -1, bool fold_pass = false)
         : n(log2n), N(1 << log2n), m(1 << (log2n - 1)), LEAFLOG(leaflog), RG(rg) {
+        fold = fold_pass;
         const int jend = jmax > 0 ? jmax : n - 1;
         for (int side = 0; side < 2; ++side)
             for (int j = 0; j < jend; ++j) {
                 const int L = 1 << (n - 2 - j);
-                Loc l = decompose(side * m + m - 2 * L, 1, L, side, 0, j);  // first touch folds x
+                Loc l = decompose(side * m + m - 2 * L, 1, L, side, 0, fold_pass ? -1 : j);  // first touch folds x
                 if (l.buf) (side ? smask : cmask) |= 1u << j;
             }
     }
-    int passes() const { return 2 + 2 * (int)f.size(); }  // F... (fold on load), leaves, B..., chain
+    bool fold = false;  // a separate fold pass precedes the F passes
+    int passes() const { return (fold ? 3 : 2) + 2 * (int)f.size(); }  // [fold], F..., leaves, B..., chain
 };
 
 }  // namespace qft
