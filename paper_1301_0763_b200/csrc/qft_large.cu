@@ -216,65 +216,54 @@ struct ItemCfg {
     static constexpr int SMEM = U_OFF + UCELLS * (int)sizeof(T);
 };
 
+// async 8/16-byte global -> shared copies (no registers, all in flight at once)
+template <typename T>
+QFT_DEV void cp_async_cell(vec2<T> *dst, const vec2<T> *src) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    if constexpr (sizeof(vec2<T>) == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+QFT_DEV void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// the W0 cells an item reads, as up to 3 runs (lowest cell, count) -- for the
+// L2 prefetch of the next item
+template <int SUBLOG>
+QFT_DEV int item_runs(const Item &it, const LeafTask *tasks, int N, long long *lo, int *cnt) {
+    const int m = N / 2, mp = 1 << (SUBLOG - 1);
+    if (it.kind == 0) {
+        lo[0] = m - mp;
+        cnt[0] = mp;
+        lo[1] = N - mp;
+        cnt[1] = mp + 2;
+        return 2;
+    }
+    const int K = it.kind == 1 ? 1 : 2;
+    for (int k = 0; k < K; ++k) {
+        const LeafTask tk = tasks[it.k0 + k];
+        lo[k] = tk.sg > 0 ? tk.c : tk.c - (tk.L - 1);
+        cnt[k] = tk.L;
+    }
+    return K;
+}
+
+// Leaf item: K leaves of 2^A cells from W0 runs -> their spectra along the runs.
 template <int A, typename T, int NT, int NW>
-QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const T *kcu, const vec2<T> *xb,
-                       vec2<T> *wb, int N, int tid) {
+QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const T *kcu, vec2<T> *wb, int tid) {
     constexpr int L = 1 << A;
     const int warp = tid >> 5, lane = tid & 31;
-    // load (fold on load for whole blocks); UNR loads per thread in flight
-    constexpr int UNR = sizeof(T) == 8 ? 1 : 4;
-    const bool both = K == 2 && tks[0].j >= 0 && tks[0].j == tks[1].j && tks[0].dst != tks[1].dst;
-    if (both) {
-        // the cosine and sine blocks of one j: one gather feeds both folds
-        vec2<T> *sc = S + padx((tks[0].dst ? 1 : 0) * L), *ss = S + padx((tks[0].dst ? 0 : 1) * L);
-        const int j = tks[0].j;
-        for (int e0 = tid; e0 < L; e0 += NT * UNR) {
-            vec2<T> a[UNR], b[UNR];
-#pragma unroll
-            for (int r = 0; r < UNR; ++r) {
-                const int e = e0 + r * NT;
-                if (e < L) {
-                    const int n = (2 * e + 1) << j;
-                    a[r] = xb[n];
-                    b[r] = xb[N - n];
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < UNR; ++r) {
-                const int e = e0 + r * NT;
-                if (e < L) {
-                    sc[padx(e)] = vadd(a[r], b[r]);
-                    ss[padx(e)] = vsub(a[r], b[r]);
-                }
-            }
-        }
-    } else {
-        for (int k = 0; k < K; ++k) {
-            const LeafTask tk = tks[k];
-            vec2<T> *s = S + padx(k * L);
-            for (int e0 = tid; e0 < L; e0 += NT * UNR) {
-                vec2<T> a[UNR], b[UNR];
-#pragma unroll
-                for (int r = 0; r < UNR; ++r) {
-                    const int e = e0 + r * NT;
-                    if (e < L) {
-                        if (tk.j >= 0) {
-                            const int n = (2 * e + 1) << tk.j;
-                            a[r] = xb[n];
-                            b[r] = xb[N - n];
-                        } else {
-                            a[r] = wb[tk.c + tk.sg * e];
-                        }
-                    }
-                }
-#pragma unroll
-                for (int r = 0; r < UNR; ++r) {
-                    const int e = e0 + r * NT;
-                    if (e < L) s[padx(e)] = tk.j < 0 ? a[r] : (tk.dst ? vsub(a[r], b[r]) : vadd(a[r], b[r]));
-                }
-            }
-        }
+    // load: async cell copies along the (forward or reversed) runs
+    for (int k = 0; k < K; ++k) {
+        const LeafTask tk = tks[k];
+        vec2<T> *s = S + padx(k * L);
+        const vec2<T> *src = wb + tk.c;
+        for (int e = tid; e < L; e += NT) cp_async_cell<T>(s + padx(e), src + tk.sg * e);
     }
+    cp_async_wait_all();
     __syncthreads();
     // TF: top fold levels in place
     for (int it = tid; it < K * 1024; it += NT) {
@@ -303,28 +292,40 @@ QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const
         __syncwarp();
     }
     __syncthreads();
-    // TB: block spectrum straight to the leaf's run in W0
-    constexpr int G = LeafTop<A, false, T>::G;
-    for (int it = tid; it < K * 1024; it += NT) {
-        const int k = it >> 10, i = it & 1023;
+    // TB: every column's outputs held in registers across one barrier, then the
+    // natural block spectrum in place, then coalesced stores along the runs
+    constexpr int G = LeafTop<A, false, T>::G, IT = (2 * 1024 + NT - 1) / NT;
+    {
+        vec2<T> out[IT][G];
+#pragma unroll
+        for (int r = 0; r < IT; ++r) {
+            const int it = tid + r * NT;
+            if (it < K * 1024) {
+                const int k = it >> 10, i = it & 1023;
+                const vec2<T> *s = S + padx(k * L);
+                if (tks[k].dst) LeafTop<A, true, T>::tb(s, i, out[r]);
+                else LeafTop<A, false, T>::tb(s, i, out[r]);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < IT; ++r) {
+            const int it = tid + r * NT;
+            if (it < K * 1024) {
+                const int k = it >> 10, i = it & 1023;
+                vec2<T> *o = S + padx(k * L) + padx(i * G);  // G <= 32 slots inside one 32-cell row
+#pragma unroll
+                for (int q = 0; q < G; ++q) o[q] = out[r][q];
+            }
+        }
+    }
+    __syncthreads();
+    for (int k = 0; k < K; ++k) {
         const LeafTask tk = tks[k];
         const vec2<T> *s = S + padx(k * L);
-        vec2<T> out[G];
-        if (tk.dst) LeafTop<A, true, T>::tb(s, i, out);
-        else LeafTop<A, false, T>::tb(s, i, out);
-        vec2<T> *o = wb + tk.c + tk.sg * (i * G);
-        if (sizeof(T) == 4 && ((tk.c & 1) == (tk.sg < 0 ? 1 : 0))) {
-            // 16-byte pairs: (q, q+1) at (o+q, o+q+1) forward, (o-q-1, o-q) reversed
-            float4 *o4 = reinterpret_cast<float4 *>(tk.sg > 0 ? o : o - 1);
-#pragma unroll
-            for (int q = 0; q < G; q += 2) {
-                const vec2<T> lo = tk.sg > 0 ? out[q] : out[q + 1], hi = tk.sg > 0 ? out[q + 1] : out[q];
-                o4[tk.sg * (q >> 1)] = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < G; ++q) o[tk.sg * q] = out[q];
-        }
+        vec2<T> *dst = wb + tk.c;
+#pragma unroll 8
+        for (int e = tid; e < L; e += NT) dst[tk.sg * e] = s[padx(e)];
     }
 }
 
@@ -338,28 +339,14 @@ QFT_DEV void sub_item(const vec2<T> *w0b, int m, vec2<T> *W, const T *U, const T
     // the folded blocks j >= J0 are contiguous in W0: cosine cells [m - m', m-1),
     // sine cells [N - m', N-1), base pair N-1, N  ->  the sub-signal's layout
     {
-        constexpr int MP = P::m, UNR = sizeof(T) == 8 ? 2 : 4;
+        constexpr int MP = P::m;
         const vec2<T> *wc = w0b + (m - MP), *ws = w0b + (2 * m - MP);
-        for (int c0 = tid; c0 < MP - 1; c0 += NT * UNR) {
-            vec2<T> a[UNR], b[UNR];
-#pragma unroll
-            for (int r = 0; r < UNR; ++r) {
-                const int c = c0 + r * NT;
-                if (c < MP - 1) {
-                    a[r] = wc[c];
-                    b[r] = ws[c];
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < UNR; ++r) {
-                const int c = c0 + r * NT;
-                if (c < MP - 1) {
-                    W[padx(c)] = a[r];
-                    W[padx(P::S0 + c)] = b[r];
-                }
-            }
+        for (int c = tid; c < MP - 1; c += NT) {
+            cp_async_cell<T>(W + padx(c), wc + c);
+            cp_async_cell<T>(W + padx(P::S0 + c), ws + c);
         }
-        if (tid < 2) W[padx(P::BASE + tid)] = w0b[2 * m - 1 + tid];
+        if (tid < 2) cp_async_cell<T>(W + padx(P::BASE + tid), w0b + 2 * m - 1 + tid);
+        cp_async_wait_all();
     }
     __syncthreads();
     if constexpr (P::JH > 0) top_f<SUBLOG, T, 0>(W, U, 1, tid);
@@ -376,9 +363,9 @@ QFT_DEV void sub_item(const vec2<T> *w0b, int m, vec2<T> *W, const T *U, const T
 
 template <int SUBLOG, typename T>
 __global__ void __launch_bounds__(ItemCfg<SUBLOG, T>::NT, 1)
-    lg_item_kernel(const vec2<T> *__restrict__ x, vec2<T> *W0, long long Ws, int log2n, int J0,
-                   const Item *__restrict__ items, int ni, const LeafTask *__restrict__ tasks, long long batch,
-                   const T *__restrict__ Ug, const __grid_constant__ LeeConstL<T> kc) {
+    lg_item_kernel(vec2<T> *W0, long long Ws, int log2n, const Item *__restrict__ items, int ni,
+                   const LeafTask *__restrict__ tasks, long long batch, const T *__restrict__ Ug,
+                   const __grid_constant__ LeeConstL<T> kc) {
     using C = ItemCfg<SUBLOG, T>;
     constexpr int NT = C::NT, NW = C::NW;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -392,15 +379,22 @@ __global__ void __launch_bounds__(ItemCfg<SUBLOG, T>::NT, 1)
     for (long long g = blockIdx.x; g < batch * ni; g += gridDim.x) {
         const long long b = g / ni;
         const Item it = items[g - b * ni];
-        const vec2<T> *xb = x + b * N;
         vec2<T> *wb = W0 + b * Ws;
+        // pull the next item's cells into L2 while this one runs
+        if (tid == 0 && g + gridDim.x < batch * ni) {
+            const long long g2 = g + gridDim.x, b2 = g2 / ni;
+            long long lo[3];
+            int cnt[3];
+            const int nr = item_runs<SUBLOG>(items[g2 - b2 * ni], tasks, N, lo, cnt);
+            for (int r = 0; r < nr; ++r) l2_prefetch(W0 + b2 * Ws + lo[r], (uint32_t)(cnt[r] * sizeof(vec2<T>)));
+        }
         if (it.kind == 0) {
             vec2<T> *cbuf = wb + (N + 2);
             sub_item<SUBLOG, T>(wb, N / 2, S, U, kc.u, cbuf, cbuf + SPlan<SUBLOG>::m + 1, tid);
         } else if (it.kind == 1) {
-            leaf_item<SUBLOG, T, NT, NW>(tasks + it.k0, 1, S, U, kc.u, xb, wb, N, tid);
+            leaf_item<SUBLOG, T, NT, NW>(tasks + it.k0, 1, S, U, kc.u, wb, tid);
         } else {
-            leaf_item<SUBLOG - 1, T, NT, NW>(tasks + it.k0, 2, S, U, kc.u, xb, wb, N, tid);
+            leaf_item<SUBLOG - 1, T, NT, NW>(tasks + it.k0, 2, S, U, kc.u, wb, tid);
         }
         __syncthreads();
     }
@@ -576,8 +570,7 @@ int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long ba
         auto run = [&](auto kern, int nt, int smem) -> cudaError_t {
             cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (e2) return e2;
-            return launch(kern, dim3(grid), dim3(nt), (size_t)smem, st, x, W0, Ws, S.n, p->J0, it, p->nitems, lv,
-                          batch, U, kc);
+            return launch(kern, dim3(grid), dim3(nt), (size_t)smem, st, W0, Ws, S.n, it, p->nitems, lv, batch, U, kc);
         };
         switch (p->sublog) {
 #define QFT_IT(SL) \
