@@ -265,36 +265,43 @@ QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const
     }
     cp_async_wait_all();
     __syncthreads();
-    // TF: top fold levels in place
-    for (int it = tid; it < K * 1024; it += NT) {
-        const int k = it >> 10, t = it & 1023;
-        vec2<T> *s = S + padx(k * L);
-        if (tks[k].dst) LeafTop<A, true, T>::tf(s, U, t);
-        else LeafTop<A, false, T>::tf(s, U, t);
+    // TF: top fold levels, held across one barrier, stored sub-block-major
+    constexpr int G = LeafTop<A, false, T>::G, IT = (2 * 1024 + NT - 1) / NT;
+    {
+        vec2<T> v[IT][G];
+#pragma unroll
+        for (int r = 0; r < IT; ++r) {
+            const int it = tid + r * NT;
+            if (it < K * 1024) {
+                const int k = it >> 10, t = it & 1023;
+                const vec2<T> *s = S + padx(k * L);
+                if (tks[k].dst) LeafTop<A, true, T>::tf_load(s, U, t, v[r]);
+                else LeafTop<A, false, T>::tf_load(s, U, t, v[r]);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < IT; ++r) {
+            const int it = tid + r * NT;
+            if (it < K * 1024) {
+                const int k = it >> 10, t = it & 1023;
+                LeafTop<A, false, T>::tf_store(S + padx(k * L), t, v[r]);
+            }
+        }
     }
     __syncthreads();
-    // 1024-cell warp units on the (possibly reversed) sub-block runs
+    // 1024-cell warp units on the sub-blocks
     constexpr int NSUB = L / 1024;
     for (int u = warp; u < K * NSUB; u += NW) {
         const int k = u / NSUB, p = u - k * NSUB;
-        int lo;
-        bool rev;
-        LeafTop<A, false, T>::sub(p, lo, rev);
-        vec2<T> *ws = S + padx(k * L) + padx(lo);
-        const bool dst = tks[k].dst;
-        if (dst) {
-            if (rev) unit_big<1024, 5, T, true, true>(ws, U, kcu, lane);
-            else unit_big<1024, 5, T, true, false>(ws, U, kcu, lane);
-        } else {
-            if (rev) unit_big<1024, 5, T, false, true>(ws, U, kcu, lane);
-            else unit_big<1024, 5, T, false, false>(ws, U, kcu, lane);
-        }
+        vec2<T> *ws = S + padx(k * L + 1024 * p);
+        if (tks[k].dst) unit_big<1024, 5, T, true>(ws, U, kcu, lane);
+        else unit_big<1024, 5, T, false>(ws, U, kcu, lane);
         __syncwarp();
     }
     __syncthreads();
     // TB: every column's outputs held in registers across one barrier, then the
     // natural block spectrum in place, then coalesced stores along the runs
-    constexpr int G = LeafTop<A, false, T>::G, IT = (2 * 1024 + NT - 1) / NT;
     {
         vec2<T> out[IT][G];
 #pragma unroll

@@ -217,14 +217,12 @@ static void emu_leaf_dst(vec2<T> *w, const LeafTask &tk, const T *U, const vec2<
     std::vector<vec2<T>> sv(L + L / 32 + 1);
     vec2<T> *s = sv.data();
     for (int e = 0; e < L; ++e) s[padx(e)] = tk.j >= 0 ? fold_load<T, DST>(x, N, tk.j, e) : w[tk.c + tk.sg * e];
-    for (int t = 0; t < 1024; ++t) LT::tf(s, U, t);  // groups are disjoint: any order
-    for (int p = 0; p < L / 1024; ++p) {
-        int lo;
-        bool rev;
-        LT::sub(p, lo, rev);
-        if (rev) emu_unit_big<1024, 5, T, DST, true>(s + padx(lo), U);
-        else emu_unit_big<1024, 5, T, DST, false>(s + padx(lo), U);
+    {  // TF: every item loads before any store (CTA barrier)
+        std::vector<vec2<T>> v(1024 * LT::G);
+        for (int t = 0; t < 1024; ++t) LT::tf_load(s, U, t, &v[t * LT::G]);
+        for (int t = 0; t < 1024; ++t) LT::tf_store(s, t, &v[t * LT::G]);
     }
+    for (int p = 0; p < L / 1024; ++p) emu_unit_big<1024, 5, T, DST>(s + padx(1024 * p), U);
     for (int i = 0; i < 1024; ++i) {  // TB reads shared memory only, writes the run
         vec2<T> out[LT::G];
         LT::tb(s, i, out);
