@@ -18,6 +18,9 @@
 #ifndef QFT_A0_TMA
 #define QFT_A0_TMA 1       // A0 input: TMA bulk copy into a staging buffer when it fits (1), else L2-prefetched global loads
 #endif
+#ifndef QFT_A0_UNR
+#define QFT_A0_UNR 8       // A0 from global memory: 64-sample chunks in flight per warp (fp32)
+#endif
 #ifndef QFT_TT_MAX
 #define QFT_TT_MAX 4       // cap on signals per CTA iteration
 #endif
@@ -472,7 +475,7 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
         } else if constexpr (TMA) {
             a0_complex<LOG2N, T, 1>(stage, W, ntr, TT, tid, NT, NW, a0l64);
         } else {
-            a0_complex<LOG2N, T, sizeof(T) == 8 ? 1 : 4>(in + bt * TT * P::N, W, ntr, TT, tid, NT, NW, a0l64);
+            a0_complex<LOG2N, T, sizeof(T) == 8 ? 1 : QFT_A0_UNR>(in + bt * TT * P::N, W, ntr, TT, tid, NT, NW, a0l64);
         }
         __syncthreads();
         // the staging buffer is free: prefetch the next batch while we compute
