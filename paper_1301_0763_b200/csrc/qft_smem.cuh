@@ -25,6 +25,9 @@
 #pragma once
 #include "qft_lee.cuh"
 
+#ifndef QFT_RC_SMALL
+#define QFT_RC_SMALL 5  // phase-D unfold depth for N <= 2^12
+#endif
 #ifndef QFT_RC_BIG
 #define QFT_RC_BIG 5  // phase-D unfold depth for N >= 2^13 (257 items at 2^14)
 #endif
@@ -38,7 +41,7 @@ struct SPlan {
     static constexpr int n = LOG2N, N = 1 << LOG2N, m = N / 2, q = N / 4;
     static constexpr int JF = n > 7 ? n - 7 : 0;     // big blocks j < JF (L > 32)
     static constexpr int JS = n - 6;                 // first small block (L = 16)
-    static constexpr int RC0 = n >= 13 ? QFT_RC_BIG : 4;
+    static constexpr int RC0 = n >= 13 ? QFT_RC_BIG : QFT_RC_SMALL;
     static constexpr int RC = n - 2 < RC0 ? n - 2 : RC0;  // chain levels unfolded in phase D
     static constexpr int L(int j) { return 1 << (n - 2 - j); }
     static constexpr int off(int j) { return m - 2 * L(j); }
