@@ -140,7 +140,10 @@ struct qft_plan {
     // scratch for layout conversion / host path
     void *d_scratch = nullptr;
     size_t scratch_bytes = 0;
-    cudaStream_t streams[2] = {nullptr, nullptr};
+    static constexpr int kHostStreams = 3;
+    cudaStream_t streams[kHostStreams] = {nullptr, nullptr, nullptr};
+    void *d_host = nullptr;     // host path staging (per stream: in, out, 2x layout scratch)
+    size_t host_bytes = 0;
     std::mutex mu;
     void *large = nullptr;      // multi-pass schedule
     bool multipass = false;     // served by the multi-pass schedule
@@ -340,6 +343,7 @@ int qft_plan_destroy(qft_plan *p) {
     if (p->d_lscratch) cudaFree(p->d_lscratch);
     if (p->d_T) cudaFree(p->d_T);
     if (p->d_arena) cudaFree(p->d_arena);
+    if (p->d_host) cudaFree(p->d_host);
     if (p->large) {
         if (p->prec == QFT_PREC_F32) qft_large_destroy_f32(p->large);
         else qft_large_destroy_f64(p->large);
@@ -533,48 +537,79 @@ int qft_exec_cdft_host(qft_plan *p, const void *h_in, void *h_out, int64_t batch
         return fail(QFT_EINVAL, "host path supports batch-major or (N, batch) layouts only");
     for (auto &s : p->streams)
         if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    // chunk the batch so copies of one chunk overlap the transform of the other
-    const size_t target = (size_t)64 << 20;  // bytes per chunk
+    // chunk the batch over kHostStreams streams: the H2D copy, transform and D2H
+    // copy of different chunks overlap (both copy directions run concurrently)
+    constexpr int NS = qft_plan::kHostStreams;
+    const size_t target = (size_t)32 << 20;  // bytes per chunk
     long long chunk = (long long)(target / ((size_t)N * esz));
     if (chunk < 1) chunk = 1;
     if (chunk > batch) chunk = batch;
     const size_t cbytes = (size_t)chunk * N * esz;
-    // per stream: in buffer, out buffer, (transpose scratch is inside exec_impl's scratch -> use own)
-    void *bufs = nullptr;
-    CUDA_TRY(cudaMalloc(&bufs, cbytes * 8));  // per stream: in, out, 2x layout scratch
+    // per stream: in, out, 2x layout scratch; kept in the plan across calls
+    if (p->host_bytes < cbytes * 4 * NS) {
+        if (p->d_host) cudaFree(p->d_host);
+        p->d_host = nullptr;
+        p->host_bytes = 0;
+        CUDA_TRY(cudaMalloc(&p->d_host, cbytes * 4 * NS));
+        p->host_bytes = cbytes * 4 * NS;
+    }
+    void *bufs = p->d_host;
+    // three streams: H2D copies, transforms (serialised: the plan's scratch is
+    // shared), D2H copies; chunk k uses buffer slot k % NS, events chain the stages
+    cudaStream_t sin = p->streams[0], scomp = p->streams[1], sout = p->streams[2];
+    cudaEvent_t ev_in[NS], ev_out[NS], ev_free[NS];
+    for (int i = 0; i < NS; ++i) {
+        CUDA_TRY(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming));
+    }
     int rc = 0;
     for (long long b0 = 0, it = 0; b0 < batch && !rc; b0 += chunk, ++it) {
         const long long nb = (batch - b0) < chunk ? (batch - b0) : chunk;
-        cudaStream_t st = p->streams[it & 1];
-        char *din = (char *)bufs + (it & 1) * 4 * cbytes, *dout = din + cbytes, *dscr = din + 2 * cbytes;
-        cudaError_t e;
-        if (batch_major_in)
-            e = cudaMemcpyAsync(din, (const char *)h_in + (size_t)b0 * N * esz, (size_t)nb * N * esz,
-                                cudaMemcpyHostToDevice, st);
-        else  // columns [b0, b0+nb) of the (N, batch) array -> (N, nb) pitched
-            e = cudaMemcpy2DAsync(din, (size_t)nb * esz, (const char *)h_in + (size_t)b0 * esz, (size_t)batch * esz,
-                                  (size_t)nb * esz, (size_t)N, cudaMemcpyHostToDevice, st);
+        const int slot = (int)(it % NS);
+        char *din = (char *)bufs + slot * 4 * cbytes, *dout = din + cbytes, *dscr = din + 2 * cbytes;
+        cudaError_t e = cudaSuccess;
+        if (it >= NS) e = cudaStreamWaitEvent(sin, ev_free[slot], 0);  // slot's previous D2H done
+        if (e == cudaSuccess) {
+            if (batch_major_in)
+                e = cudaMemcpyAsync(din, (const char *)h_in + (size_t)b0 * N * esz, (size_t)nb * N * esz,
+                                    cudaMemcpyHostToDevice, sin);
+            else  // columns [b0, b0+nb) of the (N, batch) array -> (N, nb) pitched
+                e = cudaMemcpy2DAsync(din, (size_t)nb * esz, (const char *)h_in + (size_t)b0 * esz,
+                                      (size_t)batch * esz, (size_t)nb * esz, (size_t)N, cudaMemcpyHostToDevice, sin);
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(ev_in[slot], sin);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(scomp, ev_in[slot], 0);
         if (e != cudaSuccess) {
             rc = fail(QFT_ECUDA, std::string("H2D: ") + cudaGetErrorString(e));
             break;
         }
         // device layout of the chunk: batch-major (nb, N) or (N, nb)
         rc = exec_impl(p, din, dout, nb, batch_major_in ? N : 1, batch_major_in ? 1 : nb, batch_major_out ? N : 1,
-                       batch_major_out ? 1 : nb, st, dscr);
+                       batch_major_out ? 1 : nb, scomp, dscr);
         if (rc) break;
-        if (batch_major_out)
-            e = cudaMemcpyAsync((char *)h_out + (size_t)b0 * N * esz, dout, (size_t)nb * N * esz,
-                                cudaMemcpyDeviceToHost, st);
-        else
-            e = cudaMemcpy2DAsync((char *)h_out + (size_t)b0 * esz, (size_t)batch * esz, dout, (size_t)nb * esz,
-                                  (size_t)nb * esz, (size_t)N, cudaMemcpyDeviceToHost, st);
+        e = cudaEventRecord(ev_out[slot], scomp);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, ev_out[slot], 0);
+        if (e == cudaSuccess) {
+            if (batch_major_out)
+                e = cudaMemcpyAsync((char *)h_out + (size_t)b0 * N * esz, dout, (size_t)nb * N * esz,
+                                    cudaMemcpyDeviceToHost, sout);
+            else
+                e = cudaMemcpy2DAsync((char *)h_out + (size_t)b0 * esz, (size_t)batch * esz, dout, (size_t)nb * esz,
+                                      (size_t)nb * esz, (size_t)N, cudaMemcpyDeviceToHost, sout);
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(ev_free[slot], sout);
         if (e != cudaSuccess) rc = fail(QFT_ECUDA, std::string("D2H: ") + cudaGetErrorString(e));
     }
-    for (auto &s : p->streams) {
-        cudaError_t e = cudaStreamSynchronize(s);
+    for (auto &st : p->streams) {
+        cudaError_t e = cudaStreamSynchronize(st);
         if (e != cudaSuccess && !rc) rc = fail(QFT_ECUDA, std::string("sync: ") + cudaGetErrorString(e));
     }
-    cudaFree(bufs);
+    for (int i = 0; i < NS; ++i) {
+        cudaEventDestroy(ev_in[i]);
+        cudaEventDestroy(ev_out[i]);
+        cudaEventDestroy(ev_free[i]);
+    }
     return rc;
 }
 
