@@ -295,7 +295,7 @@ def main():
             el = float(t.item())
         e2e = {"value": ws * hb / el, "unit": UNIT, "h2d_bytes_per_step": hb * N * esz,
                "d2h_bytes_per_step": hb * N * esz, "ms_per_step": el * 1000.0, "batch_per_step": hb,
-               "path": "qft_exec_cdft_host (pinned host buffers, 2-stream chunked pipeline)"}
+               "path": "qft_exec_cdft_host (pinned host buffers; H2D, transform, D2H on three event-chained streams)"}
 
     # parity spot check of this run's own data (sampled rows vs the oracle)
     parity = None
