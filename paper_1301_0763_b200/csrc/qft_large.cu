@@ -87,11 +87,13 @@ static int upload(const std::vector<TT> &v, void **d) {
 // their mirrors N-n), coalesced loads; the stores of one warp land in a few
 // contiguous segments (block j takes every 2^(j+1)-th n).
 constexpr int kFoldN = 2048, kFoldT = 256;
+// samples n = n' << sh for n' in [0, m >> sh): the blocks j >= sh (the blocks
+// j < sh are folded on first touch by the F passes)
 template <typename T>
 __global__ void __launch_bounds__(kFoldT) lg_fold_kernel(const vec2<T> *__restrict__ x, vec2<T> *__restrict__ W0,
-                                                         int log2n, long long batch, long long Ws) {
-    const int N = 1 << log2n, m = N / 2;
-    const int nch = m / kFoldN;
+                                                         int log2n, int sh, long long batch, long long Ws) {
+    const int N = 1 << log2n, m = N / 2, cnt = m >> sh;
+    const int nch = (cnt + kFoldN - 1) / kFoldN;
     for (long long g = blockIdx.x; g < batch * nch; g += gridDim.x) {
         const long long b = g / nch;
         const int a = (int)(g - b * nch) * kFoldN;
@@ -101,13 +103,16 @@ __global__ void __launch_bounds__(kFoldT) lg_fold_kernel(const vec2<T> *__restri
         vec2<T> u[UNR], v[UNR];
 #pragma unroll
         for (int r = 0; r < UNR; ++r) {
-            const int n = a + r * kFoldT + threadIdx.x;
-            u[r] = xb[n];
-            v[r] = xb[n == 0 ? m : N - n];
+            const int n = (a + r * kFoldT + (int)threadIdx.x) << sh;
+            if (n < m) {
+                u[r] = xb[n];
+                v[r] = xb[n == 0 ? m : N - n];
+            }
         }
 #pragma unroll
         for (int r = 0; r < UNR; ++r) {
-            const int n = a + r * kFoldT + threadIdx.x;
+            const int n = (a + r * kFoldT + (int)threadIdx.x) << sh;
+            if (n >= m) continue;
             if (n == 0) {
                 w[N - 1] = u[r];  // s(0) = x[0], s(m) = x[m]
                 w[N] = v[r];
@@ -550,9 +555,9 @@ int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long ba
     cudaError_t e;
     // fold pass
     {
-        const long long work = batch * (S.m / kFoldN);
+        const long long work = batch * (((S.m >> S.jfold) + kFoldN - 1) / kFoldN);
         const unsigned grid = (unsigned)std::min<long long>(work, 1 << 20);
-        e = launch(lg_fold_kernel<T>, dim3(grid), dim3(kFoldT), 0, st, x, W0, S.n, batch, Ws);
+        e = launch(lg_fold_kernel<T>, dim3(grid), dim3(kFoldT), 0, st, x, W0, S.n, S.jfold, batch, Ws);
         if (e) return (int)e;
     }
     // forward passes: one launch per depth

@@ -62,14 +62,19 @@ struct LargeSchedule {
         : n(log2n), N(1 << log2n), m(1 << (log2n - 1)), LEAFLOG(leaflog), RG(rg) {
         fold = fold_pass;
         const int jend = jmax > 0 ? jmax : n - 1;
+        // blocks j < jfold are cut by F passes whose first touch folds x; with a
+        // fold pass, it folds only the samples of blocks j >= jfold
+        jfold = 0;
+        while (jfold < jend && (1 << (n - 2 - jfold)) > (1 << LEAFLOG)) ++jfold;
         for (int side = 0; side < 2; ++side)
             for (int j = 0; j < jend; ++j) {
                 const int L = 1 << (n - 2 - j);
-                Loc l = decompose(side * m + m - 2 * L, 1, L, side, 0, fold_pass ? -1 : j);  // first touch folds x
+                Loc l = decompose(side * m + m - 2 * L, 1, L, side, 0, (fold_pass && j >= jfold) ? -1 : j);
                 if (l.buf) (side ? smask : cmask) |= 1u << j;
             }
     }
     bool fold = false;  // a separate fold pass precedes the F passes
+    int jfold = 0;      // the fold pass covers the samples n with ctz(n) >= jfold (and n = 0)
     int passes() const { return (fold ? 3 : 2) + 2 * (int)f.size(); }  // [fold], F..., leaves, B..., chain
 };
 

@@ -263,7 +263,7 @@ static int emu_large(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
     const long long Ws = N + 2 + 2 * (mj0 + 1);
     std::vector<vec2<T>> W0(Ws), W1(Ws);
     vec2<T> *W[2] = {W0.data(), W1.data()};
-    for (int n = 0; n < N / 2; ++n) lg_fold_item<T>(x, W[0], n, N, log2n);  // fold pass
+    for (int n = 0; n < N / 2; n += 1 << S.jfold) lg_fold_item<T>(x, W[0], n, N, log2n);  // fold pass (blocks j >= jfold)
     for (auto &lvl : S.f)
         for (auto &kv : lvl)
             for (auto &td : kv.second) {

@@ -106,7 +106,7 @@ def test_host_path_multi_chunk(torch_cuda, oracle_mod, lg, dt, B):
     z = (rng.standard_normal((B, N)) + 1j * rng.standard_normal((B, N))).astype(dt)
     zp = torch.from_numpy(z).pin_memory()
     out = torch.empty_like(zp).pin_memory()
-    p = _native.plan(lg, prec)
+    p = _native.Plan(lg, prec)  # uncached: default constants whatever other tests uploaded
     p.exec_host(zp.data_ptr(), out.data_ptr(), B, (N, 1), (N, 1))
     dev = torch.empty_like(zp, device="cuda")
     x = zp.cuda()
