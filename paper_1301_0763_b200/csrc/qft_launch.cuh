@@ -21,6 +21,9 @@
 #ifndef QFT_A0_UNR
 #define QFT_A0_UNR 8       // A0 from global memory: 64-sample chunks in flight per warp (fp32)
 #endif
+#ifndef QFT_NW_MIN
+#define QFT_NW_MIN 4       // lower bound on warps per CTA
+#endif
 #ifndef QFT_TT_MAX
 #define QFT_TT_MAX 4       // cap on signals per CTA iteration
 #endif
@@ -100,7 +103,8 @@ struct KCfg {
     // warps are spread over 4 SM sub-partitions of 16K registers each: 12 warps
     // keep 168 registers (fp64), 16 keep 128; 17 (fp32, N <= 4096) drop to 96
     static constexpr int NWMAX = sizeof(T) == 8 ? 12 : (P::n >= 13 ? 16 : 17);
-    static constexpr int NW = NW0 < 4 ? 4 : (NW0 > NWMAX ? NWMAX : NW0);
+    static constexpr int NWLO = QFT_NW_MIN > NWMAX ? NWMAX : QFT_NW_MIN;
+    static constexpr int NW = NW0 < NWLO ? NWLO : (NW0 > NWMAX ? NWMAX : NW0);
     static constexpr int NT = NW * 32;
     static constexpr int STAGE_OFF = 0;
     static constexpr int W_OFF = TMA ? TT * P::N * VB : 0;
