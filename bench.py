@@ -318,6 +318,7 @@ def main():
             cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "port",
                    "sample": f"{done} transforms of config {args.config} shape (N=2^{LOG2N}) in {el:.1f}s, 1 thread"}
         info = plan.info()
+        tr = read_traffic(args.config)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
@@ -330,9 +331,12 @@ def main():
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
-                         "traffic": (lambda d: None if not d or B != BATCH else
-                                     d["traffic_bytes_per_launch"] / (ms / 1000.0) / 1e9)(read_traffic(args.config)),
-                         "traffic_unit": "GB/s of measured DRAM bytes (ncu, committed under profiles/) at this launch time",
+                         "traffic": (lambda d: None if not d or B != BATCH else d["traffic_bytes_per_launch"])(tr),
+                         "traffic_unit": "bytes per step: ncu dram__bytes_read.sum + dram__bytes_write.sum of the "
+                                         "step's kernels (profiles/r1_summary.json); algorithmic bytes per step = "
+                                         f"{2 * esz * N * B}",
+                         "dominant_kernel": tr.get("dominant_kernel") if tr else None,
+                         "dominant_share_of_step": tr.get("dominant_share_of_step") if tr else None,
                          "algorithmic_bytes_per_transform": 2 * esz * N, "passes": info.passes},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
