@@ -1,20 +1,20 @@
-// qft_large.cuh -- multi-pass improved-QFT for N = 2^13 .. 2^20 (fp32 / fp64).
+// qft_large.cuh -- device phases of the multi-pass path (N > 2^14 fp32 / 2^13 fp64).
 //
-// A signal is too large for one CTA, so the Lee blocks of the time-parity
-// chain are decomposed across passes over HBM (one scratch layout per signal,
-// two scratch buffers W0/W1 of N+1 cells, the same cell map as qft_smem.cuh
-// without padding):
+// Signals larger than one SM's shared memory are cut along the improved
+// recursion itself (qft_large.cu): the Lee blocks j >= J0 are the blocks of the
+// sub-signal transform of x[k 2^J0] (single-pass machinery, qft_launch.cuh),
+// blocks of 2^SUBLOG cells or less are CTA-resident leaves (qft_leaf.cuh), and
+// only blocks larger than that are cut in HBM by the passes here:
 //   fold   x -> W0: x[n] +- x[N-n] routed to Lee block j = ctz(n) (shared.py:28-35)
-//   F(d)   in-place forward fold levels (r <= 5 per pass) of every Lee block
-//          larger than the leaf size; each pass leaves 2^r sub-blocks as
-//          contiguous (possibly reversed) runs of the same cells
-//   leaf   every block / sub-block of size <= LEAF: full Lee DCT-II/DST-II,
-//          one warp (shared memory, F/Lee-32/B with __syncwarp) or one thread
+//   F(d)   in-place forward fold levels (r <= 5 fp32 / 4 fp64 per pass) of every
+//          block larger than the leaf size; the first touch folds x on load;
+//          each pass leaves 2^r sub-blocks as contiguous (possibly reversed)
+//          runs of the same cells
 //   B(d)   backward levels (neighbour sums + interleave), deepest first,
 //          ping-pong W0 <-> W1, output in natural spectrum order
-//   chain  time-split chain + complex recombination -> y (elaborations.py:329-340,
-//          shared.py:58-72); each thread descends the chain from the DCT base
-// The host plan builder (qft_large_plan.cu) compiles the decomposition tree of
+//   chain  time-split chain levels J0-1 .. 0 + complex recombination -> y
+//          (elaborations.py:329-340, shared.py:58-72)
+// The host plan builder (qft_large_plan.h) compiles the decomposition tree of
 // the reference recursion into these task lists.
 #pragma once
 #include "qft_lee.cuh"
@@ -28,7 +28,7 @@ struct FTask {        // r forward levels of one run (in place)
 };
 struct LeafTask {     // full Lee of one run (in place, spectrum along the run)
     int c, sg, L, dst;
-    int j;            // >= 0: all of Lee block j -> fold x on load
+    int j;            // >= 0: all of Lee block j, folded on first touch (-1: a run already in W0)
 };
 
 // element i of Lee block j read straight from the input: sample n = 2^j (2i+1),
@@ -148,69 +148,6 @@ QFT_HD void lg_b_column(vec2<T> *const *W, const BTask &tk, int i) {
 #pragma unroll
     for (int s = 0; s < G; ++s) dst[s] = out[s];
 }
-
-// ----------------------------------------------------------------- leaf (thread)
-template <int L, typename T, bool DST>
-QFT_HD void lg_leaf_thread(vec2<T> *w, const LeafTask &tk, const T *U, const vec2<T> *x = nullptr, int N = 0) {
-    vec2<T> v[L];
-#pragma unroll
-    for (int e = 0; e < L; ++e) v[e] = tk.j >= 0 ? fold_load<T, DST>(x, N, tk.j, e) : w[tk.c + tk.sg * e];
-    lee_full<L, DST, T>(v, U);
-#pragma unroll
-    for (int e = 0; e < L; ++e) w[tk.c + tk.sg * e] = v[e];
-}
-
-// ----------------------------------------------------------------- leaf (warp)
-// Lee block of L = 32 << R cells staged in a padded shared buffer s (natural
-// element order); three lane phases separated by __syncwarp, as in qft_smem.cuh.
-template <int R, typename T, bool DST>
-struct WarpLee {
-    static constexpr int G = 1 << R, L = 32 << R;
-    QFT_HD static int px(int p) { return p + (p >> 5); }
-    // phase 1 (lane t): reflection group -> sub-block-major (element t of sub-block p at 32p + t)
-    struct F {
-        vec2<T> v[G];
-        QFT_HD void load(const vec2<T> *s, int t, const T *U) {
-#pragma unroll
-            for (int q = 0; q < G; ++q) {
-                int c, sg;
-                run_of(R, L, q, c, sg);
-                v[q] = s[px(c + sg * t)];
-            }
-            lee_fwd<R, L, DST, T>(v, t, U);
-        }
-        QFT_HD void store(vec2<T> *s, int t) const {
-#pragma unroll
-            for (int p = 0; p < G; ++p) s[px(32 * p + t)] = v[p];
-        }
-    };
-    // phase 2 (lane p < G): Lee-32 of sub-block p
-    QFT_HD static void lee32(vec2<T> *s, int p, const T *U) {
-        vec2<T> v[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = s[px(32 * p + e)];
-        lee_full<32, DST, T>(v, U);
-#pragma unroll
-        for (int e = 0; e < 32; ++e) s[px(32 * p + e)] = v[e];
-    }
-    // phase 3 (lane i): column i -> block spectrum slots [iG, iG + G)
-    struct B {
-        vec2<T> out[G];
-        QFT_HD void compute(const vec2<T> *s, int i) {
-            vec2<T> own[G];
-            const int ih = DST ? (i > 0 ? i - 1 : i) : (i < 31 ? i + 1 : i);
-#pragma unroll
-            for (int p = 0; p < G; ++p) own[p] = s[px(32 * p + i)];
-            auto halo = [&](int p) { return s[px(32 * p + ih)]; };
-            const bool edge = DST ? (i == 0) : (i == 31);
-            lee_bwd_fn<R, DST, T>(own, 0, halo, edge, out);
-        }
-        QFT_HD void store(vec2<T> *s, int i) const {
-#pragma unroll
-            for (int q = 0; q < G; ++q) s[px(i * G + q)] = out[q];
-        }
-    };
-};
 
 // ----------------------------------------------------------------- chain
 // Each thread t in [0, m_RC] (m_RC = N >> (RC+1)) descends the chain from the

@@ -110,23 +110,6 @@ QFT_HD void a0_item(const vec2<T> *x, vec2<T> *w, int n) {
     }
 }
 
-// A0 item of the strided sub-signal x'[i] = x[i*S] (the multi-pass path's
-// sub-transform of the blocks j >= J0, S = 2^J0)
-template <int LOG2N, typename T>
-QFT_HD void a0_item_s(const vec2<T> *x, long long S, vec2<T> *w, int n) {
-    using P = SPlan<LOG2N>;
-    if (n == 0) {
-        w[padx(P::BASE)] = x[0];
-        w[padx(P::BASE + 1)] = x[(long long)P::m * S];
-    } else {
-        const vec2<T> a = x[(long long)n * S], b = x[(long long)(P::N - n) * S];
-        const int j = ctz32((uint32_t)n);
-        const int cell = P::m - (1 << (LOG2N - 1 - j)) + (n >> (j + 1));
-        w[padx(cell)] = vadd(a, b);
-        w[padx(P::S0 + cell)] = vsub(a, b);
-    }
-}
-
 // A0 by chunks of 64 consecutive n (n = 64c + 2l and 64c + 2l + 1 for lane l):
 // one aligned pair load per side, the odd samples (Lee block 0) go to 32
 // consecutive cells, the even ones to block 1 + ctz(l); lane l's even mirror
