@@ -21,6 +21,9 @@
 #ifndef QFT_A0_UNR
 #define QFT_A0_UNR 8       // A0 from global memory: 64-sample chunks in flight per warp (fp32)
 #endif
+#ifndef QFT_MIXED_STAGE
+#define QFT_MIXED_STAGE 0  // see KCfg::MIXED
+#endif
 #ifndef QFT_NW_MIN
 #define QFT_NW_MIN 4       // lower bound on warps per CTA
 #endif
@@ -92,8 +95,15 @@ struct KCfg {
     // stage through TMA when the staging buffer still leaves room for 2 signals
     // (fp32) / 1 signal (fp64, whose global A0 path spills)
     static constexpr int TMA_MIN = sizeof(T) == 8 ? 1 : (TTC < 2 ? TTC : 2);
-    static constexpr bool TMA = QFT_A0_TMA && BUDGET / PER_S >= TMA_MIN;
-    static constexpr int TT = clampt(BUDGET / (TMA ? PER_S : PER_W));  // signals per CTA iteration
+    static constexpr bool TMA0 = QFT_A0_TMA && BUDGET / PER_S >= TMA_MIN;
+    // mixed staging (QFT_MIXED_STAGE, fp32 N = 4096): more signals per iteration
+    // than fit with staging; TS of them are TMA-staged, the rest are read from
+    // L2-prefetched global memory
+    static constexpr bool MIXED = QFT_MIXED_STAGE && sizeof(T) == 4 && P::n == 12;
+    static constexpr int TT = MIXED ? clampt(BUDGET / PER_W) : clampt(BUDGET / (TMA0 ? PER_S : PER_W));
+    static constexpr int TS0 = MIXED ? (BUDGET - TT * PER_W) / (P::N * VB) : (TMA0 ? TT : 0);
+    static constexpr int TS = TS0 > TT ? TT : TS0;  // TMA-staged signals per iteration
+    static constexpr bool TMA = TS > 0;
     static_assert(TT * PER_W <= BUDGET, "working area exceeds shared memory");
     static constexpr int mx(int a, int b) { return a > b ? a : b; }
     static constexpr int NU = 2 * (P::NU1 + 1);  // fused warp units per signal
@@ -107,7 +117,7 @@ struct KCfg {
     static constexpr int NW = NW0 < NWLO ? NWLO : (NW0 > NWMAX ? NWMAX : NW0);
     static constexpr int NT = NW * 32;
     static constexpr int STAGE_OFF = 0;
-    static constexpr int W_OFF = TMA ? TT * P::N * VB : 0;
+    static constexpr int W_OFF = TS * P::N * VB;
     static constexpr int U_OFF = W_OFF + TT * PER_W;
     static constexpr int BAR_OFF = (U_OFF + UB + 15) / 16 * 16;
     static constexpr int SMEM = BAR_OFF + 16;
@@ -448,23 +458,26 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
     if (TMA && tid == 0) mbar_init(bar, 1);
     __syncthreads();
     long long bt = blockIdx.x;
-    if (TMA && tid == 0 && bt < nbatch) {
-        const long long nt = (batch - bt * TT) < TT ? (batch - bt * TT) : TT;
-        tma_bulk_load(stage, in + bt * TT * P::N, (uint32_t)(nt * P::N * K::VB), bar);
-    }
+    constexpr int TS = K::TS;
+    // TMA part of batch b: its first min(TS, count) signals
+    auto stage_count = [&](long long b) -> long long {
+        const long long nt = (batch - b * TT) < TT ? (batch - b * TT) : TT;
+        return nt < TS ? nt : TS;
+    };
+    if (TMA && tid == 0 && bt < nbatch)
+        tma_bulk_load(stage, in + bt * TT * P::N, (uint32_t)(stage_count(bt) * P::N * K::VB), bar);
     uint32_t parity = 0;
     for (; bt < nbatch; bt += gridDim.x) {
         const int ntr = (int)((batch - bt * TT) < TT ? (batch - bt * TT) : TT);
         if constexpr (TMA) {
             mbar_wait(bar, parity);
             parity ^= 1u;
-        } else if (tid == 0 && bt + gridDim.x < nbatch) {
-            // pull the next batch into L2 while this one is transformed
+        }
+        if (MODE == 0 && TS < TT && tid == 0 && bt + gridDim.x < nbatch) {
+            // pull the next batch's unstaged signals into L2 while this one is transformed
             const long long nb = bt + gridDim.x;
-            if constexpr (MODE == 0) {
-                const long long nt = (batch - nb * TT) < TT ? (batch - nb * TT) : TT;
-                l2_prefetch(in + nb * TT * P::N, (uint32_t)(nt * P::N * K::VB));
-            }
+            const long long nt = (batch - nb * TT) < TT ? (batch - nb * TT) : TT;
+            if (nt > TS) l2_prefetch(in + (nb * TT + TS) * P::N, (uint32_t)((nt - TS) * P::N * K::VB));
         }
         // A0: fold + route -> W
         if constexpr (MODE != 0) {
@@ -476,17 +489,20 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
                 for (int nn = tid; nn <= P::m; nn += NT)
                     a0_item_real<LOG2N, T, MODE>(xr + ra * RL, xr + rb * RL, W + tau * P::PADDED, nn);
             }
-        } else if constexpr (TMA) {
-            a0_complex<LOG2N, T, 1>(stage, W, ntr, TT, tid, NT, NW, a0l64);
         } else {
-            a0_complex<LOG2N, T, sizeof(T) == 8 ? 1 : QFT_A0_UNR>(in + bt * TT * P::N, W, ntr, TT, tid, NT, NW, a0l64);
+            if constexpr (TS < TT) {
+                if (ntr > TS)
+                    a0_complex<LOG2N, T, sizeof(T) == 8 ? 1 : QFT_A0_UNR>(in + (bt * TT + TS) * P::N,
+                                                                          W + TS * P::PADDED, ntr - TS, TT - TS, tid,
+                                                                          NT, NW, a0l64);
+            }
+            if constexpr (TS > 0) a0_complex<LOG2N, T, 1>(stage, W, ntr < TS ? ntr : TS, TS, tid, NT, NW, a0l64);
         }
         __syncthreads();
         // the staging buffer is free: prefetch the next batch while we compute
         if (TMA && tid == 0 && bt + gridDim.x < nbatch) {
             const long long nb = bt + gridDim.x;
-            const long long nt = (batch - nb * TT) < TT ? (batch - nb * TT) : TT;
-            tma_bulk_load(stage, in + nb * TT * P::N, (uint32_t)(nt * P::N * K::VB), bar);
+            tma_bulk_load(stage, in + nb * TT * P::N, (uint32_t)(stage_count(nb) * P::N * K::VB), bar);
         }
         // TF: top forward levels of the huge blocks (N > 4096; ends with a barrier)
         if constexpr (P::JH > 0) top_f<LOG2N, T, MODE>(W, U, ntr, tid);
