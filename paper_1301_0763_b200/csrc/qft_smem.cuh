@@ -136,6 +136,11 @@ struct A0Chunk64 {
         ld2(x + 64 * c + 2 * l, xe, xo);                          // x[n_e], x[n_o]
         ld2(x + (1 << LOG2N) - 64 * c - 2 * l - 2, mn, mo);       // x[N - n_e - 2], x[N - n_o]
     }
+    // xf: the forward samples x[0..), xm: one past the mirror end (x + N)
+    QFT_HD void loadp(const vec2<T> *xf, const vec2<T> *xm, int c, int l) {
+        ld2(xf + 64 * c + 2 * l, xe, xo);
+        ld2(xm - 64 * c - 2 * l - 2, mn, mo);
+    }
     template <int LOG2N, class ShflUp>
     QFT_HD void store(vec2<T> *w, int c, int l, const A0Lane64 &a, ShflUp &&shfl_up) const {
         constexpr int PS = padx(SPlan<LOG2N>::S0);
