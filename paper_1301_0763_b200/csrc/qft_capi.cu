@@ -146,6 +146,7 @@ struct qft_plan {
     size_t host_bytes = 0;
     std::mutex mu;
     void *large = nullptr;      // multi-pass schedule
+    void *large_real = nullptr; // its real-mode variant (fold pass over every block), built on first use
     bool multipass = false;     // served by the multi-pass schedule
     void *d_T = nullptr;        // natural table T[0..N/4) on the device (classical recursion)
     void *d_arena = nullptr;    // classical: per-warp scratch
@@ -190,11 +191,22 @@ static bool smem_available(int log2n, int prec) {
 // by QFT_MULTIPASS=1 at plan creation (A/B comparisons and tests)
 static bool is_large(const qft_plan *p) { return p->multipass; }
 
-static int launch_large(qft_plan *p, const void *in, void *out, long long batch, cudaStream_t st) {
+// mode 0: batch complex signals; modes 1-3 (rdft / dct0 / dst0): nreal real rows,
+// batch = row pairs (one vec2 signal per pair)
+static int launch_large(qft_plan *p, int mode, const void *in, void *out, long long batch, long long nreal,
+                        cudaStream_t st) {
+    void *lp = p->large;
+    if (mode != 0) {  // real modes: a schedule whose fold pass covers every block
+        if (!p->large_real) {
+            int e = p->prec == QFT_PREC_F32 ? qft_large_create_f32(p->log2n, 1, &p->large_real)
+                                            : qft_large_create_f64(p->log2n, 1, &p->large_real);
+            if (e) return fail(QFT_ECUDA, "multi-pass schedule upload failed");
+        }
+        lp = p->large_real;
+    }
     // bound the scratch (two buffers per signal) to ~6 GiB: chunk the batch
-    const size_t esz = p->prec == QFT_PREC_F32 ? 8 : 16;
-    const long long cells = p->prec == QFT_PREC_F32 ? qft_large_scratch_cells_f32(p->large)
-                                                    : qft_large_scratch_cells_f64(p->large);
+    const size_t esz = p->prec == QFT_PREC_F32 ? 8 : 16, rsz = esz / 2;
+    const long long cells = p->prec == QFT_PREC_F32 ? qft_large_scratch_cells_f32(lp) : qft_large_scratch_cells_f64(lp);
     const size_t per = 2 * (size_t)cells * esz;
     long long chunk = (long long)(((size_t)6 << 30) / per);
     if (chunk < 1) chunk = 1;
@@ -207,12 +219,19 @@ static int launch_large(qft_plan *p, const void *in, void *out, long long batch,
         p->lscratch_bytes = per * (size_t)chunk;
     }
     const void *uh = p->prec == QFT_PREC_F32 ? (const void *)p->uhead32 : (const void *)p->uhead64;
+    const long long m = p->N / 2;
+    // bytes per input / output unit (a signal, or a real row)
+    const size_t ib = mode == 0 ? (size_t)p->N * esz : (size_t)(mode == 1 ? p->N : (mode == 2 ? m + 1 : m - 1)) * rsz;
+    const size_t ob = mode == 0 ? (size_t)p->N * esz : (mode == 1 ? (size_t)(m + 1) * esz : (size_t)(mode == 2 ? m + 1 : m - 1) * rsz);
     for (long long b0 = 0; b0 < batch; b0 += chunk) {
         const long long nb = batch - b0 < chunk ? batch - b0 : chunk;
-        const char *ci = (const char *)in + (size_t)b0 * p->N * esz;
-        char *co = (char *)out + (size_t)b0 * p->N * esz;
-        int e = p->prec == QFT_PREC_F32 ? qft_large_exec_f32(p->large, ci, co, nb, p->d_U, uh, p->d_lscratch, st)
-                                        : qft_large_exec_f64(p->large, ci, co, nb, p->d_U, uh, p->d_lscratch, st);
+        const long long u0 = mode == 0 ? b0 : 2 * b0;  // first unit of the chunk
+        const long long nr = mode == 0 ? 0 : (nreal - u0 < 2 * nb ? nreal - u0 : 2 * nb);
+        const char *ci = (const char *)in + (size_t)u0 * ib;
+        char *co = (char *)out + (size_t)u0 * ob;
+        int e = p->prec == QFT_PREC_F32
+                    ? qft_large_exec_f32(lp, mode, ci, co, nb, nr, p->d_U, uh, p->d_lscratch, st)
+                    : qft_large_exec_f64(lp, mode, ci, co, nb, nr, p->d_U, uh, p->d_lscratch, st);
         if (e) return fail(QFT_ECUDA, std::string("multi-pass launch: ") + cudaGetErrorString((cudaError_t)e));
     }
     return 0;
@@ -253,7 +272,7 @@ static int launch_classical(qft_plan *p, int mode, const void *in, void *out, lo
 
 static int launch_contig(qft_plan *p, const void *in, void *out, long long batch, cudaStream_t st) {
     if (p->algo == QFT_ALGO_CLASSICAL) return launch_classical(p, 0, in, out, batch, 0, st);
-    if (is_large(p)) return launch_large(p, in, out, batch, st);
+    if (is_large(p)) return launch_large(p, 0, in, out, batch, 0, st);
     if (!smem_available(p->log2n, p->prec))
         return fail(QFT_EUNSUPPORTED, "periodization 2^" + std::to_string(p->log2n) + " not built yet");
     LaunchArgs a{in, out, batch, p->d_U, p->prec == QFT_PREC_F32 ? (const void *)p->uhead32 : (const void *)p->uhead64,
@@ -324,7 +343,8 @@ int qft_plan_create(qft_plan **out, int log2n, int prec, int algo, int device) {
                 cudaSuccess)
             rc = fail(QFT_ECUDA, "table upload failed");
     } else if (!rc && is_large(p)) {
-        int e = prec == QFT_PREC_F32 ? qft_large_create_f32(log2n, &p->large) : qft_large_create_f64(log2n, &p->large);
+        int e = prec == QFT_PREC_F32 ? qft_large_create_f32(log2n, 0, &p->large)
+                                     : qft_large_create_f64(log2n, 0, &p->large);
         if (e) rc = fail(QFT_ECUDA, "multi-pass schedule upload failed");
     }
     if (rc) {
@@ -344,9 +364,10 @@ int qft_plan_destroy(qft_plan *p) {
     if (p->d_T) cudaFree(p->d_T);
     if (p->d_arena) cudaFree(p->d_arena);
     if (p->d_host) cudaFree(p->d_host);
-    if (p->large) {
-        if (p->prec == QFT_PREC_F32) qft_large_destroy_f32(p->large);
-        else qft_large_destroy_f64(p->large);
+    for (void *lp : {p->large, p->large_real}) {
+        if (!lp) continue;
+        if (p->prec == QFT_PREC_F32) qft_large_destroy_f32(lp);
+        else qft_large_destroy_f64(lp);
     }
     for (auto &s : p->streams)
         if (s) cudaStreamDestroy(s);
@@ -513,8 +534,7 @@ int qft_exec_real(const qft_plan *cp, int kind, const void *d_in, void *d_out, i
     CUDA_TRY(cudaSetDevice(p->device));
     std::lock_guard<std::mutex> lk(p->mu);
     if (p->algo == QFT_ALGO_CLASSICAL) return launch_classical(p, kind, d_in, d_out, (nrows + 1) / 2, nrows, (cudaStream_t)stream);
-    if (p->multipass || !smem_available(p->log2n, p->prec))
-        return fail(QFT_EUNSUPPORTED, "improved real transforms are built for N <= 16384 (fp32) / 8192 (fp64)");
+    if (p->multipass) return launch_large(p, kind, d_in, d_out, (nrows + 1) / 2, nrows, (cudaStream_t)stream);
     LaunchArgs a{d_in, d_out, (nrows + 1) / 2, p->d_U,
                  p->prec == QFT_PREC_F32 ? (const void *)p->uhead32 : (const void *)p->uhead64, p->num_sms,
                  (cudaStream_t)stream, nrows};

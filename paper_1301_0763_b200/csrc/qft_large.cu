@@ -70,8 +70,10 @@ struct QFT_LG(LargePlan) {
     void *d_items = nullptr, *d_leaves = nullptr;
     int nitems = 0;
     int launches = 0;
-    explicit QFT_LG(LargePlan)(int log2n)
-        : sublog(sublog_for(log2n)), J0(log2n - sublog_for(log2n)), s(log2n, sublog_for(log2n), kRG, J0, true) {}
+    QFT_LG(LargePlan)(int log2n, bool real_modes)
+        : sublog(sublog_for(log2n)),
+          J0(log2n - sublog_for(log2n)),
+          s(log2n, sublog_for(log2n), kRG, J0, true, !real_modes) {}
 };
 
 template <typename TT>
@@ -122,6 +124,28 @@ __global__ void __launch_bounds__(kFoldT) lg_fold_kernel(const vec2<T> *__restri
                 w[cell] = vadd(u[r], v[r]);
                 w[m + cell] = vsub(u[r], v[r]);
             }
+        }
+    }
+}
+
+// real modes: two rows of the mode's stored length per vec2 signal (pairs
+// (2p, 2p+1); an odd last row pairs with itself and only its lane is stored)
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kFoldT) lg_fold_real_kernel(const T *__restrict__ xr, vec2<T> *__restrict__ W0,
+                                                              int log2n, long long batch, long long nreal,
+                                                              long long Ws) {
+    const int N = 1 << log2n, m = N / 2;
+    const long long RL = MODE == 1 ? N : (MODE == 2 ? m + 1 : m - 1);
+    const int cnt = m + 1;  // n in [0, m]
+    const int nch = (cnt + kFoldN - 1) / kFoldN;
+    for (long long g = blockIdx.x; g < batch * nch; g += gridDim.x) {
+        const long long b = g / nch;
+        const int a = (int)(g - b * nch) * kFoldN;
+        const long long ra = 2 * b, rb = ra + 1 < nreal ? ra + 1 : ra;
+        vec2<T> *w = W0 + b * Ws;
+        for (int n = a + threadIdx.x; n < a + kFoldN && n < cnt; n += kFoldT) {
+            if (n == m) continue;  // rdft / dct0: s(m) is routed with n = 0; dst0 has no s(m)
+            lg_fold_real_item<T, MODE>(xr + ra * RL, xr + rb * RL, w, n, N, log2n);
         }
     }
 }
@@ -436,6 +460,38 @@ __global__ void lg_chain_kernel(const vec2<T> *W0, const vec2<T> *W1, const vec2
     }
 }
 
+template <typename T, int LOG2N, int RC, int MODE>
+__global__ void lg_chain_real_kernel(const vec2<T> *W0, const vec2<T> *W1, void *y, uint32_t cmask, uint32_t smask,
+                                     long long batch, long long nreal, long long Ws, int J0, int mj0) {
+    constexpr int N = 1 << LOG2N, m = N / 2;
+    constexpr long long OL = MODE == 3 ? m - 1 : m + 1;  // output row length (complex for rdft)
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > (N >> (RC + 1))) return;
+    for (long long b = blockIdx.y; b < batch; b += gridDim.y) {
+        GChain<T> g;
+        g.n = LOG2N;
+        g.N = N;
+        g.m = m;
+        g.w0 = W0 + b * Ws;
+        g.w1 = W1 + b * Ws;
+        g.x = nullptr;
+        g.cmask = cmask;
+        g.smask = smask;
+        g.J0 = J0;
+        g.cb = g.w0 + (N + 2);
+        g.sb = g.cb + mj0 + 1;
+        const long long ra = 2 * b;
+        const bool has_b = ra + 1 < nreal;
+        if constexpr (MODE == 1) {
+            vec2<T> *yy = static_cast<vec2<T> *>(y);
+            g.template unit_real<RC, MODE>(yy + ra * OL, yy + (ra + 1) * OL, has_b, t);
+        } else {
+            T *yy = static_cast<T *>(y);
+            g.template unit_real<RC, MODE>(yy + ra * OL, yy + (ra + 1) * OL, has_b, t);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ host
 template <typename K, typename... A>
 static cudaError_t launch(K k, dim3 g, dim3 bl, size_t smem, cudaStream_t st, A... a) {
@@ -447,8 +503,8 @@ static unsigned ybatch(long long batch) { return (unsigned)std::min<long long>(b
 
 extern "C++" {
 
-int QFT_LG(qft_large_create)(int log2n, void **out) {
-    auto *p = new QFT_LG(LargePlan)(log2n);
+int QFT_LG(qft_large_create)(int log2n, int real_modes, void **out) {
+    auto *p = new QFT_LG(LargePlan)(log2n, real_modes != 0);
     const Sched &S = p->s;
     int rc = 0;
     p->fset.resize(S.f.size());
@@ -539,8 +595,8 @@ long long QFT_LG(qft_large_scratch_cells)(void *pp) {
     return (long long)p->s.N + 2 + 2 * ((1ll << (p->sublog - 1)) + 1);
 }
 
-int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long batch, const void *d_U,
-                           const void *uhead, void *scratch, cudaStream_t st) {
+int QFT_LG(qft_large_exec)(void *pp, int mode, const void *d_in, void *d_out, long long batch, long long nreal,
+                           const void *d_U, const void *uhead, void *scratch, cudaStream_t st) {
     auto *p = (QFT_LG(LargePlan) *)pp;
     using T = Real;
     const Sched &S = p->s;
@@ -555,9 +611,22 @@ int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long ba
     cudaError_t e;
     // fold pass
     {
-        const long long work = batch * (((S.m >> S.jfold) + kFoldN - 1) / kFoldN);
-        const unsigned grid = (unsigned)std::min<long long>(work, 1 << 20);
-        e = launch(lg_fold_kernel<T>, dim3(grid), dim3(kFoldT), 0, st, x, W0, S.n, S.jfold, batch, Ws);
+        if (mode == 0) {
+            const long long work = batch * (((S.m >> S.jfold) + kFoldN - 1) / kFoldN);
+            const unsigned grid = (unsigned)std::min<long long>(work, 1 << 20);
+            e = launch(lg_fold_kernel<T>, dim3(grid), dim3(kFoldT), 0, st, x, W0, S.n, S.jfold, batch, Ws);
+        } else {
+            if (S.jfold != 0) return (int)cudaErrorInvalidValue;  // real modes need the full fold pass
+            const long long work = batch * ((S.m + 1 + kFoldN - 1) / kFoldN);
+            const unsigned grid = (unsigned)std::min<long long>(work, 1 << 20);
+            const T *xr = (const T *)d_in;
+            switch (mode) {
+                case 1: e = launch(lg_fold_real_kernel<T, 1>, dim3(grid), dim3(kFoldT), 0, st, xr, W0, S.n, batch, nreal, Ws); break;
+                case 2: e = launch(lg_fold_real_kernel<T, 2>, dim3(grid), dim3(kFoldT), 0, st, xr, W0, S.n, batch, nreal, Ws); break;
+                case 3: e = launch(lg_fold_real_kernel<T, 3>, dim3(grid), dim3(kFoldT), 0, st, xr, W0, S.n, batch, nreal, Ws); break;
+                default: return (int)cudaErrorInvalidValue;
+            }
+        }
         if (e) return (int)e;
     }
     // forward passes: one launch per depth
@@ -621,8 +690,19 @@ int QFT_LG(qft_large_exec)(void *pp, const void *d_in, void *d_out, long long ba
     const dim3 cg((threads + 127) / 128, yb), cb(128);
     const vec2<T> *w0 = W0, *w1 = W1;
     const int mj0 = 1 << (p->sublog - 1);
-#define QFT_CH(LG, R) \
-    case LG * 8 + R: e = launch(lg_chain_kernel<T, LG, R>, cg, cb, 0, st, w0, w1, x, y, S.cmask, S.smask, batch, Ws, p->J0, mj0); break;
+#define QFT_CH(LG, R)                                                                                           \
+    case LG * 8 + R:                                                                                            \
+        switch (mode) {                                                                                         \
+            case 0: e = launch(lg_chain_kernel<T, LG, R>, cg, cb, 0, st, w0, w1, x, y, S.cmask, S.smask, batch,  \
+                               Ws, p->J0, mj0); break;                                                          \
+            case 1: e = launch(lg_chain_real_kernel<T, LG, R, 1>, cg, cb, 0, st, w0, w1, d_out, S.cmask, S.smask, \
+                               batch, nreal, Ws, p->J0, mj0); break;                                            \
+            case 2: e = launch(lg_chain_real_kernel<T, LG, R, 2>, cg, cb, 0, st, w0, w1, d_out, S.cmask, S.smask, \
+                               batch, nreal, Ws, p->J0, mj0); break;                                            \
+            case 3: e = launch(lg_chain_real_kernel<T, LG, R, 3>, cg, cb, 0, st, w0, w1, d_out, S.cmask, S.smask, \
+                               batch, nreal, Ws, p->J0, mj0); break;                                            \
+        }                                                                                                       \
+        break;
 #define QFT_CHR(LG) QFT_CH(LG, 1) QFT_CH(LG, 2) QFT_CH(LG, 3) QFT_CH(LG, 4)
     switch (S.n * 8 + RC) {
         QFT_CHR(13) QFT_CHR(14) QFT_CHR(15) QFT_CHR(16) QFT_CHR(17) QFT_CHR(18) QFT_CHR(19) QFT_CHR(20)

@@ -216,10 +216,11 @@ struct GChain {
         }
     }
 
-    template <int J>
-    QFT_HD void up(vec2<T> *y, int k, vec2<T> cv, vec2<T> sv) const {
+    // unfold RC levels; emit(k, C_0[k], S_0[k]) for every harmonic k of the group
+    template <int J, class Emit>
+    QFT_HD void up_e(Emit &emit_fn, int k, vec2<T> cv, vec2<T> sv) const {
         if constexpr (J == 0) {
-            emit(y, k, cv, sv);
+            emit_fn(k, cv, sv);
         } else {
             const int q = qj(J - 1), mm = 2 * q;
             const bool self = (k == q);
@@ -227,8 +228,8 @@ struct GChain {
             const vec2<T> os = OS(J - 1, k > 0 ? k : 1);
             const vec2<T> clo = self ? cv : vadd(cv, o), chi = self ? cv : vsub(cv, o);
             const vec2<T> slo = self ? os : vadd(os, sv), shi = self ? os : vsub(os, sv);
-            up<J - 1>(y, k, clo, slo);
-            up<J - 1>(y, self ? q : mm - k, chi, shi);
+            up_e<J - 1>(emit_fn, k, clo, slo);
+            up_e<J - 1>(emit_fn, self ? q : mm - k, chi, shi);
         }
     }
 
@@ -236,8 +237,65 @@ struct GChain {
     QFT_HD void unit(vec2<T> *y, int t) const {
         vec2<T> cv, sv;
         descend<RC>(t, cv, sv);
-        up<RC>(y, t, cv, sv);
+        auto e = [&](int k, vec2<T> c, vec2<T> s) { emit(y, k, c, s); };
+        up_e<RC>(e, t, cv, sv);
+    }
+    // real modes (MODE 1 rdft, 2 dct0, 3 dst0): the two lanes are two real rows
+    // a, b (b absent when has_b is false); outputs as qft_cdft_smem's real modes
+    template <int RC, int MODE>
+    QFT_HD void unit_real(void *ya, void *yb, bool has_b, int t) const {
+        vec2<T> cv, sv;
+        descend<RC>(t, cv, sv);
+        auto e = [&](int k, vec2<T> c, vec2<T> s) {
+            if constexpr (MODE == 1) {  // packed half spectrum -> complex (shared.py:38-43, 94-101)
+                const bool edge = (k == 0) || (k == m);
+                static_cast<vec2<T> *>(ya)[k] = {c.x, edge ? (T)0 : -s.x};
+                if (has_b) static_cast<vec2<T> *>(yb)[k] = {c.y, edge ? (T)0 : -s.y};
+            } else if constexpr (MODE == 2) {
+                static_cast<T *>(ya)[k] = c.x;
+                if (has_b) static_cast<T *>(yb)[k] = c.y;
+            } else {
+                if (k == 0 || k == m) return;
+                static_cast<T *>(ya)[k - 1] = s.x;
+                if (has_b) static_cast<T *>(yb)[k - 1] = s.y;
+            }
+        };
+        up_e<RC>(e, t, cv, sv);
     }
 };
+
+// ----------------------------------------------------------------- fold (real modes)
+// Two real rows a, b of the mode's stored length as one vec2 signal, written
+// into the Lee-block cell layout (the a0_item_real routing of qft_smem.cuh):
+// rdft folds x[n] +- x[N-n]; dct0 / dst0 place s(n) on the cosine / sine side.
+template <typename T, int MODE>
+QFT_HD void lg_fold_real_item(const T *xa, const T *xb, vec2<T> *w, int n, int N, int log2n) {
+    const int m = N / 2;
+    auto at = [&](int i) { return vec2<T>{xa[i], xb[i]}; };
+    auto cell_of = [&](int nn) {
+        const int j = ctz32((uint32_t)nn);
+        return m - (1 << (log2n - 1 - j)) + (nn >> (j + 1));
+    };
+    if constexpr (MODE == 1) {
+        if (n == 0) {
+            w[N - 1] = at(0);
+            w[N] = at(m);
+        } else {
+            const vec2<T> a = at(n), b = at(N - n);
+            const int c = cell_of(n);
+            w[c] = vadd(a, b);
+            w[m + c] = vsub(a, b);
+        }
+    } else if constexpr (MODE == 2) {
+        if (n == 0) {
+            w[N - 1] = at(0);
+            w[N] = at(m);
+        } else {
+            w[cell_of(n)] = at(n);
+        }
+    } else {
+        if (n > 0) w[m + cell_of(n)] = at(n - 1);
+    }
+}
 
 }  // namespace qft

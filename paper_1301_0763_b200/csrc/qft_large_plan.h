@@ -58,14 +58,16 @@ struct LargeSchedule {
     // jmax > 0: only the blocks j < jmax (the rest belong to the sub-signal
     // transform of x[2^jmax k], see qft_large.cu)
     // fold_pass: a separate pass folds x into W0 first (no fold on first touch)
-    LargeSchedule(int log2n, int leaflog, int rg, int jmax = -1, bool fold_pass = false)
+    // first_touch = false: the fold pass covers every block (real modes, whose
+    // input is not the complex fold)
+    LargeSchedule(int log2n, int leaflog, int rg, int jmax = -1, bool fold_pass = false, bool first_touch = true)
         : n(log2n), N(1 << log2n), m(1 << (log2n - 1)), LEAFLOG(leaflog), RG(rg) {
         fold = fold_pass;
         const int jend = jmax > 0 ? jmax : n - 1;
         // blocks j < jfold are cut by F passes whose first touch folds x; with a
         // fold pass, it folds only the samples of blocks j >= jfold
         jfold = 0;
-        while (jfold < jend && (1 << (n - 2 - jfold)) > (1 << LEAFLOG)) ++jfold;
+        while (first_touch && jfold < jend && (1 << (n - 2 - jfold)) > (1 << LEAFLOG)) ++jfold;
         for (int side = 0; side < 2; ++side)
             for (int j = 0; j < jend; ++j) {
                 const int L = 1 << (n - 2 - j);

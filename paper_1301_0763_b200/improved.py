@@ -16,7 +16,7 @@ numpy inputs go through the C-ABI host path (H2D, transform, D2H); a CUDA
 ``torch.Tensor`` stays on its device.  ``cdft_rows`` is the batch-major fast
 path ((batch, N) tensor, transform along the last axis).  ``rdft``, ``dct0`` and
 ``dst0`` (improved.py:117-136) run the same kernels on real rows, two rows per
-complex lane (``qft_exec_real``; N <= 4096).  There is no CPU fallback: without
+complex lane (``qft_exec_real``; every N up to 2^20).  There is no CPU fallback: without
 the CUDA library or a GPU these functions raise.
 """
 

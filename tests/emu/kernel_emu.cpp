@@ -172,8 +172,18 @@ static void emu_real_one(const T *xa, const T *xb, T *ya, T *yb, const T *U) {
     for (int t = 0; t < P::DT; ++t) Chain<LOG2N, T>::unit_e(w, emit, t);
 }
 
+template <typename T, int SUBLOG, int MODE>
+static int emu_large_real(int log2n, const T *xa, const T *xb, T *ya, T *yb, const T *U);
+
 template <typename T, int MODE>
 static int emu_real_dispatch(int log2n, const T *xa, const T *xb, T *ya, T *yb, const T *U) {
+    const int cap = sizeof(T) == 4 ? 14 : 13;
+    if (log2n > cap) {
+        const int sl = log2n - 1 < cap ? log2n - 1 : cap;
+        if (sl == 13) return emu_large_real<T, 13, MODE>(log2n, xa, xb, ya, yb, U);
+        if (sl == 14) return emu_large_real<T, 14, MODE>(log2n, xa, xb, ya, yb, U);
+        return -1;
+    }
     switch (log2n) {
         case 6: emu_real_one<6, T, MODE>(xa, xb, ya, yb, U); return 0;
         case 7: emu_real_one<7, T, MODE>(xa, xb, ya, yb, U); return 0;
@@ -318,6 +328,71 @@ static int emu_large(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
     }
     return 0;
 }
+// real modes through the multi-pass path: fold pass over every block (no
+// first touch), same items / B passes, real-mode chain emit
+template <typename T, int SUBLOG, int MODE>
+static int emu_large_real(int log2n, const T *xa, const T *xb, T *ya, T *yb, const T *U) {
+    const int J0 = log2n - SUBLOG, RG = sizeof(T) == 4 ? 5 : 4;
+    LargeSchedule S(log2n, SUBLOG, RG, J0, true, false);
+    const int N = S.N, mj0 = 1 << (SUBLOG - 1);
+    const long long Ws = N + 2 + 2 * (mj0 + 1);
+    std::vector<vec2<T>> W0(Ws), W1(Ws);
+    vec2<T> *W[2] = {W0.data(), W1.data()};
+    for (int n = 0; n < N / 2; ++n) lg_fold_real_item<T, MODE>(xa, xb, W[0], n, N, log2n);
+    for (auto &lvl : S.f)
+        for (auto &kv : lvl)
+            for (auto &td : kv.second) {
+                switch (kv.first) {
+                    case 1: emu_f_task<1, T>(W[0], td.first, td.second, U, nullptr, N); break;
+                    case 2: emu_f_task<2, T>(W[0], td.first, td.second, U, nullptr, N); break;
+                    case 3: emu_f_task<3, T>(W[0], td.first, td.second, U, nullptr, N); break;
+                    case 4: emu_f_task<4, T>(W[0], td.first, td.second, U, nullptr, N); break;
+                    case 5: emu_f_task<5, T>(W[0], td.first, td.second, U, nullptr, N); break;
+                }
+            }
+    vec2<T> *cb = W[0] + (N + 2), *sb = cb + mj0 + 1;
+    emu_sub<SUBLOG, T>(W[0], N / 2, cb, sb, U);
+    for (auto &kv : S.leaf)
+        for (auto &tk : kv.second) {
+            if (kv.first == SUBLOG) emu_leaf<SUBLOG, T>(W[0], tk, U, nullptr, N);
+            else emu_leaf<SUBLOG - 1, T>(W[0], tk, U, nullptr, N);
+        }
+    for (int d = (int)S.b.size() - 1; d >= 0; --d)
+        for (auto &kv : S.b[d])
+            for (auto &tk : kv.second) {
+                switch (kv.first) {
+                    case 1: emu_b_task<1, T>(W, tk); break;
+                    case 2: emu_b_task<2, T>(W, tk); break;
+                    case 3: emu_b_task<3, T>(W, tk); break;
+                    case 4: emu_b_task<4, T>(W, tk); break;
+                    case 5: emu_b_task<5, T>(W, tk); break;
+                }
+            }
+    GChain<T> g;
+    g.n = log2n;
+    g.N = N;
+    g.m = N / 2;
+    g.w0 = W[0];
+    g.w1 = W[1];
+    g.x = nullptr;
+    g.cmask = S.cmask;
+    g.smask = S.smask;
+    g.J0 = J0;
+    g.cb = cb;
+    g.sb = sb;
+    const int RC = J0 < 4 ? J0 : 4;
+    // the emulator's output rows: rdft as interleaved (re, im) pairs
+    for (int t = 0; t <= (N >> (RC + 1)); ++t) {
+        switch (RC) {
+            case 1: g.template unit_real<1, MODE>(ya, yb, true, t); break;
+            case 2: g.template unit_real<2, MODE>(ya, yb, true, t); break;
+            case 3: g.template unit_real<3, MODE>(ya, yb, true, t); break;
+            case 4: g.template unit_real<4, MODE>(ya, yb, true, t); break;
+        }
+    }
+    return 0;
+}
+
 // sub-signal size of the device plan (qft_large.cu sublog_for)
 template <typename T>
 static int emu_large_any(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {

@@ -48,7 +48,7 @@ def test_emulated_kernel_bitwise(emu, oracle_mod, dt, lg):
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
-@pytest.mark.parametrize("lg", [6, 9, 12, 13, 14])
+@pytest.mark.parametrize("lg", [6, 9, 12, 13, 14, 15, 16, 18])
 @pytest.mark.parametrize("kind", ["rdft", "dct0", "dst0"])
 def test_emulated_real_modes_bitwise(emu, oracle_mod, dt, lg, kind):
     """improved.rdft/dct0/dst0 through the same phase functions (two real rows per lane)."""
