@@ -285,12 +285,23 @@ template <int A, typename T, int NT, int NW>
 QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const T *kcu, vec2<T> *wb, int tid) {
     constexpr int L = 1 << A;
     const int warp = tid >> 5, lane = tid & 31;
-    // load: async cell copies along the (forward or reversed) runs
+    // load: async cell copies along the (forward or reversed) runs; with NT a
+    // multiple of 32 dividing L, thread tid's cells are tid + k NT and their padded
+    // addresses advance by NT + NT/32: pointer increments only
+    constexpr bool LIN = (L % NT) == 0 && (NT % 32) == 0;
     for (int k = 0; k < K; ++k) {
         const LeafTask tk = tks[k];
         vec2<T> *s = S + padx(k * L);
         const vec2<T> *src = wb + tk.c;
-        for (int e = tid; e < L; e += NT) cp_async_cell<T>(s + padx(e), src + tk.sg * e);
+        if constexpr (LIN) {
+            vec2<T> *d = s + padx(tid);
+            const vec2<T> *q = src + tk.sg * tid;
+            const long long step = (long long)tk.sg * NT;
+#pragma unroll 8
+            for (int r = 0; r < L / NT; ++r, d += NT + NT / 32, q += step) cp_async_cell<T>(d, q);
+        } else {
+            for (int e = tid; e < L; e += NT) cp_async_cell<T>(s + padx(e), src + tk.sg * e);
+        }
     }
     cp_async_wait_all();
     __syncthreads();
@@ -360,8 +371,16 @@ QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const
         const LeafTask tk = tks[k];
         const vec2<T> *s = S + padx(k * L);
         vec2<T> *dst = wb + tk.c;
+        if constexpr (LIN) {
+            const vec2<T> *d = s + padx(tid);
+            vec2<T> *q = dst + tk.sg * tid;
+            const long long step = (long long)tk.sg * NT;
 #pragma unroll 8
-        for (int e = tid; e < L; e += NT) dst[tk.sg * e] = s[padx(e)];
+            for (int r = 0; r < L / NT; ++r, d += NT + NT / 32, q += step) *q = *d;
+        } else {
+#pragma unroll 8
+            for (int e = tid; e < L; e += NT) dst[tk.sg * e] = s[padx(e)];
+        }
     }
 }
 
@@ -377,9 +396,22 @@ QFT_DEV void sub_item(const vec2<T> *w0b, int m, vec2<T> *W, const T *U, const T
     {
         constexpr int MP = P::m;
         const vec2<T> *wc = w0b + (m - MP), *ws = w0b + (2 * m - MP);
-        for (int c = tid; c < MP - 1; c += NT) {
-            cp_async_cell<T>(W + padx(c), wc + c);
-            cp_async_cell<T>(W + padx(P::S0 + c), ws + c);
+        if constexpr (MP % NT == 0 && NT % 32 == 0) {
+            // cells tid + r NT (the last cosine / sine cell MP-1 is unused or the base)
+            vec2<T> *dc = W + padx(tid), *dsn = W + padx(P::S0 + tid);
+#pragma unroll 8
+            for (int r = 0; r < MP / NT; ++r, dc += NT + NT / 32, dsn += NT + NT / 32) {
+                const int c = tid + r * NT;
+                if (c < MP - 1) {
+                    cp_async_cell<T>(dc, wc + c);
+                    cp_async_cell<T>(dsn, ws + c);
+                }
+            }
+        } else {
+            for (int c = tid; c < MP - 1; c += NT) {
+                cp_async_cell<T>(W + padx(c), wc + c);
+                cp_async_cell<T>(W + padx(P::S0 + c), ws + c);
+            }
         }
         if (tid < 2) cp_async_cell<T>(W + padx(P::BASE + tid), w0b + 2 * m - 1 + tid);
         cp_async_wait_all();
