@@ -16,6 +16,12 @@
  *
  * Every function returns 0 on success or a negative QFT_E* code; the message
  * of the last failure on the calling thread is available from qft_last_error().
+ *
+ * Sizes: N = 2 .. 2^20 in both precisions.  N <= 2^14 (fp32) / 2^13 (fp64) runs
+ * one single-pass kernel; larger N the multi-pass schedule (qft_plan_info_t
+ * passes / kernel_launches).  Concurrency: a plan owns scratch memory (multi-
+ * pass, classical and layout conversion), so one plan serves one stream at a
+ * time, like a cuFFT plan; create one plan per concurrent stream.
  */
 #ifndef QFT_B200_H
 #define QFT_B200_H
@@ -93,7 +99,8 @@ int qft_exec_cdft(const qft_plan *plan, const void *d_in, void *d_out, int64_t b
  *   QFT_KIND_DCT0: rows of N/2+1 reals s(0..N/2) -> N/2+1 reals
  *   QFT_KIND_DST0: rows of N/2-1 reals s(1..N/2-1) -> N/2-1 reals
  * Precision = the plan's (real float32 for QFT_PREC_F32).  Two rows share one
- * complex-typed lane of the kernels; every row is bit-identical to the reference. */
+ * complex-typed lane of the kernels; every row is bit-identical to the reference.
+ * On a QFT_ALGO_CLASSICAL plan: classical.rdft / dct0 / dst0 (classical.py:134-153). */
 int qft_exec_real(const qft_plan *plan, int kind, const void *d_in, void *d_out, int64_t nrows, void *stream);
 
 /* Same transform on HOST buffers: chunked host->device copy, transform and
