@@ -13,7 +13,7 @@
 #include "qft_smem.cuh"
 
 #ifndef QFT_CTAS_PER_SM
-#define QFT_CTAS_PER_SM 1  // shared-memory budget split: CTAs resident per SM
+#define QFT_CTAS_PER_SM 1  // shared-memory budget split: CTAs resident per SM (N <= 4096)
 #endif
 #ifndef QFT_A0_TMA
 #define QFT_A0_TMA 1       // A0 input: TMA bulk copy into a staging buffer when it fits (1), else L2-prefetched global loads
@@ -101,14 +101,16 @@ struct KCfg {
     using P = SPlan<LOG2N>;
     static constexpr int VB = (int)sizeof(vec2<T>);
     static constexpr int UB = P::UCELLS * (int)sizeof(T);
-    static constexpr int BUDGET = (226 * 1024) / QFT_CTAS_PER_SM - UB - 64;
+    // CTAs per SM: the QFT_CTAS_PER_SM split applies where one signal still fits
+    static constexpr int CPS = (P::n <= 12 && QFT_CTAS_PER_SM > 1) ? QFT_CTAS_PER_SM : 1;
+    static constexpr int BUDGET = (226 * 1024) / CPS - UB - 64;
     static constexpr int PER_W = P::PADDED * VB;        // working area per signal
     static constexpr int PER_S = P::N * VB + PER_W;     // + TMA staging
     static constexpr int TTC = P::n >= 12 ? QFT_TT_MAX : 64;
     static constexpr int clampt(int t) { return t < 1 ? 1 : (t > TTC ? TTC : t); }
     // stage through TMA when the staging buffer still leaves room for 2 signals
     // (fp32) / 1 signal (fp64, whose global A0 path spills)
-    static constexpr int TMA_MIN = sizeof(T) == 8 ? 1 : (TTC < 2 ? TTC : 2);
+    static constexpr int TMA_MIN = (sizeof(T) == 8 || CPS > 1) ? 1 : (TTC < 2 ? TTC : 2);
     static constexpr bool TMA0 = QFT_A0_TMA && BUDGET / PER_S >= TMA_MIN;
     // mixed staging (QFT_MIXED_STAGE, fp32 N = 4096): more signals per iteration
     // than fit with staging; TS of them are TMA-staged, the rest are read from
@@ -148,7 +150,7 @@ struct KCfg {
 template <int LOG2N, typename T>
 constexpr bool smem_fits() {
     using P = SPlan<LOG2N>;
-    return (P::PADDED * (int)sizeof(vec2<T>) + P::UCELLS * (int)sizeof(T) + 64) <= (226 * 1024) / QFT_CTAS_PER_SM;
+    return (P::PADDED * (int)sizeof(vec2<T>) + P::UCELLS * (int)sizeof(T) + 64) <= (226 * 1024) / ((LOG2N <= 12 && QFT_CTAS_PER_SM > 1) ? QFT_CTAS_PER_SM : 1);
 }
 
 // ------------------------------------------------------------ small N
@@ -477,7 +479,7 @@ QFT_DEV void a0_chunks(const vec2<T> *xf, const vec2<T> *xm, int c0, int c1, vec
 // dst0 on real rows (nreal rows of the mode's stored length), two rows per vec2
 // signal; `batch` then counts row pairs.
 template <int LOG2N, typename T, int MODE = 0>
-__global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, QFT_CTAS_PER_SM)
+__global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
     qft_cdft_smem(const vec2<T> *__restrict__ in, vec2<T> *__restrict__ out, long long batch,
                   const T *__restrict__ Ug, const __grid_constant__ LeeConst<T> kc, long long nreal = 0) {
     using P = SPlan<LOG2N>;
