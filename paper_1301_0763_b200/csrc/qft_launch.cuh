@@ -21,6 +21,9 @@
 #ifndef QFT_A0_UNR
 #define QFT_A0_UNR 8       // A0 from global memory: 64-sample chunks in flight per warp (fp32)
 #endif
+#ifndef QFT_D_HALF
+#define QFT_D_HALF 0  // see KCfg::DHALF
+#endif
 #ifndef QFT_HALF_STAGE
 #define QFT_HALF_STAGE 0  // see KCfg::HS (measured slower at N = 2^14)
 #endif
@@ -129,7 +132,10 @@ struct KCfg {
     static constexpr int mx(int a, int b) { return a > b ? a : b; }
     static constexpr int NU = 2 * (P::NU1 + 1);  // fused warp units per signal
     static constexpr int W_U = TT * NU;
-    static constexpr int W_D = (TT * P::DT + 31) / 32;
+    // phase D in half items (QFT_D_HALF): twice the items, each half the unfold
+    static constexpr bool DHALF = QFT_D_HALF && P::RC >= 1;
+    static constexpr int DI = DHALF ? 2 * P::DT : P::DT;  // phase-D items per signal
+    static constexpr int W_D = (TT * DI + 31) / 32;
     static constexpr int NW0 = mx(W_U, W_D);
     // warps are spread over 4 SM sub-partitions of 16K registers each: 12 warps
     // keep 168 registers (fp64), 16 keep 128; 17 (fp32, N <= 4096) drop to 96
@@ -574,12 +580,19 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
         // TB: top backward levels of the huge blocks (ends with a barrier)
         if constexpr (P::JH > 0) top_b<LOG2N, T, MODE>(W, ntr, tid);
         // D: chain + recombination -> global
-        for (int it = tid; it < TT * P::DT; it += NT) {
-            const int tau = it / P::DT, t = it - tau * P::DT;
+        for (int it = tid; it < TT * K::DI; it += NT) {
+            const int tau = it / K::DI, ti = it - tau * K::DI;
             if (tau >= ntr) continue;
             if constexpr (MODE == 0) {
-                Chain<LOG2N, T>::unit(W + tau * P::PADDED, out + (bt * TT + tau) * P::N, t);
+                if constexpr (K::DHALF) {
+                    const int h = ti >= P::DT, t = ti - (h ? P::DT : 0);
+                    Chain<LOG2N, T>::unit_half(W + tau * P::PADDED, out + (bt * TT + tau) * P::N, t, h);
+                } else {
+                    Chain<LOG2N, T>::unit(W + tau * P::PADDED, out + (bt * TT + tau) * P::N, ti);
+                }
             } else {
+                const int t = K::DHALF ? (ti >= P::DT ? ti - P::DT : ti) : ti;
+                const int h = K::DHALF ? (ti >= P::DT) : 0;
                 // per-signal outputs: rdft packed half spectrum (shared.py:38-43 with
                 // complex_from_packed, shared.py:94-101), dct0 / dst0 real spectra
                 const long long ra = 2 * (bt * TT + tau);
@@ -601,7 +614,8 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
                         if (has_b) ya[P::m - 1 + k - 1] = sv.y;
                     }
                 };
-                Chain<LOG2N, T>::unit_e(W + tau * P::PADDED, emit, t);
+                if constexpr (K::DHALF) Chain<LOG2N, T>::unit_e_half(W + tau * P::PADDED, emit, t, h);
+                else Chain<LOG2N, T>::unit_e(W + tau * P::PADDED, emit, t);
             }
         }
         __syncthreads();

@@ -430,6 +430,26 @@ struct Chain {
         auto emit = [&](int k, vec2<T> cv, vec2<T> sv) { emit_u(y, k, cv, sv); };
         unit_e(w, emit, t);
     }
+    // half of a phase-D item: the descent, then the low (h = 0) or high (h = 1)
+    // child of the first unfold level (selected branch-free), then RC-1 levels
+    template <class Emit>
+    static QFT_HD void unit_e_half(const vec2<T> *w, Emit &emit, int t, int h) {
+        static_assert(P::RC >= 1, "half items need one unfold level");
+        vec2<T> cv, sv;
+        if constexpr (P::RC < n - 1) desc2<P::RC>(w, t, cv, sv);
+        constexpr int q = qj(P::RC - 1), mm = 2 * q;
+        const bool self = (t == q);
+        const vec2<T> o = OC(w, P::RC - 1, t < q ? t : 0);
+        const vec2<T> os = OS(w, P::RC - 1, t > 0 ? t : 1);
+        const vec2<T> c_lo = vadd(cv, o), c_hi = vsub(cv, o), s_lo = vadd(os, sv), s_hi = vsub(os, sv);
+        const int k = h ? (self ? q : mm - t) : t;
+        const vec2<T> c1 = self ? cv : (h ? c_hi : c_lo), s1 = self ? os : (h ? s_hi : s_lo);
+        up_e<P::RC - 1>(w, emit, k, c1, s1);
+    }
+    static QFT_HD void unit_half(const vec2<T> *w, vec2<T> *y, int t, int h) {
+        auto emit = [&](int k, vec2<T> cv, vec2<T> sv) { emit_u(y, k, cv, sv); };
+        unit_e_half(w, emit, t, h);
+    }
 };
 
 }  // namespace qft
