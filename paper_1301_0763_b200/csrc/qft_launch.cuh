@@ -24,9 +24,6 @@
 #ifndef QFT_D_HALF
 #define QFT_D_HALF 0  // see KCfg::DHALF
 #endif
-#ifndef QFT_HALF_STAGE
-#define QFT_HALF_STAGE 0  // see KCfg::HS (measured slower at N = 2^14)
-#endif
 #ifndef QFT_MIXED_STAGE
 #define QFT_MIXED_STAGE 0  // see KCfg::MIXED
 #endif
@@ -83,17 +80,6 @@ QFT_DEV void tma_bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t 
                  : "memory");
 }
 
-// two bulk copies completing one mbarrier phase
-QFT_DEV void tma_bulk_load2(void *d1, const void *s1, uint32_t b1, void *d2, const void *s2, uint32_t b2,
-                            uint64_t *bar) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(b1 + b2) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(d1)), "l"(s1), "r"(b1), "r"(smem_u32(bar)) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(d2)), "l"(s2), "r"(b2), "r"(smem_u32(bar)) : "memory");
-}
-
 QFT_DEV void l2_prefetch(const void *src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
@@ -123,11 +109,6 @@ struct KCfg {
     static constexpr int TS0 = MIXED ? (BUDGET - TT * PER_W) / (P::N * VB) : (TMA0 ? TT : 0);
     static constexpr int TS = TS0 > TT ? TT : TS0;  // TMA-staged signals per iteration
     static constexpr bool TMA = TS > 0;
-    // half staging (one signal per iteration, no room for a full staging buffer):
-    // x[0, N/4) and x[3N/4, N) -- the samples of the first half of the A0
-    // chunks and their mirrors -- are TMA-staged, the rest read from L2
-    static constexpr bool HS = QFT_HALF_STAGE && !TMA && sizeof(T) == 4 && TT == 1 &&
-                               BUDGET - PER_W >= (P::N / 2) * VB;
     static_assert(TT * PER_W <= BUDGET, "working area exceeds shared memory");
     static constexpr int mx(int a, int b) { return a > b ? a : b; }
     static constexpr int NU = 2 * (P::NU1 + 1);  // fused warp units per signal
@@ -144,7 +125,7 @@ struct KCfg {
     static constexpr int NW = NW0 < NWLO ? NWLO : (NW0 > NWMAX ? NWMAX : NW0);
     static constexpr int NT = NW * 32;
     static constexpr int STAGE_OFF = 0;
-    static constexpr int W_OFF = HS ? (P::N / 2) * VB : TS * P::N * VB;
+    static constexpr int W_OFF = TS * P::N * VB;
     static constexpr int U_OFF = W_OFF + TT * PER_W;
     static constexpr int BAR_OFF = (U_OFF + UB + 15) / 16 * 16;
     static constexpr int SMEM = BAR_OFF + 16;
@@ -451,33 +432,15 @@ QFT_DEV void a0_complex(const vec2<T> *src, vec2<T> *W, int ntr, int TTn, int ti
                 if (u < TTn * NC64 && tau < ntr) ch[r].template store<LOG2N>(W + tau * P::PADDED, c, lane, a0l64, shfl_up);
             }
         }
-        for (int it = tid; it < TTn * NC64; it += NT) {
-            const int tau = it / NC64, c = it - tau * NC64;
-            if (tau < ntr) a0_item<LOG2N, T>(src + tau * P::N, W + tau * P::PADDED, 64 * c);
+        if constexpr (!QFT_A0_LANE0) {
+            for (int it = tid; it < TTn * NC64; it += NT) {
+                const int tau = it / NC64, c = it - tau * NC64;
+                if (tau < ntr) a0_item<LOG2N, T>(src + tau * P::N, W + tau * P::PADDED, 64 * c);
+            }
         }
     } else {
         for (int tau = 0; tau < ntr; ++tau)
             for (int nn = tid; nn < P::m; nn += NT) a0_item<LOG2N, T>(src + tau * P::N, W + tau * P::PADDED, nn);
-    }
-}
-
-// A0 chunks c in [c0, c1) of one signal; forward samples from xf, mirrors below xm
-template <int LOG2N, typename T, int UNR>
-QFT_DEV void a0_chunks(const vec2<T> *xf, const vec2<T> *xm, int c0, int c1, vec2<T> *w, int warp, int lane, int NW,
-                       const A0Lane64 &a0l64) {
-    auto shfl_up = [](vec2<T> v) { return shfl_vec(v, false); };
-    for (int cb = c0 + warp; cb < c1; cb += NW * UNR) {
-        A0Chunk64<T> ch[UNR];
-#pragma unroll
-        for (int r = 0; r < UNR; ++r) {
-            const int c = cb + r * NW;
-            if (c < c1) ch[r].loadp(xf, xm, c, lane);
-        }
-#pragma unroll
-        for (int r = 0; r < UNR; ++r) {
-            const int c = cb + r * NW;
-            if (c < c1) ch[r].template store<LOG2N>(w, c, lane, a0l64, shfl_up);
-        }
     }
 }
 
@@ -502,7 +465,7 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
     const long long nbatch = (batch + TT - 1) / TT;
     const A0Lane64 a0l64 = a0_lane64<LOG2N>(lane);
     for (int i = tid; i < P::UCELLS; i += NT) U[i] = Ug[i];
-    if ((TMA || (K::HS && MODE == 0)) && tid == 0) mbar_init(bar, 1);
+    if (TMA && tid == 0) mbar_init(bar, 1);
     __syncthreads();
     long long bt = blockIdx.x;
     constexpr int TS = K::TS;
@@ -511,24 +474,16 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
         const long long nt = (batch - b * TT) < TT ? (batch - b * TT) : TT;
         return nt < TS ? nt : TS;
     };
-    constexpr bool HS = K::HS && MODE == 0;
-    constexpr uint32_t QB = (P::N / 4) * K::VB;  // one staged quarter
     if (TMA && tid == 0 && bt < nbatch)
         tma_bulk_load(stage, in + bt * TT * P::N, (uint32_t)(stage_count(bt) * P::N * K::VB), bar);
-    if (HS && tid == 0 && bt < nbatch)
-        tma_bulk_load2(stage, in + bt * P::N, QB, stage + P::N / 4, in + bt * P::N + 3 * P::N / 4, QB, bar);
     uint32_t parity = 0;
     for (; bt < nbatch; bt += gridDim.x) {
         const int ntr = (int)((batch - bt * TT) < TT ? (batch - bt * TT) : TT);
-        if constexpr (TMA || HS) {
+        if constexpr (TMA) {
             mbar_wait(bar, parity);
             parity ^= 1u;
         }
-        if (MODE == 0 && HS && tid == 0 && bt + gridDim.x < nbatch) {
-            // the unstaged middle half of the next signal -> L2
-            const long long nb = bt + gridDim.x;
-            l2_prefetch(in + nb * P::N + P::N / 4, 2 * QB);
-        } else if (MODE == 0 && TS < TT && tid == 0 && bt + gridDim.x < nbatch) {
+        if (MODE == 0 && TS < TT && tid == 0 && bt + gridDim.x < nbatch) {
             // pull the next batch's unstaged signals into L2 while this one is transformed
             const long long nb = bt + gridDim.x;
             const long long nt = (batch - nb * TT) < TT ? (batch - nb * TT) : TT;
@@ -544,15 +499,6 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
                 for (int nn = tid; nn <= P::m; nn += NT)
                     a0_item_real<LOG2N, T, MODE>(xr + ra * RL, xr + rb * RL, W + tau * P::PADDED, nn);
             }
-        } else if constexpr (HS) {
-            // TT = 1: chunks [NC/2, NC) from global memory (mirrors in the middle
-            // half), chunks [0, NC/2) from the staged quarters; multiples of 64
-            // (and the base pair) from global memory
-            constexpr int NC64 = P::m / 64;
-            const vec2<T> *xg = in + bt * P::N;
-            a0_chunks<LOG2N, T, QFT_A0_UNR / 2>(xg, xg + P::N, NC64 / 2, NC64, W, warp, lane, NW, a0l64);
-            a0_chunks<LOG2N, T, 2>(stage, stage + P::N / 2, 0, NC64 / 2, W, warp, lane, NW, a0l64);
-            for (int c = tid; c < NC64; c += NT) a0_item<LOG2N, T>(xg, W, 64 * c);
         } else {
             if constexpr (TS < TT) {
                 if (ntr > TS)
@@ -567,10 +513,6 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
         if (TMA && tid == 0 && bt + gridDim.x < nbatch) {
             const long long nb = bt + gridDim.x;
             tma_bulk_load(stage, in + nb * TT * P::N, (uint32_t)(stage_count(nb) * P::N * K::VB), bar);
-        }
-        if (HS && tid == 0 && bt + gridDim.x < nbatch) {
-            const long long nb = bt + gridDim.x;
-            tma_bulk_load2(stage, in + nb * P::N, QB, stage + P::N / 4, in + nb * P::N + 3 * P::N / 4, QB, bar);
         }
         // TF: top forward levels of the huge blocks (N > 4096; ends with a barrier)
         if constexpr (P::JH > 0) top_f<LOG2N, T, MODE>(W, U, ntr, tid);

@@ -25,6 +25,12 @@
 #pragma once
 #include "qft_lee.cuh"
 
+#ifndef QFT_A0_SPLIT
+#define QFT_A0_SPLIT 0  // A0 even-sample stores in two groups (block 1 / blocks >= 2)
+#endif
+#ifndef QFT_A0_LANE0
+#define QFT_A0_LANE0 0  // A0 chunk lane 0 also folds n = 64c (else a separate pass)
+#endif
 #ifndef QFT_RC_SMALL
 #define QFT_RC_SMALL 5  // phase-D unfold depth for N <= 2^12
 #endif
@@ -130,28 +136,53 @@ QFT_HD A0Lane64 a0_lane64(int l) {
 }
 template <typename T>
 struct A0Chunk64 {
-    vec2<T> xe, xo, mn, mo;
+    vec2<T> xe, xo, mn, mo, m0;
+    // lane 0 also loads the mirror x[N - 64c] of its even sample n = 64c
+    // (x[m] for c = 0: the base pair s(0), s(m))
     template <int LOG2N>
     QFT_HD void load(const vec2<T> *x, int c, int l) {
-        ld2(x + 64 * c + 2 * l, xe, xo);                          // x[n_e], x[n_o]
-        ld2(x + (1 << LOG2N) - 64 * c - 2 * l - 2, mn, mo);       // x[N - n_e - 2], x[N - n_o]
+        constexpr int N = 1 << LOG2N;
+        ld2(x + 64 * c + 2 * l, xe, xo);             // x[n_e], x[n_o]
+        ld2(x + N - 64 * c - 2 * l - 2, mn, mo);     // x[N - n_e - 2], x[N - n_o]
+        if (QFT_A0_LANE0 && l == 0) m0 = x[c ? N - 64 * c : N / 2];
     }
-    // xf: the forward samples x[0..), xm: one past the mirror end (x + N)
-    QFT_HD void loadp(const vec2<T> *xf, const vec2<T> *xm, int c, int l) {
-        ld2(xf + 64 * c + 2 * l, xe, xo);
-        ld2(xm - 64 * c - 2 * l - 2, mn, mo);
-    }
+    // Stores: the odd samples (block 0, 32 consecutive cells), then the even
+    // samples in two groups -- block 1 (odd lanes, 16 consecutive cells) and
+    // blocks >= 2 (with lane 0's n = 64c) -- so no store instruction mixes the
+    // block-1 run with the other blocks (bank conflicts).
     template <int LOG2N, class ShflUp>
     QFT_HD void store(vec2<T> *w, int c, int l, const A0Lane64 &a, ShflUp &&shfl_up) const {
-        constexpr int PS = padx(SPlan<LOG2N>::S0);
+        using P = SPlan<LOG2N>;
+        constexpr int PS = padx(P::S0);
         const vec2<T> me = shfl_up(mn);                  // x[N - n_e] from lane l-1
         const int po = 33 * c + l;                       // block 0 cell 32c + l, padded
         w[po] = vadd(xo, mo);
         w[po + PS] = vsub(xo, mo);
-        if (l) {
-            const int pe = a.A + c * a.B + (c >> a.sh);
+        const int pe = a.A + c * a.B + (c >> a.sh);
+#if QFT_A0_SPLIT
+        if (l & 1) {
             w[pe] = vadd(xe, me);
             w[pe + PS] = vsub(xe, me);
+        }
+#if defined(__CUDA_ARCH__)
+        __syncwarp();
+#endif
+        if (l > 0 && !(l & 1)) {
+#else
+        if (l > 0) {
+#endif
+            w[pe] = vadd(xe, me);
+            w[pe + PS] = vsub(xe, me);
+        } else if (QFT_A0_LANE0 && l == 0) {
+            if (c == 0) {
+                w[padx(P::BASE)] = xe;      // dc[0] = x[0]
+                w[padx(P::BASE + 1)] = m0;  // dc[m] = x[m]
+            } else {
+                const int n = 64 * c, j = ctz32((uint32_t)n);
+                const int cell = P::m - (1 << (LOG2N - 1 - j)) + (n >> (j + 1));
+                w[padx(cell)] = vadd(xe, m0);
+                w[padx(P::S0 + cell)] = vsub(xe, m0);
+            }
         }
     }
 };

@@ -137,7 +137,7 @@ static void emu_one(const vec2<T> *x, vec2<T> *y, const T *U) {
             };
             a0_chunk64<LOG2N, T>(x, w, c, l, a0_lane64<LOG2N>(l), shfl_up);
         }
-        a0_item<LOG2N, T>(x, w, 64 * c);
+        if (!QFT_A0_LANE0) a0_item<LOG2N, T>(x, w, 64 * c);  // else lane 0 of the chunk did n = 64c
     }
     emu_side<LOG2N, T, false>(w, U);
     emu_side<LOG2N, T, true>(w, U);
