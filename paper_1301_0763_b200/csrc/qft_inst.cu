@@ -2,7 +2,7 @@
 // Compiled once per instance with -DQFT_INST_PREC={32,64} -DQFT_INST_LOG2N={1..14}.
 // An instance whose working area does not fit in shared memory (fp64 N = 2^14)
 // reports cfg[0] = 0 and is served by the multi-pass path.
-#include "qft_launch.cuh"
+#include "qft_pipe.cuh"
 
 #if !defined(QFT_INST_PREC) || !defined(QFT_INST_LOG2N)
 #error "compile with -DQFT_INST_PREC=<32|64> -DQFT_INST_LOG2N=<1..14>"
@@ -30,6 +30,12 @@ void smem_cfg(int *cfg) {
         cfg[0] = K::SMEM;
         cfg[1] = K::NT;
         cfg[2] = K::TT;
+        if constexpr (qft::use_pipe<L, R>()) {  // the cdft path
+            using C = qft::PCfg<L, R>;
+            cfg[0] = C::SMEM;
+            cfg[1] = C::NT;
+            cfg[2] = C::TT;
+        }
     } else {
         cfg[0] = cfg[1] = cfg[2] = 0;
     }
@@ -38,7 +44,9 @@ template <int L, typename R>
 int smem_launch(const qft::LaunchArgs *a, int mode) {
     if constexpr (qft::smem_fits<L, R>()) {
         switch (mode) {
-            case 0: return (int)qft::launch_smem<L, R, 0>(*a);
+            case 0:
+                if constexpr (qft::use_pipe<L, R>()) return (int)qft::launch_pipe<L, R>(*a);
+                else return (int)qft::launch_smem<L, R, 0>(*a);
             case 1: return (int)qft::launch_smem<L, R, 1>(*a);
             case 2: return (int)qft::launch_smem<L, R, 2>(*a);
             case 3: return (int)qft::launch_smem<L, R, 3>(*a);

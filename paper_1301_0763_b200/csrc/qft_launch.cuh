@@ -30,8 +30,50 @@
 #ifndef QFT_NW_MIN
 #define QFT_NW_MIN 4       // lower bound on warps per CTA
 #endif
+#ifndef QFT_HALO_SHFL
+#define QFT_HALO_SHFL 0    // phase-C halo column by warp shuffle (else a second shared-memory read)
+#endif
 #ifndef QFT_TT_MAX
 #define QFT_TT_MAX 4       // cap on signals per CTA iteration
+#endif
+
+// Phase timestamps for tools/probe (compiled out unless QFT_PROBE is defined):
+// per (CTA, iteration < 16) 8 CTA-level marks (thread 0, after each barrier)
+// and one mark per warp when it leaves the fused-unit phase.
+#ifdef QFT_PROBE
+static __device__ long long qft_probe_buf[160 * 16 * 64];
+#define QFT_MARK(k)                                                                       \
+    do {                                                                                  \
+        const long long it_ = (bt - blockIdx.x) / gridDim.x;                              \
+        if (tid == 0 && blockIdx.x < 160 && it_ < 16) qft_probe_buf[(blockIdx.x * 16 + it_) * 64 + (k)] = clock64(); \
+    } while (0)
+#define QFT_WMARK()                                                                       \
+    do {                                                                                  \
+        const long long it_ = (bt - blockIdx.x) / gridDim.x;                              \
+        if (lane == 0 && blockIdx.x < 160 && it_ < 16) qft_probe_buf[(blockIdx.x * 16 + it_) * 64 + 8 + warp] = clock64(); \
+    } while (0)
+#define QFT_WMARK_AT(o)                                                                   \
+    do {                                                                                  \
+        const long long it_ = (bt - blockIdx.x) / gridDim.x;                              \
+        if (lane == 0 && blockIdx.x < 160 && it_ < 16) qft_probe_buf[(blockIdx.x * 16 + it_) * 64 + (o) + warp] = clock64(); \
+    } while (0)
+#define QFT_UMARK(k)                                                                      \
+    do {                                                                                  \
+        if (blockIdx.x == 0 && threadIdx.x == 0) qft_probe_buf[160 * 16 * 64 - 64 + (k)] = clock64(); \
+    } while (0)
+#else
+#define QFT_WMARK_AT(o) \
+    do {                \
+    } while (0)
+#define QFT_UMARK(k) \
+    do {             \
+    } while (0)
+#define QFT_MARK(k) \
+    do {            \
+    } while (0)
+#define QFT_WMARK() \
+    do {            \
+    } while (0)
 #endif
 
 namespace qft {
@@ -256,8 +298,14 @@ QFT_DEV void run_c_blockp(vec2<T> *wb, int lane) {
     CBlockP<R, DST, T> c;
     c.load(wb, lane);
     vec2<T> out[1 << R];
+#if QFT_HALO_SHFL
+    // the halo column is the neighbour lane's own column: a register shuffle
+    // (the edge lane's value is unused -- it copies instead of adding)
+    auto halo = [&](int p) { return shfl_vec(c.own[p], !DST); };
+#else
     const vec2<T> *hc = CBlockP<R, DST, T>::halo_colp(wb, lane);
     auto halo = [&](int p) { return hc[33 * p]; };  // read before the __syncwarp below
+#endif
     c.compute(lane, halo, out);
     __syncwarp();
     CBlockP<R, DST, T>::storep(wb, lane, out);
@@ -282,14 +330,19 @@ QFT_DEV void run_c_blocks(vec2<T> *w, bool dst, int lane) {
 // N <= 4096, a 1024-cell (sub-)block for N > 4096): one Lee-32 per lane
 template <int L, int R, typename T, bool DST, bool REV = false>
 QFT_DEV void unit_big(vec2<T> *wb, const T *U, const T *kcu, int lane) {
+    QFT_UMARK(0);
     FBlockP<L, R, DST, T> f;
     f.template load<REV>(wb, U, lane);
     __syncwarp();
+    QFT_UMARK(1);
     f.store(wb, lane);
     __syncwarp();
+    QFT_UMARK(2);
     if (lane < (1 << R)) b_l32p<DST, T>(wb + 33 * lane, kcu);
     __syncwarp();
+    QFT_UMARK(3);
     run_c_blockp<R, DST, T>(wb, lane);
+    QFT_UMARK(4);
 }
 // rest unit: blocks JR..JF-1, the L = 32 block and the blocks with L <= 16
 template <int LOG2N, typename T, bool DST>
@@ -479,10 +532,12 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
     uint32_t parity = 0;
     for (; bt < nbatch; bt += gridDim.x) {
         const int ntr = (int)((batch - bt * TT) < TT ? (batch - bt * TT) : TT);
+        QFT_MARK(0);
         if constexpr (TMA) {
             mbar_wait(bar, parity);
             parity ^= 1u;
         }
+        QFT_MARK(1);
         if (MODE == 0 && TS < TT && tid == 0 && bt + gridDim.x < nbatch) {
             // pull the next batch's unstaged signals into L2 while this one is transformed
             const long long nb = bt + gridDim.x;
@@ -509,6 +564,7 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
             if constexpr (TS > 0) a0_complex<LOG2N, T, 1>(stage, W, ntr < TS ? ntr : TS, TS, tid, NT, NW, a0l64);
         }
         __syncthreads();
+        QFT_MARK(2);
         // the staging buffer is free: prefetch the next batch while we compute
         if (TMA && tid == 0 && bt + gridDim.x < nbatch) {
             const long long nb = bt + gridDim.x;
@@ -518,7 +574,9 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
         if constexpr (P::JH > 0) top_f<LOG2N, T, MODE>(W, U, ntr, tid);
         // A+B+C fused: one warp per (signal, side, unit) -- no CTA barrier inside
         fused_units<LOG2N, T, MODE, TT, NW>(W, U, kc.u, ntr, warp, lane);
+        QFT_WMARK();
         __syncthreads();
+        QFT_MARK(3);
         // TB: top backward levels of the huge blocks (ends with a barrier)
         if constexpr (P::JH > 0) top_b<LOG2N, T, MODE>(W, ntr, tid);
         // D: chain + recombination -> global
@@ -560,7 +618,9 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
                 else Chain<LOG2N, T>::unit_e(W + tau * P::PADDED, emit, t);
             }
         }
+        QFT_MARK(4);
         __syncthreads();
+        QFT_MARK(5);
     }
 }
 

@@ -1,0 +1,228 @@
+// qft_pipe.cuh -- software-pipelined single-pass kernel (complex cdft, N <= 4096).
+//
+// Same phases and the same per-cell arithmetic as qft_cdft_smem (qft_launch.cuh),
+// scheduled so that the latency-bound chain phase D of batch i overlaps the
+// fold/route phase A0 of batch i+1 on other warps:
+//
+//   two buffer sets X[0], X[1] of TT signal slots each (a slot is one padded
+//   working area, PADDED cells >= N, so the raw signal fits in it);
+//   TMA bulk-loads the raw signals of batch i into set i&1;
+//   A0 runs IN PLACE in the slot: a warp group loads the raw samples into
+//   registers, synchronises on a named barrier, then stores the folded cells
+//   (the loads of a slot all precede its stores);
+//
+//   per batch i:   units(i) on X[i&1]                      all warps
+//                  __syncthreads
+//                  D(i) from X[i&1] -> y                   warps [0, NWD)
+//                  | wait TMA(i+1), A0(i+1) in X[(i+1)&1]  warps [NWD, NWD+NWA)
+//                  __syncthreads
+//                  TMA(i+2) -> X[i&1]                      thread 0
+//
+// The probe (tools/probe) measured D at ~30 % of the unpipelined iteration with
+// only half the warps busy; here those idle warps fold the next batch.
+#pragma once
+#include "qft_launch.cuh"
+
+#ifndef QFT_PIPE
+#define QFT_PIPE 1  // serve fp32 N = 4096 cdft with the pipelined kernel
+#endif
+#ifndef QFT_PIPE_NWA
+#define QFT_PIPE_NWA 5  // warps running the in-place A0 of the next batch during D
+#endif
+
+namespace qft {
+
+template <int LOG2N, typename T>
+struct PCfg {
+    using P = SPlan<LOG2N>;
+    static constexpr int VB = (int)sizeof(vec2<T>);
+    static constexpr int UB = P::UCELLS * (int)sizeof(T);
+    static constexpr int BUDGET = 226 * 1024 - UB - 64;
+    static constexpr int PER_W = P::PADDED * VB;  // slot: padded working area (>= N cells)
+    static constexpr int TT0 = BUDGET / (2 * PER_W);
+    static constexpr int TTC = P::n >= 12 ? QFT_TT_MAX : 64;
+    static constexpr int TT = TT0 > TTC ? TTC : TT0;
+    static constexpr bool FITS = TT >= 1 && P::m >= 64 && PER_W % 16 == 0;  // TMA slots 16-byte aligned
+    static constexpr int mx(int a, int b) { return a > b ? a : b; }
+    static constexpr int NU = 2 * (P::NU1 + 1);
+    static constexpr int W_U = (TT > 0 ? TT : 1) * NU;
+    static constexpr int DI = P::DT;
+    static constexpr int NWD = ((TT > 0 ? TT : 1) * DI + 31) / 32;  // D warps
+    static constexpr int NWA = QFT_PIPE_NWA;                         // A0 warps
+    static constexpr int NW = mx(W_U, NWD + NWA);
+    static constexpr int NT = NW * 32;
+    static constexpr int NC64 = P::m / 64;  // A0 chunks per signal
+    static constexpr int RA = (NC64 + NWA - 1) / NWA;
+    static constexpr int X_OFF = 0;
+    static constexpr int U_OFF = 2 * (TT > 0 ? TT : 1) * PER_W;
+    static constexpr int BAR_OFF = (U_OFF + UB + 15) / 16 * 16;
+    static constexpr int SMEM = BAR_OFF + 32;
+};
+
+template <int LOG2N, typename T>
+constexpr bool pipe_fits() {
+    return PCfg<LOG2N, T>::FITS && PCfg<LOG2N, T>::SMEM <= 227 * 1024 && PCfg<LOG2N, T>::NW <= 16;
+}
+
+// (LOG2N, T) instances served by the pipelined kernel (mode 0)
+template <int LOG2N, typename T>
+constexpr bool use_pipe() {
+    return QFT_PIPE && pipe_fits<LOG2N, T>() && LOG2N == 12 && sizeof(T) == 4;
+}
+
+QFT_DEV void named_bar(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
+
+// one thread: arm bar with the bytes of ntr signals and bulk-copy each raw
+// signal (N cells) into its slot
+template <int LOG2N, typename T>
+QFT_DEV void tma_load_slots(vec2<T> *X, const vec2<T> *src, int ntr, uint64_t *bar) {
+    using P = SPlan<LOG2N>;
+    constexpr uint32_t BYTES = P::N * (uint32_t)sizeof(vec2<T>);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(BYTES * ntr)
+                 : "memory");
+    for (int tau = 0; tau < ntr; ++tau)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(X + tau * P::PADDED)),
+                     "l"(src + (long long)tau * P::N), "r"(BYTES), "r"(smem_u32(bar))
+                     : "memory");
+}
+
+// In-place A0 of ntr signals (raw samples at the start of each slot) by the
+// NWA-warp group; ga = thread index within the group.  Per signal: every load
+// (chunks of 64 samples + the items n = 64c) into registers, named barrier,
+// every store (same fold / route as a0_complex).
+template <int LOG2N, typename T>
+QFT_DEV void a0_inplace(vec2<T> *X, int ntr, int ga, const A0Lane64 &a0l64) {
+    using P = SPlan<LOG2N>;
+    using C = PCfg<LOG2N, T>;
+    constexpr int NWA = C::NWA, NC64 = C::NC64, RA = C::RA;
+    const int lane = ga & 31, gw = ga >> 5;
+    auto shfl_up = [](vec2<T> v) { return shfl_vec(v, false); };
+    for (int tau = 0; tau < ntr; ++tau) {
+        vec2<T> *s = X + tau * P::PADDED;
+        A0Chunk64<T> ch[RA];
+#pragma unroll
+        for (int r = 0; r < RA; ++r) {
+            const int c = gw + r * NWA;
+            if (c < NC64) ch[r].template load<LOG2N>(s, c, lane);
+        }
+        const bool item = ga < NC64;  // n = 64 ga (ga = 0: the base pair)
+        vec2<T> ia, ib;
+        if (item) {
+            ia = s[64 * ga];
+            ib = s[ga == 0 ? P::m : P::N - 64 * ga];
+        }
+        named_bar(1, NWA * 32);
+#pragma unroll
+        for (int r = 0; r < RA; ++r) {
+            const int c = gw + r * NWA;  // warp-uniform: the store's shuffle sees the whole warp
+            if (c < NC64) ch[r].template store<LOG2N>(s, c, lane, a0l64, shfl_up);
+        }
+        if (item) {
+            if (ga == 0) {
+                s[padx(P::BASE)] = ia;      // dc[0] = x[0]
+                s[padx(P::BASE + 1)] = ib;  // dc[m] = x[m]
+            } else {
+                const int n = 64 * ga, j = ctz32((uint32_t)n);
+                const int cell = P::m - (1 << (LOG2N - 1 - j)) + (n >> (j + 1));
+                s[padx(cell)] = vadd(ia, ib);
+                s[padx(P::S0 + cell)] = vsub(ia, ib);
+            }
+        }
+        // the next signal's loads read another slot: no barrier needed here
+    }
+}
+
+template <int LOG2N, typename T>
+__global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
+    qft_cdft_pipe(const vec2<T> *__restrict__ in, vec2<T> *__restrict__ out, long long batch, const T *__restrict__ Ug,
+                  const __grid_constant__ LeeConst<T> kc) {
+    using P = SPlan<LOG2N>;
+    using C = PCfg<LOG2N, T>;
+    constexpr int TT = C::TT, NT = C::NT, NW = C::NW, NWD = C::NWD, NWA = C::NWA;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    vec2<T> *X0 = reinterpret_cast<vec2<T> *>(smem_raw + C::X_OFF);
+    T *U = reinterpret_cast<T *>(smem_raw + C::U_OFF);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::BAR_OFF);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool a0_warp = warp >= NWD && warp < NWD + NWA;
+    const int ga = tid - NWD * 32;
+    const A0Lane64 a0l64 = a0_lane64<LOG2N>(lane);
+    const long long nbatch = (batch + TT - 1) / TT, G = gridDim.x;
+    auto ntr_of = [&](long long b) { return (int)((batch - b * TT) < TT ? (batch - b * TT) : TT); };
+    auto set = [&](int s) { return X0 + s * TT * P::PADDED; };
+
+    for (int i = tid; i < P::UCELLS; i += NT) U[i] = Ug[i];
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+    }
+    __syncthreads();
+    long long bt = blockIdx.x;
+    if (bt >= nbatch) return;
+    if (tid == 0) {
+        tma_load_slots<LOG2N, T>(set(0), in + bt * TT * P::N, ntr_of(bt), &bar[0]);
+        if (bt + G < nbatch) tma_load_slots<LOG2N, T>(set(1), in + (bt + G) * TT * P::N, ntr_of(bt + G), &bar[1]);
+    }
+    uint32_t ph0 = 0, ph1 = 0;
+    // prologue: A0 of the first batch
+    if (a0_warp) {
+        mbar_wait(&bar[0], ph0);
+        a0_inplace<LOG2N, T>(set(0), ntr_of(bt), ga, a0l64);
+    }
+    ph0 ^= 1u;
+    __syncthreads();
+    int cur = 0;
+    for (; bt < nbatch; bt += G) {
+        const int ntr = ntr_of(bt);
+        vec2<T> *W = set(cur);
+        QFT_MARK(1);
+        QFT_WMARK_AT(24);
+        fused_units<LOG2N, T, 0, TT, NW>(W, U, kc.u, ntr, warp, lane);
+        QFT_WMARK();
+        __syncthreads();
+        QFT_MARK(3);
+        if (warp < NWD) {
+            for (int it = tid; it < TT * P::DT; it += NWD * 32) {
+                const int tau = it / P::DT, ti = it - tau * P::DT;
+                if (tau < ntr) Chain<LOG2N, T>::unit(W + tau * P::PADDED, out + (bt * TT + tau) * P::N, ti);
+            }
+        } else if (a0_warp && bt + G < nbatch) {
+            uint32_t &ph = cur ? ph0 : ph1;  // the next batch sits in set cur^1
+            mbar_wait(&bar[cur ^ 1], ph);
+            a0_inplace<LOG2N, T>(set(cur ^ 1), ntr_of(bt + G), ga, a0l64);
+        }
+        if (bt + G < nbatch) {
+            if (cur) ph0 ^= 1u;
+            else ph1 ^= 1u;
+        }
+        QFT_MARK(4);
+        __syncthreads();
+        QFT_MARK(5);
+        // set cur is free: bring in batch bt + 2G
+        if (tid == 0 && bt + 2 * G < nbatch)
+            tma_load_slots<LOG2N, T>(W, in + (bt + 2 * G) * TT * P::N, ntr_of(bt + 2 * G), &bar[cur]);
+        QFT_MARK(6);
+        cur ^= 1;
+    }
+}
+
+template <int LOG2N, typename T>
+cudaError_t launch_pipe(const LaunchArgs &a) {
+    using C = PCfg<LOG2N, T>;
+    auto kern = qft_cdft_pipe<LOG2N, T>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    const long long nbatch = (a.batch + C::TT - 1) / C::TT;
+    long long grid = a.num_sms;
+    if (grid > nbatch) grid = nbatch;
+    if (grid < 1) grid = 1;
+    LeeConst<T> kc;
+    for (int i = 0; i < 32; ++i) kc.u[i] = ((const T *)a.Uhead)[i];
+    kern<<<(unsigned)grid, C::NT, C::SMEM, a.stream>>>((const vec2<T> *)a.in, (vec2<T> *)a.out, a.batch, (const T *)a.U,
+                                                       kc);
+    return cudaGetLastError();
+}
+
+}  // namespace qft

@@ -1,0 +1,132 @@
+// Phase-timeline probe of qft_cdft_smem (tools only, not shipped): compiles the
+// kernel with QFT_PROBE so thread 0 of every CTA records clock64() at each
+// phase barrier, runs the config-2 (or -DPLOG2N=k) workload on random data and
+// prints the median cycles per phase.  Build + run: tools/probe/run_probe.sh
+#define QFT_PROBE 1
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <algorithm>
+#include <cstring>
+#include "../../paper_1301_0763_b200/csrc/qft_pipe.cuh"
+
+// qft_probe_buf is defined by qft_launch.cuh under QFT_PROBE
+
+#ifndef PLOG2N
+#define PLOG2N 12
+#endif
+
+int main(int argc, char **argv) {
+    constexpr int LOG2N = PLOG2N, N = 1 << LOG2N;
+    long long batch = argc > 1 ? atoll(argv[1]) : (LOG2N == 12 ? 16384 : 262144 / 4);
+#ifdef PIPE
+    using K = qft::PCfg<LOG2N, float>;
+#define LAUNCH qft::launch_pipe<LOG2N, float>
+#else
+    using K = qft::KCfg<LOG2N, float>;
+#define LAUNCH qft::launch_smem<LOG2N, float, 0>
+#endif
+    printf("N=2^%d batch=%lld TT=%d NW=%d SMEM=%d\n", LOG2N, batch, K::TT, K::NW, K::SMEM);
+    size_t bytes = (size_t)batch * N * 8;
+    float *in, *out, *U;
+    cudaMalloc(&in, bytes);
+    cudaMalloc(&out, bytes);
+    cudaMalloc(&U, N / 4 * 4);
+    std::vector<float> h(N / 4, 0.5f), hin(1 << 20);
+    for (auto &v : hin) v = (float)rand() / RAND_MAX - 0.5f;
+    for (size_t o = 0; o < bytes / 4; o += hin.size()) cudaMemcpy(in + o, hin.data(), std::min(hin.size(), bytes / 4 - o) * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(U, h.data(), N, cudaMemcpyHostToDevice);
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    qft::LaunchArgs a{in, out, batch, U, h.data(), sms, 0};
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int i = 0; i < 3; ++i) LAUNCH(a);
+    cudaEventRecord(e0);
+    const int REP = 10;
+    for (int i = 0; i < REP; ++i) LAUNCH(a);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= REP;
+    printf("kernel %.3f ms  %.2f M tr/s  %.1f GB/s  err=%s\n", ms, batch / ms / 1e3, batch * N * 16.0 / ms / 1e6,
+           cudaGetErrorString(cudaGetLastError()));
+    std::vector<long long> b(160 * 16 * 64);
+    cudaMemcpyFromSymbol(b.data(), qft_probe_buf, b.size() * 8);
+#ifdef PIPE
+    {   // bitwise check against the unpipelined kernel on the same input
+        float *out2;
+        cudaMalloc(&out2, bytes);
+        qft::LaunchArgs a2{in, out2, batch, U, h.data(), sms, 0};
+        qft::launch_smem<LOG2N, float, 0>(a2);
+        std::vector<float> r1(bytes / 4), r2(bytes / 4);
+        cudaMemcpy(r1.data(), out, bytes, cudaMemcpyDeviceToHost);
+        cudaMemcpy(r2.data(), out2, bytes, cudaMemcpyDeviceToHost);
+        size_t bad = 0;
+        for (size_t i = 0; i < r1.size(); ++i) bad += memcmp(&r1[i], &r2[i], 4) != 0;
+        printf("bitwise vs qft_cdft_smem: %zu differing words of %zu\n", bad, r1.size());
+        cudaFree(out2);
+    }
+#endif
+
+    // per-phase durations over CTAs < sms, iterations 2..13
+#ifdef PIPE
+    // pipe marks: 1 start, 3 after units, 4 D done (thread 0), 5 after phase-2 barrier
+    for (int c = 0; c < sms; ++c)
+        for (int it = 0; it < 16; ++it) {
+            long long *m = &b[(c * 16 + it) * 64];
+            m[0] = m[1];
+            m[2] = m[1];
+        }
+    const char *names[] = {"-", "-", "units", "D(thr0)", "A0_extra", "loop"};
+    for (int c = 0; c < sms; ++c)
+        for (int it = 0; it < 15; ++it) b[(c * 16 + it) * 64 + 0] = b[(c * 16 + it) * 64 + 0];
+#else
+    const char *names[] = {"tma_wait", "A0", "units", "D(thr0)", "D_bar", "loop"};
+#endif
+    std::vector<double> ph[6], wspread, wmin;
+    for (int c = 0; c < sms; ++c)
+        for (int it = 2; it < 14; ++it) {
+            long long *m = &b[(c * 16 + it) * 64], *mn = &b[(c * 16 + it + 1) * 64];
+            ph[0].push_back(m[1] - m[0]);
+            ph[1].push_back(m[2] - m[1]);
+            ph[2].push_back(m[3] - m[2]);
+            ph[3].push_back(m[4] - m[3]);
+            ph[4].push_back(m[5] - m[4]);
+#ifdef PIPE
+            ph[5].push_back(mn[1] - m[5]);
+#else
+            ph[5].push_back(mn[0] - m[5]);
+#endif
+            long long lo = 1LL << 62, hi = 0;
+            for (int w = 0; w < K::NW; ++w) {
+                lo = std::min(lo, m[8 + w] - m[2]);
+                hi = std::max(hi, m[8 + w] - m[2]);
+            }
+            wmin.push_back(lo);
+            wspread.push_back(hi);
+        }
+    auto med = [](std::vector<double> v) {
+        std::sort(v.begin(), v.end());
+        return v[v.size() / 2];
+    };
+    double tot = 0;
+    for (int k = 0; k < 6; ++k) tot += med(ph[k]);
+    for (int k = 0; k < 6; ++k) printf("  %-9s %7.0f cycles (%4.1f%%)\n", names[k], med(ph[k]), 100 * med(ph[k]) / tot);
+    printf("  iteration %7.0f cycles = %.0f per transform; units: first warp done %.0f, last %.0f\n", tot, tot / K::TT,
+           med(wmin), med(wspread));
+    long long *u = &b[160 * 16 * 64 - 64];
+    {
+        long long *m = &b[(0 * 16 + 14) * 64];
+        printf("  CTA 0 iteration 15: start %lld, unit start +%lld, units barrier +%lld\n", m[1], u[0] - m[1], m[3] - m[1]);
+        printf("  m5 -> after TMA issue %lld -> m1(next) %lld\n", m[6] - m[5], (m + 64)[1] - m[5]);
+        printf("  per-warp units start/end:");
+        for (int w = 0; w < K::NW; ++w) printf(" %lld/%lld", m[24 + w] - m[1], m[8 + w] - m[1]);
+        printf("\n");
+    }
+    printf("  unit_big (CTA 0 warp 0, last iteration): F load+fold %lld, F store %lld, Lee-32 %lld, C %lld cycles\n",
+           u[1] - u[0], u[2] - u[1], u[3] - u[2], u[4] - u[3]);
+    return 0;
+}
