@@ -56,11 +56,14 @@ def _compile(src, obj, defines):
     return obj
 
 
-def build(jobs=None, verbose=True, defines=(), lib=None):
+def build(jobs=None, verbose=True, defines=(), lib=None, only=None):
     """Compile all translation units (cached) and link libqftb200.so.
-    ``defines``/``lib``: build an experimental variant (e.g. QFT_CTAS_PER_SM=3)."""
+    ``defines``/``lib``: build an experimental variant (e.g. QFT_CTAS_PER_SM=3);
+    ``only``: instance tags ("32_12", ...) that get the defines -- every other
+    translation unit is the default build's object."""
     os.makedirs(BUILD, exist_ok=True)
-    dig = _headers_digest() + ("_" + hashlib.sha256(" ".join(defines).encode()).hexdigest()[:8] if defines else "")
+    dig0 = _headers_digest()
+    dig = dig0 + ("_" + hashlib.sha256(" ".join(defines).encode()).hexdigest()[:8] if defines else "")
     target = lib or LIB
     units = [(os.path.join(CSRC, "qft_capi.cu"), os.path.join(BUILD, f"capi_{dig}.o"), list(defines))]
     for p in PRECS:
@@ -70,8 +73,12 @@ def build(jobs=None, verbose=True, defines=(), lib=None):
                       [f"QFT_CL_PREC={p}"] + list(defines)))
     for p in PRECS:
         for l in LOG2NS:
-            units.append((os.path.join(CSRC, "qft_inst.cu"), os.path.join(BUILD, f"inst_{p}_{l}_{dig}.o"),
-                          [f"QFT_INST_PREC={p}", f"QFT_INST_LOG2N={l}"] + list(defines)))
+            d = dig if only is None or f"{p}_{l}" in only else dig0
+            units.append((os.path.join(CSRC, "qft_inst.cu"), os.path.join(BUILD, f"inst_{p}_{l}_{d}.o"),
+                          [f"QFT_INST_PREC={p}", f"QFT_INST_LOG2N={l}"] + (list(defines) if d == dig else [])))
+    if only is not None:  # the shared units stay the default build's
+        units = [(u[0], u[1].replace(dig, dig0), [x for x in u[2] if x not in defines]) if "inst_" not in u[1] else u
+                 for u in units]
     todo = [u for u in units if not os.path.exists(u[1])]
     if todo:
         jobs = jobs or max(2, os.cpu_count() or 2)
@@ -122,7 +129,9 @@ def ptxas_report():
 
 if __name__ == "__main__":
     # python -m paper_1301_0763_b200.build [out.so DEFINE=VAL ...]
+    # QFT_ONLY=32_12,32_14 restricts the defines to those instances
     if len(sys.argv) > 1:
-        build(lib=os.path.abspath(sys.argv[1]), defines=tuple(sys.argv[2:]))
+        only = os.environ.get("QFT_ONLY")
+        build(lib=os.path.abspath(sys.argv[1]), defines=tuple(sys.argv[2:]), only=only.split(",") if only else None)
     else:
         build()

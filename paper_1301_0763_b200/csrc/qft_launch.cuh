@@ -33,6 +33,9 @@
 #ifndef QFT_HALO_SHFL
 #define QFT_HALO_SHFL 0    // phase-C halo column by warp shuffle (else a second shared-memory read)
 #endif
+#ifndef QFT_REST_FUSED
+#define QFT_REST_FUSED 0   // rest unit: F / C levels of all its blocks together (measured slower: 54.0 vs 55.5M tr/s)
+#endif
 #ifndef QFT_TT_MAX
 #define QFT_TT_MAX 4       // cap on signals per CTA iteration
 #endif
@@ -344,18 +347,83 @@ QFT_DEV void unit_big(vec2<T> *wb, const T *U, const T *kcu, int lane) {
     run_c_blockp<R, DST, T>(wb, lane);
     QFT_UMARK(4);
 }
-// rest unit: blocks JR..JF-1, the L = 32 block and the blocks with L <= 16
+// rest unit: blocks JR..JF-1, the L = 32 block and the blocks with L <= 16.
+// QFT_REST_FUSED: the F levels of every block JR..JF-1 are loaded / folded
+// together (one __syncwarp before their stores), and likewise the C levels,
+// instead of block after block (more independent work per warp).
+template <int LOG2N, typename T, bool DST, int J, bool = (J < SPlan<LOG2N>::JF)>
+struct FRest {
+    QFT_DEV void load(const vec2<T> *, const T *, int) {}
+    QFT_DEV void store(vec2<T> *, int) const {}
+};
+template <int LOG2N, typename T, bool DST, int J>
+struct FRest<LOG2N, T, DST, J, true> {
+    FBlock<LOG2N, J, DST, T> f;
+    FRest<LOG2N, T, DST, J + 1> next;
+    QFT_DEV void load(const vec2<T> *w, const T *U, int lane) {
+        f.load(w, U, lane);
+        next.load(w, U, lane);
+    }
+    QFT_DEV void store(vec2<T> *w, int lane) const {
+        f.store(w, lane);
+        next.store(w, lane);
+    }
+};
+template <int LOG2N, typename T, bool DST, int J, bool = (J < SPlan<LOG2N>::JF)>
+struct CRest {
+    QFT_DEV void compute(const vec2<T> *, int) {}
+    QFT_DEV void store(vec2<T> *, int) const {}
+};
+template <int LOG2N, typename T, bool DST, int J>
+struct CRest<LOG2N, T, DST, J, true> {
+    using P = SPlan<LOG2N>;
+    static constexpr int R = P::RF(J), base = (DST ? P::S0 : 0) + P::off(J);
+    vec2<T> out[1 << R];
+    CRest<LOG2N, T, DST, J + 1> next;
+    QFT_DEV void compute(const vec2<T> *w, int lane) {
+        const vec2<T> *wb = w + padx(base);
+        CBlockP<R, DST, T> c;
+        c.load(wb, lane);
+        const vec2<T> *hc = CBlockP<R, DST, T>::halo_colp(wb, lane);
+        auto halo = [&](int p) { return hc[33 * p]; };
+        c.compute(lane, halo, out);
+        next.compute(w, lane);
+    }
+    QFT_DEV void store(vec2<T> *w, int lane) const {
+        CBlockP<R, DST, T>::storep(w + padx(base), lane, out);
+        next.store(w, lane);
+    }
+};
 template <int LOG2N, typename T, bool DST>
 QFT_DEV void unit_rest(vec2<T> *w, const T *U, const T *kcu, int lane) {
     using P = SPlan<LOG2N>;
     constexpr int sb = DST ? P::S0 : 0;
     constexpr int CNT = P::NL32 - P::K0;
+#if QFT_REST_FUSED
+    {
+        FRest<LOG2N, T, DST, P::JR> fr;
+        fr.load(w, U, lane);
+        __syncwarp();
+        fr.store(w, lane);
+    }
+#else
     run_f_blocks<LOG2N, T, P::JR>(w, U, DST, lane);
+#endif
     __syncwarp();
     if (lane < CNT) b_l32<DST, T>(w, sb + 32 * (P::K0 + lane), kcu);
     else if (lane == CNT) b_small<LOG2N, DST, T>(w, kcu);
     __syncwarp();
+#if QFT_REST_FUSED
+    {
+        CRest<LOG2N, T, DST, P::JR> cr;
+        cr.compute(w, lane);
+        __syncwarp();
+        cr.store(w, lane);
+        __syncwarp();
+    }
+#else
     run_c_blocks<LOG2N, T, P::JR>(w, DST, lane);
+#endif
 }
 
 // ---- top levels of the huge blocks (N > 4096), whole CTA.  For one signal at

@@ -72,20 +72,26 @@ constexpr bool use_pipe() {
 
 QFT_DEV void named_bar(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
 
-// one thread: arm bar with the bytes of ntr signals and bulk-copy each raw
-// signal (N cells) into its slot
+// one warp: lane 0 arms bar with the bytes of ntr signals, then lane tau
+// bulk-copies raw signal tau (N cells) into its slot (the copies issue in
+// parallel; each issuing lane first orders the CTA's earlier generic accesses
+// of the slots -- published to it by the preceding barrier -- before its
+// async-proxy writes)
 template <int LOG2N, typename T>
-QFT_DEV void tma_load_slots(vec2<T> *X, const vec2<T> *src, int ntr, uint64_t *bar) {
+QFT_DEV void tma_load_slots(vec2<T> *X, const vec2<T> *src, int ntr, uint64_t *bar, int lane) {
     using P = SPlan<LOG2N>;
     constexpr uint32_t BYTES = P::N * (uint32_t)sizeof(vec2<T>);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(BYTES * ntr)
-                 : "memory");
-    for (int tau = 0; tau < ntr; ++tau)
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         smem_u32(X + tau * P::PADDED)),
-                     "l"(src + (long long)tau * P::N), "r"(BYTES), "r"(smem_u32(bar))
+    if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(BYTES * ntr)
                      : "memory");
+    __syncwarp();
+    if (lane < ntr) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(X + lane * P::PADDED)),
+                     "l"(src + (long long)lane * P::N), "r"(BYTES), "r"(smem_u32(bar))
+                     : "memory");
+    }
 }
 
 // In-place A0 of ntr signals (raw samples at the start of each slot) by the
@@ -161,9 +167,9 @@ __global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
     __syncthreads();
     long long bt = blockIdx.x;
     if (bt >= nbatch) return;
-    if (tid == 0) {
-        tma_load_slots<LOG2N, T>(set(0), in + bt * TT * P::N, ntr_of(bt), &bar[0]);
-        if (bt + G < nbatch) tma_load_slots<LOG2N, T>(set(1), in + (bt + G) * TT * P::N, ntr_of(bt + G), &bar[1]);
+    if (warp == 0) {
+        tma_load_slots<LOG2N, T>(set(0), in + bt * TT * P::N, ntr_of(bt), &bar[0], lane);
+        if (bt + G < nbatch) tma_load_slots<LOG2N, T>(set(1), in + (bt + G) * TT * P::N, ntr_of(bt + G), &bar[1], lane);
     }
     uint32_t ph0 = 0, ph1 = 0;
     // prologue: A0 of the first batch
@@ -201,8 +207,8 @@ __global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
         __syncthreads();
         QFT_MARK(5);
         // set cur is free: bring in batch bt + 2G
-        if (tid == 0 && bt + 2 * G < nbatch)
-            tma_load_slots<LOG2N, T>(W, in + (bt + 2 * G) * TT * P::N, ntr_of(bt + 2 * G), &bar[cur]);
+        if (warp == 0 && bt + 2 * G < nbatch)
+            tma_load_slots<LOG2N, T>(W, in + (bt + 2 * G) * TT * P::N, ntr_of(bt + 2 * G), &bar[cur], lane);
         QFT_MARK(6);
         cur ^= 1;
     }
