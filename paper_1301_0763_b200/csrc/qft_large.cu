@@ -73,7 +73,13 @@ struct QFT_LG(LargePlan) {
     QFT_LG(LargePlan)(int log2n, bool real_modes)
         : sublog(sublog_for(log2n)),
           J0(log2n - sublog_for(log2n)),
-          s(log2n, sublog_for(log2n), kRG, J0, true, !real_modes) {}
+          s(log2n, sublog_for(log2n), kRG, J0, real_modes || !fold_on_load(log2n), !real_modes) {}
+    // fold_on_load: the complex plan has no fold pass -- whole-block leaves fold x
+    // while loading (tf_load_x) and the sub-signal folds x[k 2^J0] while loading
+    // (sub_item).  Those gathers read every sector of x several times from L2, so
+    // this only pays where the fold pass is a large share of the step: measured
+    // +3.7 % at fp32 N = 2^16 (config 3), -4 % at fp64 N = 2^20 (config 4).
+    static bool fold_on_load(int log2n) { return QFT_LARGE_PREC == 32 && log2n - sublog_for(log2n) <= 2; }
 };
 
 template <typename TT>
@@ -282,7 +288,8 @@ QFT_DEV int item_runs(const Item &it, const LeafTask *tasks, int N, long long *l
 
 // Leaf item: K leaves of 2^A cells from W0 runs -> their spectra along the runs.
 template <int A, typename T, int NT, int NW>
-QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const T *kcu, vec2<T> *wb, int tid) {
+QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const T *kcu, vec2<T> *wb, int tid,
+                       const vec2<T> *xb, int N) {
     constexpr int L = 1 << A;
     const int warp = tid >> 5, lane = tid & 31;
     // load: async cell copies along the (forward or reversed) runs; with NT a
@@ -291,6 +298,7 @@ QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const
     constexpr bool LIN = (L % NT) == 0 && (NT % 32) == 0;
     for (int k = 0; k < K; ++k) {
         const LeafTask tk = tks[k];
+        if (tk.j >= 0) continue;  // whole Lee block j: TF reads (and folds) x directly
         vec2<T> *s = S + padx(k * L);
         const vec2<T> *src = wb + tk.c;
         if constexpr (LIN) {
@@ -315,8 +323,14 @@ QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const
             if (it < K * 1024) {
                 const int k = it >> 10, t = it & 1023;
                 const vec2<T> *s = S + padx(k * L);
-                if (tks[k].dst) LeafTop<A, true, T>::tf_load(s, U, t, v[r]);
-                else LeafTop<A, false, T>::tf_load(s, U, t, v[r]);
+                const int j = tks[k].j;
+                if (j >= 0) {
+                    if (tks[k].dst) LeafTop<A, true, T>::tf_load_x(xb, N, j, U, t, v[r]);
+                    else LeafTop<A, false, T>::tf_load_x(xb, N, j, U, t, v[r]);
+                } else {
+                    if (tks[k].dst) LeafTop<A, true, T>::tf_load(s, U, t, v[r]);
+                    else LeafTop<A, false, T>::tf_load(s, U, t, v[r]);
+                }
             }
         }
         __syncthreads();
@@ -386,14 +400,35 @@ QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const
 
 template <int SUBLOG, typename T>
 QFT_DEV void sub_item(const vec2<T> *w0b, int m, vec2<T> *W, const T *U, const T *kcu, vec2<T> *cbuf, vec2<T> *sbuf,
-                      int tid) {
+                      int tid, const vec2<T> *xb) {
     using P = SPlan<SUBLOG>;
     using C = ItemCfg<SUBLOG, T>;
     constexpr int NT = C::NT, NW = C::NW;
     const int warp = tid >> 5, lane = tid & 31;
-    // the folded blocks j >= J0 are contiguous in W0: cosine cells [m - m', m-1),
-    // sine cells [N - m', N-1), base pair N-1, N  ->  the sub-signal's layout
-    {
+    if (xb) {
+        // no fold pass: the sub-signal s[k] = x[k 2^J0] folded and routed while
+        // loading -- the big signal's fold x[n] +- x[N-n] at n = k 2^J0 is the
+        // sub-signal's fold s[k] +- s[N'-k] (shared.py:28-35, a0_item)
+        const int J0 = __ffs(m) - SUBLOG;  // m = 2^(n-1), m' = 2^(SUBLOG-1)
+#pragma unroll 8
+        for (int r = 0; r < (P::m + NT - 1) / NT; ++r) {
+            const int k = tid + r * NT;
+            if (k < P::m) {
+                const vec2<T> a = xb[k << J0], b = xb[k ? 2 * m - (k << J0) : m];
+                if (k == 0) {
+                    W[padx(P::BASE)] = a;      // s(0) = x[0]
+                    W[padx(P::BASE + 1)] = b;  // s(m') = x[m]
+                } else {
+                    const int jj = ctz32((uint32_t)k);
+                    const int cell = P::m - (1 << (SUBLOG - 1 - jj)) + (k >> (jj + 1));
+                    W[padx(cell)] = vadd(a, b);
+                    W[padx(P::S0 + cell)] = vsub(a, b);
+                }
+            }
+        }
+    } else {
+        // the folded blocks j >= J0 are contiguous in W0: cosine cells [m - m', m-1),
+        // sine cells [N - m', N-1), base pair N-1, N  ->  the sub-signal's layout
         constexpr int MP = P::m;
         const vec2<T> *wc = w0b + (m - MP), *ws = w0b + (2 * m - MP);
         if constexpr (MP % NT == 0 && NT % 32 == 0) {
@@ -433,7 +468,7 @@ template <int SUBLOG, typename T>
 __global__ void __launch_bounds__(ItemCfg<SUBLOG, T>::NT, 1)
     lg_item_kernel(vec2<T> *W0, long long Ws, int log2n, const Item *__restrict__ items, int ni,
                    const LeafTask *__restrict__ tasks, long long batch, const T *__restrict__ Ug,
-                   const __grid_constant__ LeeConstL<T> kc) {
+                   const __grid_constant__ LeeConstL<T> kc, const vec2<T> *__restrict__ x, int fold_x) {
     using C = ItemCfg<SUBLOG, T>;
     constexpr int NT = C::NT, NW = C::NW;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -451,18 +486,25 @@ __global__ void __launch_bounds__(ItemCfg<SUBLOG, T>::NT, 1)
         // pull the next item's cells into L2 while this one runs
         if (tid == 0 && g + gridDim.x < batch * ni) {
             const long long g2 = g + gridDim.x, b2 = g2 / ni;
-            long long lo[3];
-            int cnt[3];
-            const int nr = item_runs<SUBLOG>(items[g2 - b2 * ni], tasks, N, lo, cnt);
-            for (int r = 0; r < nr; ++r) l2_prefetch(W0 + b2 * Ws + lo[r], (uint32_t)(cnt[r] * sizeof(vec2<T>)));
+            if (fold_x) {
+                // the items of a signal gather from all of its input: the CTA that
+                // starts the signal's first item pulls the whole signal into L2
+                if (g2 == b2 * ni) l2_prefetch(x + b2 * N, (uint32_t)(N * sizeof(vec2<T>)));
+            } else {
+                long long lo[3];
+                int cnt[3];
+                const int nr = item_runs<SUBLOG>(items[g2 - b2 * ni], tasks, N, lo, cnt);
+                for (int r = 0; r < nr; ++r) l2_prefetch(W0 + b2 * Ws + lo[r], (uint32_t)(cnt[r] * sizeof(vec2<T>)));
+            }
         }
         if (it.kind == 0) {
             vec2<T> *cbuf = wb + (N + 2);
-            sub_item<SUBLOG, T>(wb, N / 2, S, U, kc.u, cbuf, cbuf + SPlan<SUBLOG>::m + 1, tid);
+            sub_item<SUBLOG, T>(wb, N / 2, S, U, kc.u, cbuf, cbuf + SPlan<SUBLOG>::m + 1, tid,
+                                fold_x ? x + b * N : nullptr);
         } else if (it.kind == 1) {
-            leaf_item<SUBLOG, T, NT, NW>(tasks + it.k0, 1, S, U, kc.u, wb, tid);
+            leaf_item<SUBLOG, T, NT, NW>(tasks + it.k0, 1, S, U, kc.u, wb, tid, x + b * N, N);
         } else {
-            leaf_item<SUBLOG - 1, T, NT, NW>(tasks + it.k0, 2, S, U, kc.u, wb, tid);
+            leaf_item<SUBLOG - 1, T, NT, NW>(tasks + it.k0, 2, S, U, kc.u, wb, tid, x + b * N, N);
         }
         __syncthreads();
     }
@@ -592,7 +634,7 @@ int QFT_LG(qft_large_create)(int log2n, int real_modes, void **out) {
         p->nitems = (int)items.size();
         rc |= upload(items, &p->d_items) | upload(leaves, &p->d_leaves);
     }
-    p->launches = 3;
+    p->launches = S.fold ? 3 : 2;
     for (auto &v : p->fset) p->launches += (int)v.size();
     for (auto &v : p->bset) p->launches += (int)v.size();
     *out = p;
@@ -641,8 +683,9 @@ int QFT_LG(qft_large_exec)(void *pp, int mode, const void *d_in, void *d_out, lo
     memcpy(kc.u, uhead, sizeof(kc.u));
     const unsigned yb = ybatch(batch);
     cudaError_t e;
-    // fold pass
-    {
+    // fold pass (real modes; complex plans fold on first touch)
+    if (mode != 0 && !S.fold) return (int)cudaErrorInvalidValue;
+    if (S.fold) {
         if (mode == 0) {
             const long long work = batch * (((S.m >> S.jfold) + kFoldN - 1) / kFoldN);
             const unsigned grid = (unsigned)std::min<long long>(work, 1 << 20);
@@ -683,7 +726,8 @@ int QFT_LG(qft_large_exec)(void *pp, int mode, const void *d_in, void *d_out, lo
         auto run = [&](auto kern, int nt, int smem) -> cudaError_t {
             cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (e2) return e2;
-            return launch(kern, dim3(grid), dim3(nt), (size_t)smem, st, W0, Ws, S.n, it, p->nitems, lv, batch, U, kc);
+            return launch(kern, dim3(grid), dim3(nt), (size_t)smem, st, W0, Ws, S.n, it, p->nitems, lv, batch, U, kc, x,
+                          (int)!S.fold);
         };
         switch (p->sublog) {
 #define QFT_IT(SL) \

@@ -13,6 +13,7 @@
 // the same order, so the spectrum is bit-identical.
 #pragma once
 #include "qft_smem.cuh"
+#include "qft_large.cuh"
 
 namespace qft {
 
@@ -29,6 +30,17 @@ struct LeafTop {
             int c, sg;
             run_of(RT, L, q, c, sg);
             v[q] = s[padx(c + sg * t)];
+        }
+        lee_fwd<RT, L, DST, T>(v, t, U);
+    }
+    // the same, with the leaf being all of Lee block j read straight from the
+    // input signal x (first touch folds x[n] +- x[N-n], shared.py:28-35)
+    QFT_HD static void tf_load_x(const vec2<T> *x, int N, int j, const T *U, int t, vec2<T> *v) {
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+            int c, sg;
+            run_of(RT, L, q, c, sg);
+            v[q] = fold_load<T, DST>(x, N, j, c + sg * t);
         }
         lee_fwd<RT, L, DST, T>(v, t, U);
     }

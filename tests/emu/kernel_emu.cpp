@@ -245,10 +245,26 @@ static void emu_leaf(vec2<T> *w, const LeafTask &tk, const T *U, const vec2<T> *
     else emu_leaf_dst<A, T, false>(w, tk, U, x, N);
 }
 template <int SUBLOG, typename T>
-static void emu_sub(const vec2<T> *w0, int m, vec2<T> *cb, vec2<T> *sb, const T *U) {
+static void emu_sub(const vec2<T> *w0, int m, vec2<T> *cb, vec2<T> *sb, const T *U, const vec2<T> *x = nullptr) {
     using P = SPlan<SUBLOG>;
     std::vector<vec2<T>> Wv(P::PADDED);
     vec2<T> *w = Wv.data();
+    if (x) {  // no fold pass: fold the sub-signal x[k 2^J0] while loading (sub_item)
+        int J0 = 0;
+        while ((P::m << J0) < m) ++J0;
+        for (int k = 0; k < P::m; ++k) {
+            const vec2<T> a = x[k << J0], b = x[k ? 2 * m - (k << J0) : m];
+            if (k == 0) {
+                w[padx(P::BASE)] = a;
+                w[padx(P::BASE + 1)] = b;
+            } else {
+                const int jj = ctz32((uint32_t)k);
+                const int cell = P::m - (1 << (SUBLOG - 1 - jj)) + (k >> (jj + 1));
+                w[padx(cell)] = vadd(a, b);
+                w[padx(P::S0 + cell)] = vsub(a, b);
+            }
+        }
+    } else {
     // the folded blocks j >= J0 of W0 are the sub-signal's blocks (sub_item)
     for (int c = 0; c < P::m - 1; ++c) {
         w[padx(c)] = w0[m - P::m + c];
@@ -256,6 +272,7 @@ static void emu_sub(const vec2<T> *w0, int m, vec2<T> *cb, vec2<T> *sb, const T 
     }
     w[padx(P::BASE)] = w0[2 * m - 1];
     w[padx(P::BASE + 1)] = w0[2 * m];
+    }
     emu_side<SUBLOG, T, false>(w, U);
     emu_side<SUBLOG, T, true>(w, U);
     auto emit = [&](int k, vec2<T> cv, vec2<T> sv) {
@@ -268,12 +285,14 @@ static void emu_sub(const vec2<T> *w0, int m, vec2<T> *cb, vec2<T> *sb, const T 
 template <typename T, int SUBLOG>
 static int emu_large(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
     const int J0 = log2n - SUBLOG, RG = sizeof(T) == 4 ? 5 : 4;
-    LargeSchedule S(log2n, SUBLOG, RG, J0, true);
+    // complex plans fold on load (no fold pass) for fp32 with J0 <= 2 (qft_large.cu fold_on_load)
+    LargeSchedule S(log2n, SUBLOG, RG, J0, !(sizeof(T) == 4 && J0 <= 2));
     const int N = S.N, mj0 = 1 << (SUBLOG - 1);
     const long long Ws = N + 2 + 2 * (mj0 + 1);
     std::vector<vec2<T>> W0(Ws), W1(Ws);
     vec2<T> *W[2] = {W0.data(), W1.data()};
-    for (int n = 0; n < N / 2; n += 1 << S.jfold) lg_fold_item<T>(x, W[0], n, N, log2n);  // fold pass (blocks j >= jfold)
+    if (S.fold)
+        for (int n = 0; n < N / 2; n += 1 << S.jfold) lg_fold_item<T>(x, W[0], n, N, log2n);  // fold pass (blocks j >= jfold)
     for (auto &lvl : S.f)
         for (auto &kv : lvl)
             for (auto &td : kv.second) {
@@ -286,7 +305,7 @@ static int emu_large(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
                 }
             }
     vec2<T> *cb = W[0] + (N + 2), *sb = cb + mj0 + 1;
-    emu_sub<SUBLOG, T>(W[0], N / 2, cb, sb, U);
+    emu_sub<SUBLOG, T>(W[0], N / 2, cb, sb, U, S.fold ? nullptr : x);
     for (auto &kv : S.leaf) {
         if (kv.first != SUBLOG && kv.first != SUBLOG - 1) return -2;
         for (auto &tk : kv.second) {

@@ -18,7 +18,7 @@ EMU_LIB = os.path.join(EMU_DIR, "libkernel_emu.so")
 def emu():
     src = os.path.join(EMU_DIR, "kernel_emu.cpp")
     hdrs = [os.path.join(ROOT, "paper_1301_0763_b200", "csrc", f) for f in
-            ("qft_common.cuh", "qft_lee.cuh", "qft_smem.cuh")]
+            ("qft_common.cuh", "qft_lee.cuh", "qft_smem.cuh", "qft_large.cuh", "qft_large_plan.h", "qft_leaf.cuh")]
     newest = max(os.path.getmtime(p) for p in [src] + hdrs)
     if not os.path.exists(EMU_LIB) or os.path.getmtime(EMU_LIB) < newest:
         cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
