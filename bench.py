@@ -59,7 +59,7 @@ def read_traffic(config):
             with open(f) as fh:
                 d = json.load(fh).get(f"config{config}")
             if d and d.get("traffic_bytes_per_launch"):
-                best = d
+                best = dict(d, _file=os.path.relpath(f, ROOT))
         except Exception:
             pass
     return best
@@ -333,8 +333,16 @@ def main():
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": (lambda d: None if not d or B != BATCH else d["traffic_bytes_per_launch"])(tr),
                          "traffic_unit": "bytes per step: ncu dram__bytes_read.sum + dram__bytes_write.sum of the "
-                                         "step's kernels (profiles/r1_summary.json); algorithmic bytes per step = "
-                                         f"{2 * esz * N * B}",
+                                         f"step's kernels ({tr.get('_file') if tr else 'profiles/'}); algorithmic "
+                                         f"bytes per step = {2 * esz * N * B}",
+                         # the unit that actually binds the single-pass kernels: the shared-memory /
+                         # L1 data pipe (128 B/clk/SM), from the same committed ncu capture
+                         "secondary": (lambda fc: None if not fc else {
+                             "bound": "smem (L1 data pipe, 128 B/clk/SM)",
+                             "frac": fc.get("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", 0) / 100.0,
+                             "smem_wavefronts_per_transform": fc.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 0) / B,
+                             "kernel": fc.get("kernel", "").split("(")[0],
+                             "source": tr.get("_file")})((tr or {}).get("full_capture") if B == BATCH else None),
                          "dominant_kernel": tr.get("dominant_kernel") if tr else None,
                          "dominant_share_of_step": tr.get("dominant_share_of_step") if tr else None,
                          "algorithmic_bytes_per_transform": 2 * esz * N, "passes": info.passes},

@@ -1,8 +1,10 @@
 #!/bin/bash
 # Round-end measurement on one B200 (inside gpurun): bench lines for every
 # config, the reference arm, launch lists and ncu full captures of the top kernels.
+# usage: bash tools/final_measure.sh [tag]   (outputs under gpurun_out/<tag>/)
 export PYTHONUNBUFFERED=1
-out=gpurun_out/final; mkdir -p $out
+tag=${1:-final}
+out=gpurun_out/$tag; mkdir -p $out
 timeout 400 python bench.py > $out/bench_c2.json 2> $out/bench_c2.err
 for c in 1 3 4 5; do timeout 400 python bench.py --config $c > $out/bench_c$c.json 2> $out/bench_c$c.err; done
 timeout 400 python bench.py --impl reference > $out/bench_ref.json 2> $out/bench_ref.err
@@ -10,7 +12,7 @@ for c in 2 3 4 5; do
   timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -k regex:"qft_|lg_" -c 40 --csv --log-file $out/launches_c$c.csv python bench.py --config $c --steps 2 --warmup 1 --no-cpu --no-e2e > /dev/null 2>&1
 done
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:qft_cdft_smem -s 3 -c 1 -o $out/prof_c2 python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"qft_cdft_(smem|pipe)" -s 3 -c 1 -o $out/prof_c2 python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:qft_cdft_smem -s 1 -c 1 -o $out/prof_c5 python bench.py --config 5 --steps 1 --warmup 1 --no-cpu --no-e2e > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:lg_item -s 1 -c 1 -o $out/prof_c3 python bench.py --config 3 --steps 1 --warmup 1 --no-cpu --no-e2e > /dev/null 2>&1
 echo done > $out/status

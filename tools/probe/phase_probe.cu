@@ -126,6 +126,7 @@ int main(int argc, char **argv) {
         for (int w = 0; w < K::NW; ++w) printf(" %lld/%lld", m[24 + w] - m[1], m[8 + w] - m[1]);
         printf("\n");
     }
+    printf("  TMA issue (CTA 0 last): fence %lld, expect_tx %lld, copies %lld\n", u[11] - u[10], u[12] - u[11], u[13] - u[12]);
     printf("  unit_big (CTA 0 warp 0, last iteration): F load+fold %lld, F store %lld, Lee-32 %lld, C %lld cycles\n",
            u[1] - u[0], u[2] - u[1], u[3] - u[2], u[4] - u[3]);
     return 0;

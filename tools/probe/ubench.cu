@@ -58,6 +58,45 @@ __global__ void k_lds(unsigned long long *out, long long *cyc, int iters, int ma
     out[threadIdx.x] = s;
     if (threadIdx.x == 0) cyc[0] = t1 - t0;
 }
+// LDS.128 / LDS.32 / STS.64 throughput
+template <int ACC, int W>
+__global__ void k_ldsw(unsigned long long *out, long long *cyc, int iters) {
+    __shared__ __align__(16) unsigned long long sm[4096];
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) sm[i] = i;
+    __syncthreads();
+    unsigned long long s = 0;
+    int base = threadIdx.x & 31;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        unsigned long long v[ACC];
+#pragma unroll
+        for (int i = 0; i < ACC; ++i) {
+            const unsigned a = (unsigned)__cvta_generic_to_shared(&sm[((base + 32 * i + it) * 2) & 4095]);
+            if (W == 16) {
+                unsigned long long b;
+                asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v[i]), "=l"(b) : "r"(a));
+                v[i] ^= b;
+            } else if (W == 4) {
+                unsigned b;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(b) : "r"(a));
+                v[i] = b;
+            } else if (W == -8) {
+                asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"((unsigned long long)it));
+                v[i] = 0;
+            } else if (W == -16) {
+                asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(a), "l"((unsigned long long)it), "l"((unsigned long long)i));
+                v[i] = 0;
+            } else {
+                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v[i]) : "r"(a));
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < ACC; ++i) s += v[i];
+    }
+    long long t1 = clock64();
+    out[threadIdx.x] = s;
+    if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
 int main() {
     unsigned long long *o;
     long long *c, h;
@@ -79,6 +118,22 @@ int main() {
         cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
         double l = (double)h / (it * 8.0);
         printf("warps/CTA %2d: FADD2 %.2f cyc/inst/warp (dep chain %.2f), FADD %.2f, LDS.64 %.2f cyc/inst/warp\n", w, f2, f2l, f1, l);
+    }
+    for (int w : {1, 4, 16}) {
+        double r[5];
+        int k = 0;
+        for (int W : {4, 8, 16, -8, -16}) {
+            switch (W) {
+                case 4: k_ldsw<8, 4><<<1, 32 * w>>>(o, c, it); break;
+                case 8: k_ldsw<8, 8><<<1, 32 * w>>>(o, c, it); break;
+                case 16: k_ldsw<8, 16><<<1, 32 * w>>>(o, c, it); break;
+                case -8: k_ldsw<8, -8><<<1, 32 * w>>>(o, c, it); break;
+                case -16: k_ldsw<8, -16><<<1, 32 * w>>>(o, c, it); break;
+            }
+            cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+            r[k++] = (double)h / (it * 8.0);
+        }
+        printf("warps %2d: cyc/inst/warp LDS.32 %.2f LDS.64 %.2f LDS.128 %.2f STS.64 %.2f STS.128 %.2f\n", w, r[0], r[1], r[2], r[3], r[4]);
     }
     // which warps share an SM sub-partition: run only warps {0, w} of an 8-warp CTA
     for (int w = 1; w < 8; ++w) {
