@@ -78,7 +78,14 @@ def test_no_fused_multiply_add_in_transform_kernels():
 def test_sm100a_and_packed_fp32():
     funcs, out = sass_by_function()
     assert "sm_100a" in out
-    smem32 = [k for k in funcs if "qft_cdft_smem" in k and "ILi12EfLi0E" in k]
-    assert smem32, "fp32 N=4096 kernel missing"
-    ops = funcs[smem32[0]]
-    assert any(o.startswith("FADD2") for o, _, _ in ops), "fp32 adds should use the packed FADD2 pipe"
+    # the fp32 N=4096 cdft path is the pipelined kernel (qft_pipe.cuh); the real
+    # modes keep qft_cdft_smem
+    for pat in ("qft_cdft_pipeILi12EfE", "qft_cdft_smemILi12EfLi1E", "qft_cdft_smemILi14EfLi0E"):
+        ks = [k for k in funcs if pat in k]
+        assert ks, f"{pat} kernel missing"
+        ops = funcs[ks[0]]
+        assert any(o.startswith("FADD2") for o, _, _ in ops), f"{pat}: fp32 adds should use the packed FADD2 pipe"
+    pipe = [k for k in funcs if "qft_cdft_pipeILi12EfE" in k][0]
+    ops = [o for o, _, _ in funcs[pipe]]
+    assert any(o.startswith("UBLKCP") or o.startswith("UTMALDG") or "BLK" in o for o in ops), \
+        "the pipelined kernel should issue TMA bulk copies"
