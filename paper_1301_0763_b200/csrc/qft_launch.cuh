@@ -36,6 +36,9 @@
 #ifndef QFT_REST_FUSED
 #define QFT_REST_FUSED 0   // rest unit: F / C levels of all its blocks together (measured slower: 54.0 vs 55.5M tr/s)
 #endif
+#ifndef QFT_UFENCE
+#define QFT_UFENCE 0       // scheduling fences between the sub-phases of a warp unit (see QFT_UMARK)
+#endif
 #ifndef QFT_TT_MAX
 #define QFT_TT_MAX 4       // cap on signals per CTA iteration
 #endif
@@ -68,9 +71,27 @@ static __device__ long long qft_probe_buf[160 * 16 * 64];
 #define QFT_WMARK_AT(o) \
     do {                \
     } while (0)
+#if QFT_UFENCE == 1
+// compiler-only memory fence between the sub-phases of a warp unit
+#define QFT_UMARK(k) asm volatile("" ::: "memory")
+#elif QFT_UFENCE == 2
+// a never-taken branch: a basic-block boundary between the sub-phases
+#define QFT_UMARK(k)                                     \
+    do {                                                 \
+        if (threadIdx.x == 0xffff) asm volatile("trap;"); \
+    } while (0)
+#elif QFT_UFENCE == 3
+#define QFT_UMARK(k)                                     \
+    do {                                                 \
+        long long c_;                                    \
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_)); \
+        if (c_ == -1) asm volatile("trap;");              \
+    } while (0)
+#else
 #define QFT_UMARK(k) \
     do {             \
     } while (0)
+#endif
 #define QFT_MARK(k) \
     do {            \
     } while (0)

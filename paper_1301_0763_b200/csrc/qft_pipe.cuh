@@ -24,10 +24,35 @@
 #include "qft_launch.cuh"
 
 #ifndef QFT_PIPE
-#define QFT_PIPE 1  // serve fp32 N = 4096 cdft with the pipelined kernel
+#define QFT_PIPE 1  // serve fp32 N = 4096 cdft with the pipelined kernel (1: barrier-phased, 2: dataflow -- measured no faster)
 #endif
 #ifndef QFT_PIPE_NWA
 #define QFT_PIPE_NWA 5  // warps running the in-place A0 of the next batch during D
+#endif
+
+// probe marks of the dataflow kernel, individually selectable (tools/probe)
+#if defined(QFT_PROBE) && !defined(QFT_PMASK)
+#define QFT_PMASK 15
+#endif
+#if defined(QFT_PROBE) && (QFT_PMASK & 1)
+#define QFT_PMARK24() QFT_WMARK_AT(24)
+#else
+#define QFT_PMARK24() do {} while (0)
+#endif
+#if defined(QFT_PROBE) && (QFT_PMASK & 2)
+#define QFT_PMARK8() QFT_WMARK_AT(8)
+#else
+#define QFT_PMARK8() do {} while (0)
+#endif
+#if defined(QFT_PROBE) && (QFT_PMASK & 4)
+#define QFT_PMARK40() QFT_WMARK_AT(40)
+#else
+#define QFT_PMARK40() do {} while (0)
+#endif
+#if defined(QFT_PROBE) && (QFT_PMASK & 8)
+#define QFT_PMARK52() QFT_WMARK_AT(52)
+#else
+#define QFT_PMARK52() do {} while (0)
 #endif
 
 namespace qft {
@@ -56,7 +81,7 @@ struct PCfg {
     static constexpr int X_OFF = 0;
     static constexpr int U_OFF = 2 * (TT > 0 ? TT : 1) * PER_W;
     static constexpr int BAR_OFF = (U_OFF + UB + 15) / 16 * 16;
-    static constexpr int SMEM = BAR_OFF + 32;
+    static constexpr int SMEM = BAR_OFF + 64;  // 5 mbarriers
 };
 
 template <int LOG2N, typename T>
@@ -184,7 +209,7 @@ __global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
         const int ntr = ntr_of(bt);
         vec2<T> *W = set(cur);
         QFT_MARK(1);
-        QFT_WMARK_AT(24);
+        QFT_PMARK24();
         fused_units<LOG2N, T, 0, TT, NW>(W, U, kc.u, ntr, warp, lane);
         QFT_WMARK();
         __syncthreads();
@@ -214,10 +239,112 @@ __global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
     }
 }
 
+// wait with a suspend-time hint: the waiting warp is parked by the hardware
+// until the phase completes (up to the hint) instead of re-polling
+QFT_DEV void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
+QFT_DEV void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Dataflow variant (QFT_PIPE == 2): no CTA-wide barrier inside the loop.  Four
+// mbarriers carry exactly the dependencies of the schedule above:
+//   adone   A0(i) stored                  -> every warp may start units(i)
+//   udone   units(i) stored (all warps)   -> D warps may start D(i)
+//   ddone   D(i) has read its set         -> warp 0 refills the set by TMA
+//   tma[s]  raw signals of a batch landed -> A0 warps may fold them
+// so the A0 warps fold batch i+1 and start units(i+1) while the D warps are
+// still in D(i), and a D warp goes from D(i) straight into units(i+1).
+// ---------------------------------------------------------------------------
+template <int LOG2N, typename T>
+__global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
+    qft_cdft_pipe2(const vec2<T> *__restrict__ in, vec2<T> *__restrict__ out, long long batch,
+                   const T *__restrict__ Ug, const __grid_constant__ LeeConst<T> kc) {
+    using P = SPlan<LOG2N>;
+    using C = PCfg<LOG2N, T>;
+    constexpr int TT = C::TT, NT = C::NT, NW = C::NW, NWD = C::NWD, NWA = C::NWA;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    vec2<T> *X0 = reinterpret_cast<vec2<T> *>(smem_raw + C::X_OFF);
+    T *U = reinterpret_cast<T *>(smem_raw + C::U_OFF);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::BAR_OFF);
+    uint64_t *tma = bar, *adone = bar + 2, *udone = bar + 3, *ddone = bar + 4;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool dwarp = warp < NWD, awarp = warp >= NWD && warp < NWD + NWA;
+    const int ga = tid - NWD * 32;
+    const A0Lane64 a0l64 = a0_lane64<LOG2N>(lane);
+    const long long nbatch = (batch + TT - 1) / TT, G = gridDim.x;
+    auto ntr_of = [&](long long b) { return (int)((batch - b * TT) < TT ? (batch - b * TT) : TT); };
+    auto set = [&](int s) { return X0 + s * TT * P::PADDED; };
+
+    for (int i = tid; i < P::UCELLS; i += NT) U[i] = Ug[i];
+    if (tid == 0) {
+        mbar_init(&tma[0], 1);
+        mbar_init(&tma[1], 1);
+        mbar_init(adone, NWA * 32);
+        (void)udone;
+        (void)ddone;
+    }
+    __syncthreads();
+    const long long b0 = blockIdx.x;
+    if (b0 >= nbatch) return;
+    if (warp == 0) {
+        tma_load_slots<LOG2N, T>(set(0), in + b0 * TT * P::N, ntr_of(b0), &tma[0], lane);
+        if (b0 + G < nbatch) tma_load_slots<LOG2N, T>(set(1), in + (b0 + G) * TT * P::N, ntr_of(b0 + G), &tma[1], lane);
+    }
+    if (awarp) {
+        mbar_wait(&tma[0], 0);
+        a0_inplace<LOG2N, T>(set(0), ntr_of(b0), ga, a0l64);
+        mbar_arrive(adone);
+    }
+    uint32_t k = 0;
+    for (long long bt = b0; bt < nbatch; bt += G, ++k) {
+        const int cur = k & 1;
+        const uint32_t ph = k & 1;
+        const int ntr = ntr_of(bt);
+        vec2<T> *W = set(cur);
+        mbar_wait_sleep(adone, ph);  // A0(bt) is in set cur
+        QFT_PMARK24();
+        fused_units<LOG2N, T, 0, TT, NW>(W, U, kc.u, ntr, warp, lane);
+        QFT_PMARK8();
+        // all units of the batch stored (named barrier 2, every thread); the D
+        // warps then need only each other (barrier 3) before the set is refilled,
+        // and every warp only the A0 group (mbarrier adone) before units(i+1):
+        // the A0 warps start units(i+1) while the D warps are still in D(i)
+        named_bar(2, NT);
+        if (dwarp) {
+            QFT_PMARK40();
+            for (int it = tid; it < TT * P::DT; it += NWD * 32) {
+                const int tau = it / P::DT, ti = it - tau * P::DT;
+                if (tau < ntr) Chain<LOG2N, T>::unit(W + tau * P::PADDED, out + (bt * TT + tau) * P::N, ti);
+            }
+            QFT_PMARK52();
+            if (bt + 2 * G < nbatch) {
+                named_bar(3, NWD * 32);  // set cur is no longer read
+                if (warp == 0)
+                    tma_load_slots<LOG2N, T>(W, in + (bt + 2 * G) * TT * P::N, ntr_of(bt + 2 * G), &tma[cur], lane);
+            }
+        } else if (awarp && bt + G < nbatch) {
+            mbar_wait_sleep(&tma[cur ^ 1], ((k + 1) >> 1) & 1u);
+            QFT_PMARK40();
+            a0_inplace<LOG2N, T>(set(cur ^ 1), ntr_of(bt + G), ga, a0l64);
+            QFT_PMARK52();
+            mbar_arrive(adone);
+        }
+    }
+}
+
 template <int LOG2N, typename T>
 cudaError_t launch_pipe(const LaunchArgs &a) {
     using C = PCfg<LOG2N, T>;
-    auto kern = qft_cdft_pipe<LOG2N, T>;
+    auto kern = QFT_PIPE == 2 ? qft_cdft_pipe2<LOG2N, T> : qft_cdft_pipe<LOG2N, T>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     const long long nbatch = (a.batch + C::TT - 1) / C::TT;

@@ -2,7 +2,12 @@
 // kernel with QFT_PROBE so thread 0 of every CTA records clock64() at each
 // phase barrier, runs the config-2 (or -DPLOG2N=k) workload on random data and
 // prints the median cycles per phase.  Build + run: tools/probe/run_probe.sh
+#ifndef NOPROBE
 #define QFT_PROBE 1
+#endif
+#ifdef PIPE2
+#define QFT_PIPE 2
+#endif
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -19,7 +24,10 @@
 int main(int argc, char **argv) {
     constexpr int LOG2N = PLOG2N, N = 1 << LOG2N;
     long long batch = argc > 1 ? atoll(argv[1]) : (LOG2N == 12 ? 16384 : 262144 / 4);
-#ifdef PIPE
+#ifdef PIPE2
+    using K = qft::PCfg<LOG2N, float>;
+#define LAUNCH qft::launch_pipe<LOG2N, float>
+#elif defined(PIPE)
     using K = qft::PCfg<LOG2N, float>;
 #define LAUNCH qft::launch_pipe<LOG2N, float>
 #else
@@ -53,8 +61,31 @@ int main(int argc, char **argv) {
     ms /= REP;
     printf("kernel %.3f ms  %.2f M tr/s  %.1f GB/s  err=%s\n", ms, batch / ms / 1e3, batch * N * 16.0 / ms / 1e6,
            cudaGetErrorString(cudaGetLastError()));
+#ifdef NOPROBE
+    return 0;
+#else
     std::vector<long long> b(160 * 16 * 64);
     cudaMemcpyFromSymbol(b.data(), qft_probe_buf, b.size() * 8);
+#ifdef PIPE2
+    // per warp, relative to warp 0's units start of the same iteration: units start / end,
+    // after its wait (D: udone, A0: tma) / end of D or A0; CTA 0 and CTA 77, iterations 5..7
+    for (int c : {0, 77})
+        for (int it = 5; it < 8; ++it) {
+            long long *m = &b[(c * 16 + it) * 64], t0 = m[24];
+            printf("CTA %d it %d:", c, it);
+            for (int w = 0; w < K::NW; ++w)
+                printf(" w%d[%lld %lld %lld %lld]", w, m[24 + w] - t0, m[8 + w] - t0, m[40 + w] - t0, m[52 + w] - t0);
+            printf("\n");
+        }
+    {
+        std::vector<double> itv;
+        for (int c = 0; c < sms; ++c)
+            for (int it = 2; it < 14; ++it) itv.push_back(b[(c * 16 + it + 1) * 64 + 24] - b[(c * 16 + it) * 64 + 24]);
+        std::sort(itv.begin(), itv.end());
+        printf("median iteration (warp 0 units start to next) %.0f cycles\n", itv[itv.size() / 2]);
+    }
+    return 0;
+#endif
 #ifdef PIPE
     {   // bitwise check against the unpipelined kernel on the same input
         float *out2;
@@ -122,12 +153,14 @@ int main(int argc, char **argv) {
         long long *m = &b[(0 * 16 + 14) * 64];
         printf("  CTA 0 iteration 15: start %lld, unit start +%lld, units barrier +%lld\n", m[1], u[0] - m[1], m[3] - m[1]);
         printf("  m5 -> after TMA issue %lld -> m1(next) %lld\n", m[6] - m[5], (m + 64)[1] - m[5]);
-        printf("  per-warp units start/end:");
-        for (int w = 0; w < K::NW; ++w) printf(" %lld/%lld", m[24 + w] - m[1], m[8 + w] - m[1]);
+        printf("  per-warp units start/end (rel. to the previous phase-2 barrier exit m5):");
+        long long *mp = m - 64;
+        for (int w = 0; w < K::NW; ++w) printf(" %lld/%lld", m[24 + w] - mp[5], m[8 + w] - mp[5]);
         printf("\n");
     }
     printf("  TMA issue (CTA 0 last): fence %lld, expect_tx %lld, copies %lld\n", u[11] - u[10], u[12] - u[11], u[13] - u[12]);
     printf("  unit_big (CTA 0 warp 0, last iteration): F load+fold %lld, F store %lld, Lee-32 %lld, C %lld cycles\n",
            u[1] - u[0], u[2] - u[1], u[3] - u[2], u[4] - u[3]);
     return 0;
+#endif
 }
