@@ -50,17 +50,17 @@
 static __device__ long long qft_probe_buf[160 * 16 * 64];
 #define QFT_MARK(k)                                                                       \
     do {                                                                                  \
-        const long long it_ = (bt - blockIdx.x) / gridDim.x;                              \
+        const int it_ = (int)(__fdividef((float)(bt - blockIdx.x), (float)gridDim.x) + 0.5f);                              \
         if (tid == 0 && blockIdx.x < 160 && it_ < 16) qft_probe_buf[(blockIdx.x * 16 + it_) * 64 + (k)] = clock64(); \
     } while (0)
 #define QFT_WMARK()                                                                       \
     do {                                                                                  \
-        const long long it_ = (bt - blockIdx.x) / gridDim.x;                              \
+        const int it_ = (int)(__fdividef((float)(bt - blockIdx.x), (float)gridDim.x) + 0.5f);                              \
         if (lane == 0 && blockIdx.x < 160 && it_ < 16) qft_probe_buf[(blockIdx.x * 16 + it_) * 64 + 8 + warp] = clock64(); \
     } while (0)
 #define QFT_WMARK_AT(o)                                                                   \
     do {                                                                                  \
-        const long long it_ = (bt - blockIdx.x) / gridDim.x;                              \
+        const int it_ = (int)(__fdividef((float)(bt - blockIdx.x), (float)gridDim.x) + 0.5f);                              \
         if (lane == 0 && blockIdx.x < 160 && it_ < 16) qft_probe_buf[(blockIdx.x * 16 + it_) * 64 + (o) + warp] = clock64(); \
     } while (0)
 #define QFT_UMARK(k)                                                                      \

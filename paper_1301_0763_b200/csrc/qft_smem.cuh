@@ -432,8 +432,13 @@ struct Chain {
     static QFT_HD void emit_u(vec2<T> *y, int k, vec2<T> cv, vec2<T> sv) {
         const vec2<T> u = {sv.y, -sv.x};
         const bool edge = (k == 0) || (k == P::m);  // harmonics 0, N/2: copies
+#ifdef QFT_DIAG_NOSTORE  // diagnostic only (tools/probe): keep the math, drop the stores
+        const vec2<T> a = edge ? cv : vadd(cv, u), b = vsub(cv, u);
+        if (a.x == (T)1.2345e-30 && b.y == (T)1.2345e-30) y[k] = a;
+#else
         y[k] = edge ? cv : vadd(cv, u);
         if (!edge) y[P::N - k] = vsub(cv, u);
+#endif
     }
     // unfold with self-paired indices (k == q_j) duplicated: both children get
     // the C copy / S leaf and write identical values.  emit(k, C_0[k], S_0[k]).
