@@ -592,7 +592,11 @@ QFT_DEV void a0_complex(const vec2<T> *src, vec2<T> *W, int ntr, int TTn, int ti
 template <int LOG2N, typename T, int MODE = 0>
 __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
     qft_cdft_smem(const vec2<T> *__restrict__ in, vec2<T> *__restrict__ out, long long batch,
-                  const T *__restrict__ Ug, const __grid_constant__ LeeConst<T> kc, long long nreal = 0) {
+                  const T *__restrict__ Ug, const __grid_constant__ LeeConst<T> kc, long long nreal = 0,
+                  int tt_arg = KCfg<LOG2N, T>::TT) {
+    // tt <= TT: signals per CTA iteration (smaller for small batches, so that
+    // the batch spreads over every SM; the shared-memory slots stay TT)
+    const int tt = KCfg<LOG2N, T>::TT == 1 ? 1 : tt_arg;
     using P = SPlan<LOG2N>;
     using K = KCfg<LOG2N, T>;
     constexpr int TT = K::TT, NT = K::NT, NW = K::NW;
@@ -604,7 +608,7 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + K::BAR_OFF);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    const long long nbatch = (batch + TT - 1) / TT;
+    const long long nbatch = (batch + tt - 1) / tt;
     const A0Lane64 a0l64 = a0_lane64<LOG2N>(lane);
     for (int i = tid; i < P::UCELLS; i += NT) U[i] = Ug[i];
     if (TMA && tid == 0) mbar_init(bar, 1);
@@ -613,14 +617,14 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
     constexpr int TS = K::TS;
     // TMA part of batch b: its first min(TS, count) signals
     auto stage_count = [&](long long b) -> long long {
-        const long long nt = (batch - b * TT) < TT ? (batch - b * TT) : TT;
+        const long long nt = (batch - b * tt) < tt ? (batch - b * tt) : tt;
         return nt < TS ? nt : TS;
     };
     if (TMA && tid == 0 && bt < nbatch)
-        tma_bulk_load(stage, in + bt * TT * P::N, (uint32_t)(stage_count(bt) * P::N * K::VB), bar);
+        tma_bulk_load(stage, in + bt * tt * P::N, (uint32_t)(stage_count(bt) * P::N * K::VB), bar);
     uint32_t parity = 0;
     for (; bt < nbatch; bt += gridDim.x) {
-        const int ntr = (int)((batch - bt * TT) < TT ? (batch - bt * TT) : TT);
+        const int ntr = (int)((batch - bt * tt) < tt ? (batch - bt * tt) : tt);
         QFT_MARK(0);
         if constexpr (TMA) {
             mbar_wait(bar, parity);
@@ -630,8 +634,8 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
         if (MODE == 0 && TS < TT && tid == 0 && bt + gridDim.x < nbatch) {
             // pull the next batch's unstaged signals into L2 while this one is transformed
             const long long nb = bt + gridDim.x;
-            const long long nt = (batch - nb * TT) < TT ? (batch - nb * TT) : TT;
-            if (nt > TS) l2_prefetch(in + (nb * TT + TS) * P::N, (uint32_t)((nt - TS) * P::N * K::VB));
+            const long long nt = (batch - nb * tt) < tt ? (batch - nb * tt) : tt;
+            if (nt > TS) l2_prefetch(in + (nb * tt + TS) * P::N, (uint32_t)((nt - TS) * P::N * K::VB));
         }
         // A0: fold + route -> W
         if constexpr (MODE != 0) {
@@ -639,14 +643,14 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
             constexpr int RL = MODE == 1 ? P::N : (MODE == 2 ? P::m + 1 : P::m - 1);
             const T *xr = reinterpret_cast<const T *>(in);
             for (int tau = 0; tau < ntr; ++tau) {
-                const long long ra = 2 * (bt * TT + tau), rb = ra + 1 < nreal ? ra + 1 : ra;
+                const long long ra = 2 * (bt * tt + tau), rb = ra + 1 < nreal ? ra + 1 : ra;
                 for (int nn = tid; nn <= P::m; nn += NT)
                     a0_item_real<LOG2N, T, MODE>(xr + ra * RL, xr + rb * RL, W + tau * P::PADDED, nn);
             }
         } else {
             if constexpr (TS < TT) {
                 if (ntr > TS)
-                    a0_complex<LOG2N, T, sizeof(T) == 8 ? 1 : QFT_A0_UNR>(in + (bt * TT + TS) * P::N,
+                    a0_complex<LOG2N, T, sizeof(T) == 8 ? 1 : QFT_A0_UNR>(in + (bt * tt + TS) * P::N,
                                                                           W + TS * P::PADDED, ntr - TS, TT - TS, tid,
                                                                           NT, NW, a0l64);
             }
@@ -657,7 +661,7 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
         // the staging buffer is free: prefetch the next batch while we compute
         if (TMA && tid == 0 && bt + gridDim.x < nbatch) {
             const long long nb = bt + gridDim.x;
-            tma_bulk_load(stage, in + nb * TT * P::N, (uint32_t)(stage_count(nb) * P::N * K::VB), bar);
+            tma_bulk_load(stage, in + nb * tt * P::N, (uint32_t)(stage_count(nb) * P::N * K::VB), bar);
         }
         // TF: top forward levels of the huge blocks (N > 4096; ends with a barrier)
         if constexpr (P::JH > 0) top_f<LOG2N, T, MODE>(W, U, ntr, tid);
@@ -675,16 +679,16 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
             if constexpr (MODE == 0) {
                 if constexpr (K::DHALF) {
                     const int h = ti >= P::DT, t = ti - (h ? P::DT : 0);
-                    Chain<LOG2N, T>::unit_half(W + tau * P::PADDED, out + (bt * TT + tau) * P::N, t, h);
+                    Chain<LOG2N, T>::unit_half(W + tau * P::PADDED, out + (bt * tt + tau) * P::N, t, h);
                 } else {
-                    Chain<LOG2N, T>::unit(W + tau * P::PADDED, out + (bt * TT + tau) * P::N, ti);
+                    Chain<LOG2N, T>::unit(W + tau * P::PADDED, out + (bt * tt + tau) * P::N, ti);
                 }
             } else {
                 const int t = K::DHALF ? (ti >= P::DT ? ti - P::DT : ti) : ti;
                 const int h = K::DHALF ? (ti >= P::DT) : 0;
                 // per-signal outputs: rdft packed half spectrum (shared.py:38-43 with
                 // complex_from_packed, shared.py:94-101), dct0 / dst0 real spectra
-                const long long ra = 2 * (bt * TT + tau);
+                const long long ra = 2 * (bt * tt + tau);
                 const bool has_b = ra + 1 < nreal;
                 auto emit = [&](int k, vec2<T> cv, vec2<T> sv) {
                     if constexpr (MODE == 1) {
@@ -725,14 +729,19 @@ cudaError_t launch_smem(const LaunchArgs &a) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::NT, K::SMEM);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    const long long nbatch = (a.batch + K::TT - 1) / K::TT;
-    long long grid = (long long)a.num_sms * per_sm;
+    // small batches: fewer signals per CTA iteration so every SM gets work
+    const long long ctas = (long long)a.num_sms * per_sm;
+    int tt = K::TT;
+    if (a.batch < ctas * K::TT) tt = (int)((a.batch + ctas - 1) / ctas);
+    if (tt < 1) tt = 1;
+    const long long nbatch = (a.batch + tt - 1) / tt;
+    long long grid = ctas;
     if (grid > nbatch) grid = nbatch;
     if (grid < 1) grid = 1;
     LeeConst<T> kc;
     for (int i = 0; i < 32; ++i) kc.u[i] = ((const T *)a.Uhead)[i];
     kern<<<(unsigned)grid, K::NT, K::SMEM, a.stream>>>((const vec2<T> *)a.in, (vec2<T> *)a.out, a.batch,
-                                                       (const T *)a.U, kc, a.nreal);
+                                                       (const T *)a.U, kc, a.nreal, tt);
     return cudaGetLastError();
 }
 
