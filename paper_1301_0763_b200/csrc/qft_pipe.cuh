@@ -26,6 +26,9 @@
 #ifndef QFT_PIPE
 #define QFT_PIPE 1  // serve fp32 N = 4096 cdft with the pipelined kernel (1: barrier-phased, 2: dataflow -- measured no faster)
 #endif
+#ifndef QFT_PIPE_DSPREAD
+#define QFT_PIPE_DSPREAD 0  // phase-D items spread evenly over all non-A0 warps (measured -0.5 %)
+#endif
 #ifndef QFT_PIPE_NWA
 #define QFT_PIPE_NWA 5  // warps running the in-place A0 of the next batch during D
 #endif
@@ -72,9 +75,14 @@ struct PCfg {
     static constexpr int NU = 2 * (P::NU1 + 1);
     static constexpr int W_U = (TT > 0 ? TT : 1) * NU;
     static constexpr int DI = P::DT;
-    static constexpr int NWD = ((TT > 0 ? TT : 1) * DI + 31) / 32;  // D warps
-    static constexpr int NWA = QFT_PIPE_NWA;                         // A0 warps
-    static constexpr int NW = mx(W_U, NWD + NWA);
+    static constexpr int NWD0 = ((TT > 0 ? TT : 1) * DI + 31) / 32;  // D warps needed
+    static constexpr int NWA = QFT_PIPE_NWA;                          // A0 warps
+    static constexpr int NW = mx(W_U, NWD0 + NWA);
+    // every warp not folding the next batch runs phase D; the items are spread
+    // evenly (DPW consecutive items per warp) so no sub-partition carries a
+    // full D warp more than another
+    static constexpr int NWD = QFT_PIPE_DSPREAD ? NW - NWA : NWD0;
+    static constexpr int DPW = ((TT > 0 ? TT : 1) * DI + NWD - 1) / NWD;
     static constexpr int NT = NW * 32;
     static constexpr int NC64 = P::m / 64;  // A0 chunks per signal
     static constexpr int RA = (NC64 + NWA - 1) / NWA;
@@ -215,14 +223,24 @@ __global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
         __syncthreads();
         QFT_MARK(3);
         if (warp < NWD) {
-            for (int it = tid; it < TT * P::DT; it += NWD * 32) {
+            if (QFT_PIPE_DSPREAD) {
+                const int it = warp * C::DPW + lane;  // DPW <= 32 consecutive items per warp
                 const int tau = it / P::DT, ti = it - tau * P::DT;
-                if (tau < ntr) Chain<LOG2N, T>::unit(W + tau * P::PADDED, out + (bt * TT + tau) * P::N, ti);
+                if (lane < C::DPW && it < TT * P::DT && tau < ntr)
+                    Chain<LOG2N, T>::unit(W + tau * P::PADDED, out + (bt * TT + tau) * P::N, ti);
+            } else {
+                for (int it = tid; it < TT * P::DT; it += NWD * 32) {
+                    const int tau = it / P::DT, ti = it - tau * P::DT;
+                    if (tau < ntr) Chain<LOG2N, T>::unit(W + tau * P::PADDED, out + (bt * TT + tau) * P::N, ti);
+                }
             }
+            QFT_PMARK52();
         } else if (a0_warp && bt + G < nbatch) {
             uint32_t &ph = cur ? ph0 : ph1;  // the next batch sits in set cur^1
             mbar_wait(&bar[cur ^ 1], ph);
+            QFT_PMARK40();
             a0_inplace<LOG2N, T>(set(cur ^ 1), ntr_of(bt + G), ga, a0l64);
+            QFT_PMARK52();
         }
         if (bt + G < nbatch) {
             if (cur) ph0 ^= 1u;

@@ -153,6 +153,9 @@ int main(int argc, char **argv) {
         long long *m = &b[(0 * 16 + 14) * 64];
         printf("  CTA 0 iteration 15: start %lld, unit start +%lld, units barrier +%lld\n", m[1], u[0] - m[1], m[3] - m[1]);
         printf("  m5 -> after TMA issue %lld -> m1(next) %lld\n", m[6] - m[5], (m + 64)[1] - m[5]);
+        printf("  phase 2 per warp (rel. to units barrier m3): tma-wait-end/end:");
+        for (int w = 0; w < K::NW; ++w) printf(" w%d %lld/%lld", w, m[40 + w] - m[3], m[52 + w] - m[3]);
+        printf("\n");
         printf("  per-warp units start/end (rel. to the previous phase-2 barrier exit m5):");
         long long *mp = m - 64;
         for (int w = 0; w < K::NW; ++w) printf(" %lld/%lld", m[24 + w] - mp[5], m[8 + w] - mp[5]);
