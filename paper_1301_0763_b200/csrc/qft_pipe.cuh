@@ -29,6 +29,9 @@
 #ifndef QFT_PIPE_DSPREAD
 #define QFT_PIPE_DSPREAD 0  // phase-D items spread evenly over all non-A0 warps (measured -0.5 %)
 #endif
+#ifndef QFT_PIPE_NW_EXTRA
+#define QFT_PIPE_NW_EXTRA 0  // extra warps (phase D with QFT_PIPE_DSPREAD)
+#endif
 #ifndef QFT_PIPE_NWA
 #define QFT_PIPE_NWA 5  // warps running the in-place A0 of the next batch during D
 #endif
@@ -77,7 +80,7 @@ struct PCfg {
     static constexpr int DI = P::DT;
     static constexpr int NWD0 = ((TT > 0 ? TT : 1) * DI + 31) / 32;  // D warps needed
     static constexpr int NWA = QFT_PIPE_NWA;                          // A0 warps
-    static constexpr int NW = mx(W_U, NWD0 + NWA);
+    static constexpr int NW = mx(W_U, NWD0 + NWA) + QFT_PIPE_NW_EXTRA;
     // every warp not folding the next batch runs phase D; the items are spread
     // evenly (DPW consecutive items per warp) so no sub-partition carries a
     // full D warp more than another
