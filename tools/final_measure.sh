@@ -15,4 +15,5 @@ done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"qft_cdft_(smem|pipe)" -s 3 -c 1 -o $out/prof_c2 python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:qft_cdft_smem -s 1 -c 1 -o $out/prof_c5 python bench.py --config 5 --steps 1 --warmup 1 --no-cpu --no-e2e > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:lg_item -s 1 -c 1 -o $out/prof_c3 python bench.py --config 3 --steps 1 --warmup 1 --no-cpu --no-e2e > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:lg_item -s 1 -c 1 -o $out/prof_c4 python bench.py --config 4 --steps 1 --warmup 1 --no-cpu --no-e2e > /dev/null 2>&1
 echo done > $out/status

@@ -14,7 +14,7 @@ from collections import defaultdict
 
 src, dst, rnd = sys.argv[1], sys.argv[2], sys.argv[3]
 CFG = {2: (12, 16384, 8), 3: (16, 2048, 8), 4: (20, 64, 16), 5: (14, 1 << 18, 8)}  # log2 N, batch, bytes/cell
-FULL = {2: "prof_c2", 3: "prof_c3", 5: "prof_c5"}
+FULL = {2: "prof_c2", 3: "prof_c3", 4: "prof_c4", 5: "prof_c5"}
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
