@@ -1,8 +1,8 @@
-import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 """Stress check of the pipelined kernel (tools only): repeated full-size runs
 must be bitwise identical (a shared-memory race or a missed mbarrier phase
 shows up as run-to-run differences), and sampled rows must equal the oracle."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import sys
 import numpy as np
 import torch
