@@ -2,18 +2,28 @@
 
 Workload (BASELINE.json configs[1], the headline single-GPU config): complex
 fp32 forward DFT via the improved QFT, N = 2^12, batch 16384 per GPU, re/im
-i.i.d. N(0,1) from a seed (synthetic -- the reference names no dataset).
-A "step" is one batched transform of the whole batch.  The input (1 GiB) is
-larger than the 126 MB L2, so no flush is needed between steps.
+i.i.d. N(0,1) from the keyed device generator (synthetic -- the reference names
+no dataset; paper_1301_0763_b200/workloads.py).  A "step" is one batched
+transform of the whole batch.  The input (1 GiB) is larger than the 126 MB L2,
+so no flush is needed between steps.  ``--config k`` measures BASELINE config k.
 
-  value     transforms/s of the whole job, inputs resident in HBM, CUDA events
-            on the launching stream, max over ranks
-  e2e       transforms/s through the C-ABI host call (qft_exec_cdft_host) with
-            pinned HOST buffers: H2D + transform + D2H inside the timed region
-  roofline  the transform kernel vs the measured HBM copy bandwidth
-            (algorithmic bytes = 16 N per fp32 transform: read + write once)
-  cpu_baseline  the oracle port (oracle/, scalar C restatement of the reference
-            recursion) on the host cores, bounded sample
+  value        transforms/s of the whole job, inputs resident in HBM, CUDA
+               events on the launching stream, max over ranks
+  e2e          transforms/s through the C-ABI host call (qft_exec_cdft_host)
+               from pinned HOST buffers: H2D + transform + D2H inside the timed
+               region
+  e2e_dropin   the reference-facing drop-in improved.cdft(numpy (N, batch))
+               on an ordinary (pageable) numpy array, the reference's layout
+  roofline     the step vs the measured HBM copy bandwidth (algorithmic
+               bytes = 16 N per fp32 / 32 N per fp64 transform: read + write once)
+  parity       every row of the timed run's output against the CPU oracle
+               (oracle/, pinned to the reference), bit for bit
+  cpu_baseline the oracle port (oracle/, scalar C restatement of the reference
+               recursion) on one host thread, bounded sample; plus the
+               reference's own Python path (quickfourier.improved.cdft from the
+               pip-installed baseline/_ref) in 1 process and in P processes
+  accuracy     (config 4) fp64 rel-L2 of improved / classical vs numpy.fft and
+               vs each other
 
 ``--impl reference`` times the reference's CPU implementation of the path on
 the host cores (the oracle port, all threads) on the same config and prints
@@ -30,31 +40,31 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_PKG = os.path.join(ROOT, "baseline", "_ref")
 
-LOG2N = 12
-N = 1 << LOG2N
-BATCH = 16384
-SEED = 2
-METRIC = "batched FFT transforms/s (improved QFT, complex fp32, N=2^12)"
 UNIT = "transforms/s"
 
-# --config k selects another BASELINE.json configuration (default: config 2,
-# the headline single-GPU workload).  (log2 N, batch per GPU, precision, kind)
-CONFIG_TABLE = {
-    1: (10, 64, 64, "uniform"),
-    2: (12, 16384, 32, "normal"),
-    3: (16, 2048, 32, "sinusoids"),
-    4: (20, 64, 64, "uniform"),
-    5: (14, 1 << 18, 32, "normal"),  # whole box; per GPU batch = 2^18 / n_gpus (strong)
-}
+
+def host_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cores": len(os.sched_getaffinity(0))}
 
 
 def read_traffic(config):
     """DRAM bytes per launch of the dominant kernel from the committed ncu capture
-    (profiles/r*_summary.json), or None."""
+    (profiles/r*_summary.json, the newest that has this config), or None."""
     import glob
     best = None
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_summary.json"))):
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_summary.json")), key=os.path.getmtime)
+    for f in files:
         try:
             with open(f) as fh:
                 d = json.load(fh).get(f"config{config}")
@@ -69,9 +79,9 @@ def read_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: torch copy, read+write)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -90,9 +100,10 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            time.sleep(0.15)
         except Exception:
             self.proc = None
         return self
@@ -103,7 +114,7 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         if self.proc is not None:
-            time.sleep(0.25)
+            time.sleep(0.2)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -128,24 +139,91 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline_port(seconds, threads, prec=32):
-    """Oracle port (scalar C restatement of the reference recursion) on the host."""
+def sample_rows(c, rows):
+    """Host copy of the first `rows` rows of config c's input (the CPU legs time
+    the same data the GPU transforms)."""
     import numpy as np
+    from paper_1301_0763_b200 import workloads
+    cfg = workloads.CONFIGS[c]
+    N, seed = cfg["N"], workloads.SEEDS[c]
+    if c in (2, 5):
+        return workloads.keyed_normal_rows(N, rows, 0, seed)
+    if c == 3:
+        return workloads.config3_rows(N, rows, 0, seed)
+    if c == 4:
+        return workloads.uniform_rows(N, rows, seed, np.complex128)
+    return np.ascontiguousarray(workloads.config1_input().T[:rows])
+
+
+def cpu_baseline_port(c, seconds, threads):
+    """Oracle port (scalar C restatement of the reference recursion) on the host."""
     from oracle import oracle
-    rng = np.random.default_rng(SEED)
+    from paper_1301_0763_b200 import workloads
+    N = workloads.CONFIGS[c]["N"]
     per = max(1, min(512, (1 << 21) // N))
     sample = per * max(1, threads)
-    z = (rng.standard_normal((sample, N)) + 1j * rng.standard_normal((sample, N))).astype(
-        np.complex64 if prec == 32 else np.complex128)
-    oracle.cdft_rows(z[: min(sample, 64)], nthreads=threads)  # warm
+    z = sample_rows(c, min(sample, workloads.CONFIGS[c]["batch"]))
+    oracle.cdft_rows(z[: min(len(z), 8)], nthreads=threads)  # warm
     done, t0 = 0, time.perf_counter()
     while True:
         oracle.cdft_rows(z, nthreads=threads)
-        done += sample
+        done += len(z)
         el = time.perf_counter() - t0
         if el >= seconds:
             break
     return done / el, done, el
+
+
+_PYREF_CHILD = r"""
+import sys, time, numpy as np
+sys.path.insert(0, {ref!r})
+from quickfourier import improved
+z = np.load({path!r}, mmap_mode="r")
+lo, hi = {lo}, {hi}
+x = np.ascontiguousarray(z[lo:hi].T)
+improved.cdft(x[:, :1])
+t = time.perf_counter()
+improved.cdft(x)
+print(time.perf_counter() - t)
+"""
+
+
+def python_reference(c, seconds=6.0, procs=None):
+    """The reference's own Python path (quickfourier.improved.cdft, pip-installed
+    under baseline/_ref) timed with time.perf_counter around the call on
+    pre-generated (N, batch) arrays: 1 process, and P processes
+    each transforming a contiguous slice (slowest worker's time)."""
+    import tempfile
+
+    import numpy as np
+    from paper_1301_0763_b200 import workloads
+    if not os.path.isdir(os.path.join(REF_PKG, "quickfourier")):
+        return None
+    N = workloads.CONFIGS[c]["N"]
+    procs = procs or len(os.sched_getaffinity(0))
+    # per-process sample sized for ~`seconds` at the SURVEY.md §6 rates
+    rate = {1: 1855, 2: 2816, 3: 103, 4: 1.28, 5: 592}[c]
+    per = max(1, min(int(rate * seconds), workloads.CONFIGS[c]["batch"], (1 << 28) // (N * 16)))
+    z = sample_rows(c, per)  # every worker transforms the same i.i.d. rows
+    out = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "x.npy")
+        np.save(path, z)
+
+        def run(lo, hi):
+            code = _PYREF_CHILD.format(ref=REF_PKG, path=path, lo=lo, hi=hi)
+            return subprocess.Popen([sys.executable, "-c", code], stdout=subprocess.PIPE, text=True)
+        p = run(0, per)
+        t1 = float(p.communicate()[0].strip().splitlines()[-1])
+        out["one_process"] = {"value": per / t1, "transforms": per, "seconds": round(t1, 3)}
+        if c != 4 and procs > 1:
+            ps = [run(0, per) for _ in range(procs)]
+            ts = [float(q.communicate()[0].strip().splitlines()[-1]) for q in ps]
+            out["p_processes"] = {"value": per * procs / max(ts), "processes": procs, "transforms": per * procs,
+                                  "slowest_worker_seconds": round(max(ts), 3)}
+    out["what"] = ("quickfourier.improved.cdft (the unmodified reference, numpy), time.perf_counter around the "
+                   "call on a pre-generated (N, batch) array of the config's own rows")
+    return out
 
 
 def dist_env():
@@ -155,65 +233,112 @@ def dist_env():
     return ws, rank, local
 
 
+def config_meta(c):
+    from paper_1301_0763_b200 import workloads
+    cfg = workloads.CONFIGS[c]
+    N = cfg["N"]
+    lg = N.bit_length() - 1
+    prec = 32 if cfg["dtype"] == "complex64" else 64
+    metric = f"batched FFT transforms/s (improved QFT, complex {'fp32' if prec == 32 else 'fp64'}, N=2^{lg})"
+    return N, lg, prec, cfg, metric
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
     from oracle import oracle
+    N, lg, prec, cfg, metric = config_meta(args.config)
     threads = oracle.max_threads()
-    vals = []
-    samples = []
+    vals, samples = [], []
     for i in range(args.warmup + args.steps):
-        v, done, el = cpu_baseline_port(args.ref_seconds, threads, args.prec)
+        v, done, el = cpu_baseline_port(args.config, args.ref_seconds, threads)
         if i >= args.warmup:
             vals.append(v)
             samples.append(done)
     value = sorted(vals)[len(vals) // 2]
+    hi = host_info()
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * BATCH / value,
+        "impl": "reference", "metric": metric, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg["batch"] / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32" if args.prec == 32 else "f64", "data": "synthetic",
-        "config": {"workload": f"config{args.config}: improved-QFT cdft N=2^{LOG2N} batch {BATCH} "
-                               f"{'complex64' if args.prec == 32 else 'complex128'} {args.kind}",
-                   "N": N, "batch": BATCH, "parallelism": "host threads"},
+        "dtype": "f32" if prec == 32 else "f64", "data": "synthetic",
+        "config": {"workload": f"config{args.config}: {cfg['desc']}", "N": N, "batch": cfg["batch"],
+                   "parallelism": "host threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"bounded sample: {samples[0]} transforms of the config's shape per step "
-                                   f"(>= {args.ref_seconds}s of host work), oracle port on {threads} threads"},
+                         "cpu_model": hi["cpu_model"],
+                         "sample": f"bounded sample per step: {samples[0]} transforms of the config's own rows "
+                                   f"(>= {args.ref_seconds}s of host work), the oracle port (scalar C restatement "
+                                   f"of the reference recursion, bit-identical to it) on {threads} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def rel_l2_rows(a, b):
+    import numpy as np
+    a = np.asarray(a, dtype=np.complex128)
+    b = np.asarray(b, dtype=np.complex128)
+    return np.linalg.norm(a - b, axis=-1) / np.linalg.norm(b, axis=-1)
+
+
+def accuracy_config4(x, y, stream, steps=2):
+    """BASELINE config 4: fp64 rel-L2 of the improved QFT vs exact (numpy.fft,
+    pocketfft in fp64 -- its own error is ~1e-16, far below the 6e-14 being
+    measured), of the classical QFT vs exact, of improved vs classical, and of
+    improved vs the reference (bitwise equal: parity leg), as the paper's
+    accuracy claim asks.  Also times classical.cdft."""
+    import numpy as np
+    import torch
+    from paper_1301_0763_b200 import classical
+    yc = classical.cdft_rows(x)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        classical.cdft_rows(x, out=yc)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    cms = e0.elapsed_time(e1) / steps
+    xs, ys, cs = x.cpu().numpy(), y.cpu().numpy(), yc.cpu().numpy()
+    exact = np.fft.fft(xs, axis=1)
+    r_imp, r_cla, r_ic = rel_l2_rows(ys, exact), rel_l2_rows(cs, exact), rel_l2_rows(ys, cs)
+    return {"improved_vs_exact": {"mean": float(r_imp.mean()), "max": float(r_imp.max())},
+            "classical_vs_exact": {"mean": float(r_cla.mean()), "max": float(r_cla.max())},
+            "improved_vs_classical": {"mean": float(r_ic.mean()), "max": float(r_ic.max())},
+            "improved_vs_reference": "0 (bitwise equal on every row: see parity; rows 0-1 also pinned to the "
+                                     "reference's own output, tests/golden config_rows)",
+            "improved_over_classical_error_ratio": float(r_imp.mean() / r_cla.mean()),
+            "exact": "numpy.fft.fft of the same fp64 rows",
+            "rows": int(xs.shape[0]),
+            "classical_gpu": {"ms_per_step": cms, "value": xs.shape[0] / (cms / 1000.0), "unit": UNIT,
+                              "kernel": "qft_classical (warp-cooperative recursion, csrc/qft_classical.cu)"}}
+
+
 def main():
-    global LOG2N, N, BATCH, METRIC
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=BATCH)
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--ref-seconds", type=float, default=5.0)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIG_TABLE))
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     args = ap.parse_args()
-    lg, bt, prec, kind = CONFIG_TABLE[args.config]
-    LOG2N, N = lg, 1 << lg
-    BATCH = bt
-    ctype = "complex fp32" if prec == 32 else "complex fp64"
-    METRIC = f"batched FFT transforms/s (improved QFT, {ctype}, N=2^{lg})"
-    args.prec, args.kind = prec, kind
     if args.impl == "reference":
         return run_reference(args)
 
     import numpy as np
     import torch
 
-    from paper_1301_0763_b200 import _native, improved
+    from paper_1301_0763_b200 import _native, improved, workloads
 
+    N, lg, prec, cfg, metric = config_meta(args.config)
     ws, rank, local = dist_env()
     dist = None
     if ws > 1:
@@ -222,29 +347,16 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    B = args.batch if args.config == 2 or args.batch != 16384 else BATCH
-    scaling = "weak"
-    first = rank * B  # global index of this rank's first signal (generator key)
-    if args.config == 5:  # the box-wide batch 2^18 is split evenly (no collective)
+    if args.config == 5:  # the box-wide batch 2^18 is split evenly (strong scaling, no collective)
         from paper_1301_0763_b200.sharding import shard_bounds
-        b0, b1 = shard_bounds(BATCH, ws, rank)
-        B, first = b1 - b0, b0
-        scaling = "strong"
-    prec = args.prec
-    cdt = torch.complex64 if prec == 32 else torch.complex128
+        b0, b1 = shard_bounds(cfg["batch"], ws, rank)
+        B, first, scaling = b1 - b0, b0, "strong"
+    else:  # a full config batch per GPU, rows keyed on the global row index (weak scaling)
+        B, first, scaling = cfg["batch"], rank * cfg["batch"], "weak"
     esz = 8 if prec == 32 else 16
-    plan = _native.plan(LOG2N, prec, 0, local)
+    plan = _native.plan(lg, prec, 0, local)
     stream = torch.cuda.current_stream(dev)
-    if args.kind == "sinusoids":
-        from paper_1301_0763_b200 import workloads
-        x = workloads.config3_rows_torch(N, B, SEED + rank, dev)
-    else:
-        x = torch.empty((B, N), dtype=cdt, device=dev)
-        if args.kind == "uniform":
-            from paper_1301_0763_b200 import workloads
-            x.copy_(torch.from_numpy(workloads.uniform_rows(N, B, SEED + rank, np.complex64 if prec == 32 else np.complex128)))
-        else:
-            plan.fill_normal(x.data_ptr(), B, first, SEED, stream.cuda_stream)
+    x = workloads.config_rows_device(args.config, B, first, dev)
     y = torch.empty_like(x)
 
     def step():
@@ -264,28 +376,31 @@ def main():
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / args.steps
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    ms, per_rank = ms_local, [ms_local]
     if dist:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+        allt = [torch.empty_like(t) for _ in range(ws)]
+        dist.all_gather(allt, t)
+        per_rank = [float(a.item()) for a in allt]
+        ms = max(per_rank)
         dist.barrier()
     torch.cuda.synchronize()
-    value = ws * B / (ms / 1000.0)
+    value = (cfg["batch"] if scaling == "strong" else ws * B) / (ms / 1000.0)
 
     # e2e: the C-ABI host call with pinned host buffers (H2D + transform + D2H)
-    e2e = None
+    e2e = e2e_dropin = None
     if not args.no_e2e:
         hb = min(B, max(1, (1 << 30) // (N * esz)))
-        hin = torch.empty((hb, N), dtype=cdt, pin_memory=True)
+        hin = torch.empty((hb, N), dtype=x.dtype, pin_memory=True)
         hout = torch.empty_like(hin, pin_memory=True)
         hin.copy_(x[:hb].cpu())
         for _ in range(2):
             plan.exec_host(hin.data_ptr(), hout.data_ptr(), hb, (N, 1), (N, 1))
         if dist:
             dist.barrier()
-        t0 = time.perf_counter()
         reps = max(3, args.steps // 4)
+        t0 = time.perf_counter()
         for _ in range(reps):
             plan.exec_host(hin.data_ptr(), hout.data_ptr(), hb, (N, 1), (N, 1))
         el = (time.perf_counter() - t0) / reps
@@ -295,62 +410,94 @@ def main():
             el = float(t.item())
         e2e = {"value": ws * hb / el, "unit": UNIT, "h2d_bytes_per_step": hb * N * esz,
                "d2h_bytes_per_step": hb * N * esz, "ms_per_step": el * 1000.0, "batch_per_step": hb,
-               "path": "qft_exec_cdft_host (pinned host buffers; H2D, transform, D2H on three event-chained streams)"}
+               "path": "qft_exec_cdft_host (C ABI; pinned batch-major host buffers; H2D, transform, D2H "
+                       "chunk-pipelined on three event-chained streams)"}
+        # the reference-facing drop-in on an ordinary numpy array in the reference's (N, batch) layout
+        zn = np.ascontiguousarray(hin.numpy().T)  # pageable, (N, hb)
+        improved.cdft(zn[:, :2])
+        t0 = time.perf_counter()
+        reps_d = 2
+        for _ in range(reps_d):
+            yn = improved.cdft(zn)
+        eld = (time.perf_counter() - t0) / reps_d
+        ok = bool(np.array_equal(yn.T.view(np.uint8), hout.numpy().view(np.uint8)))
+        e2e_dropin = {"value": hb / eld, "unit": UNIT, "ms_per_step": eld * 1000.0, "batch_per_step": hb,
+                      "h2d_bytes_per_step": hb * N * esz, "d2h_bytes_per_step": hb * N * esz,
+                      "equals_c_abi_result": ok,
+                      "path": "paper_1301_0763_b200.improved.cdft(numpy (N, batch), pageable) -- the reference's "
+                              "signature and layout (improved.py:139-150); rank-local"}
+        del hin, hout, zn
 
-    # parity spot check of this run's own data (sampled rows vs the oracle)
+    # parity of this run's own output: every row against the CPU oracle
     parity = None
-    if rank == 0:
-        from oracle import oracle
-        idx = [0, B // 2, B - 1] if N <= 1 << 16 else [0, B - 1]
-        zs = x[idx].cpu().numpy()
-        ys = y[idx].cpu().numpy()
-        parity = bool(np.array_equal(ys.view(np.uint8), oracle.cdft_rows(zs, nthreads=2).view(np.uint8)))
+    if not args.no_parity:
+        from oracle import oracle, parity as par
+        thr = max(1, oracle.max_threads() // ws)
+        parity = par.check_rows(x, y, nthreads=thr)
+        if dist:
+            t = torch.tensor([parity["rows_checked"], parity["mismatches"]], device=dev, dtype=torch.int64)
+            dist.all_reduce(t)
+            parity["rows_checked"], parity["mismatches"] = int(t[0]), int(t[1])
+        parity["against"] = "oracle/ (C restatement pinned to the reference by tests/golden)"
+
+    accuracy = None
+    if args.config == 4 and rank == 0:
+        accuracy = accuracy_config4(x, y, stream)
 
     if rank == 0:
         peak, peak_kind = read_peaks()
         algo_bytes = 2 * esz * N * B
-        achieved = algo_bytes / (ms / 1000.0) / 1e9
+        achieved = algo_bytes / (ms_local / 1000.0) / 1e9
+        hi = host_info()
         cpu = None
         if not args.no_cpu:
-            from oracle import oracle
-            thr = 1
-            v, done, el = cpu_baseline_port(args.cpu_seconds, thr, prec)
-            cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "port",
-                   "sample": f"{done} transforms of config {args.config} shape (N=2^{LOG2N}) in {el:.1f}s, 1 thread"}
+            v, done, el = cpu_baseline_port(args.config, args.cpu_seconds, 1)
+            cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "cpu_model": hi["cpu_model"],
+                   "host_cores": hi["cores"],
+                   "sample": f"{done} transforms of config {args.config}'s own rows (N=2^{lg}) in {el:.1f}s, "
+                             f"1 thread, the oracle port (C restatement of the reference recursion)"}
+            try:
+                cpu["python_reference"] = python_reference(args.config)
+            except Exception as e:  # the reference install is optional
+                cpu["python_reference"] = {"error": str(e)[:200]}
         info = plan.info()
         tr = read_traffic(args.config)
+        fc = (tr or {}).get("full_capture") if B == cfg["batch"] else None
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "metric": metric, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32" if prec == 32 else "f64", "data": "synthetic",
-            "config": {"workload": f"config{args.config}: improved-QFT cdft N=2^{LOG2N} batch {B}/GPU "
-                                   f"{'complex64' if prec == 32 else 'complex128'} {args.kind}",
-                       "N": N, "batch_per_gpu": B, "parallelism": f"batch-sharded x{ws}, no collective",
+            "config": {"workload": f"config{args.config}: {cfg['desc']}", "N": N, "batch_per_gpu": B,
+                       "parallelism": f"batch-sharded x{ws}, no collective",
                        "l2": ("input > 126 MB L2 (no flush needed)" if B * N * esz > (126 << 20)
                               else "input fits L2: steps re-read a warm L2 (small config)")},
+            "per_gpu": {"value": [B / (t / 1000.0) for t in per_rank], "ms_per_step": per_rank},
             "e2e": e2e,
+            "e2e_dropin": e2e_dropin,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
-                         "traffic": (lambda d: None if not d or B != BATCH else d["traffic_bytes_per_launch"])(tr),
+                         "traffic": (tr or {}).get("traffic_bytes_per_launch") if B == cfg["batch"] else None,
                          "traffic_unit": "bytes per step: ncu dram__bytes_read.sum + dram__bytes_write.sum of the "
                                          f"step's kernels ({tr.get('_file') if tr else 'profiles/'}); algorithmic "
-                                         f"bytes per step = {2 * esz * N * B}",
-                         # the unit that actually binds the single-pass kernels: the shared-memory /
-                         # L1 data pipe (128 B/clk/SM), from the same committed ncu capture
-                         "secondary": (lambda fc: None if not fc else {
+                                         f"bytes per step = {algo_bytes}",
+                         "secondary": None if not fc else {
                              "bound": "smem (L1 data pipe, 128 B/clk/SM)",
-                             "frac": fc.get("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", 0) / 100.0,
-                             "smem_wavefronts_per_transform": fc.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 0) / B,
+                             "frac": fc.get("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+                                            0) / 100.0,
+                             "smem_wavefronts_per_transform": fc.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+                                                                     0) / B,
                              "kernel": fc.get("kernel", "").split("(")[0],
-                             "source": tr.get("_file")})((tr or {}).get("full_capture") if B == BATCH else None),
+                             "source": tr.get("_file")},
                          "dominant_kernel": tr.get("dominant_kernel") if tr else None,
                          "dominant_share_of_step": tr.get("dominant_share_of_step") if tr else None,
                          "algorithmic_bytes_per_transform": 2 * esz * N, "passes": info.passes},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": args.steps * info.kernel_launches,
-            "parity_bitwise_sampled": parity,
+            "parity": parity,
         }
+        if accuracy:
+            line["accuracy"] = accuracy
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

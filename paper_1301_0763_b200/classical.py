@@ -9,8 +9,6 @@ the exact classical op counts; ``table`` supplies the half-secants (the
 classical footprint is the N/4 - 1 secant slots, counting.py:189-205).
 """
 
-import numpy as np
-
 from . import _native, improved
 from .counting import OpCounter  # noqa: F401  (reference-compatible import)
 
@@ -28,21 +26,7 @@ def cdft(values, table=None, counter=None):
 
 def cdft_rows(x, table=None, counter=None, out=None):
     """Batch-major (batch, N) CUDA tensor, transform along the last axis."""
-    import torch
-    if not (improved._is_torch(x) and x.is_cuda):
-        raise TypeError("cdft_rows expects a CUDA torch.Tensor of shape (batch, N)")
-    B, N = x.shape
-    improved._check_n(N)
-    dtype = np.float32 if x.dtype == torch.complex64 else np.float64
-    if out is None:
-        out = torch.empty((B, N), dtype=x.dtype, device=x.device)
-    p = _native.plan(N.bit_length() - 1, 32 if dtype == np.float32 else 64, ALGO, x.device.index or 0)
-    with p.lock:
-        improved._apply_table(p, table, dtype, N, classical=True)
-        p.exec_device(x.data_ptr(), out.data_ptr(), B, (x.stride(0), x.stride(1)), (out.stride(0), out.stride(1)),
-                      torch.cuda.current_stream(x.device).cuda_stream)
-    improved._count(counter, N, B, ALGO)
-    return out
+    return improved._exec_rows(x, out, table, counter, ALGO)
 
 
 def rdft(values, table=None, counter=None):

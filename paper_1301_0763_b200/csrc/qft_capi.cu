@@ -79,18 +79,26 @@ template <typename T>
 __global__ void qft_transpose(const vec2<T> *__restrict__ src, vec2<T> *__restrict__ dst, long long rows,
                               long long cols) {
     // src is rows x cols (row-major), dst is cols x rows
+    // grid.x walks the column tiles, grid.y (capped at 65535) strides over the row tiles
     __shared__ vec2<T> tile[32][33];
-    long long c0 = (long long)blockIdx.x * 32, r0 = (long long)blockIdx.y * 32;
-    int tx = threadIdx.x, ty = threadIdx.y;
-    for (int i = ty; i < 32; i += 8) {
-        long long r = r0 + i, c = c0 + tx;
-        if (r < rows && c < cols) tile[i][tx] = src[r * cols + c];
+    const long long c0 = (long long)blockIdx.x * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (long long r0 = (long long)blockIdx.y * 32; r0 < rows; r0 += (long long)gridDim.y * 32) {
+        for (int i = ty; i < 32; i += 8) {
+            long long r = r0 + i, c = c0 + tx;
+            if (r < rows && c < cols) tile[i][tx] = src[r * cols + c];
+        }
+        __syncthreads();
+        for (int i = ty; i < 32; i += 8) {
+            long long c = c0 + i, r = r0 + tx;
+            if (r < rows && c < cols) dst[c * rows + r] = tile[tx][i];
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    for (int i = ty; i < 32; i += 8) {
-        long long c = c0 + i, r = r0 + tx;
-        if (r < rows && c < cols) dst[c * rows + r] = tile[tx][i];
-    }
+}
+static dim3 transpose_grid(long long rows, long long cols) {
+    const long long gy = (rows + 31) / 32;
+    return dim3((unsigned)((cols + 31) / 32), (unsigned)(gy < 65535 ? gy : 65535));
 }
 
 // general strided gather / scatter (rare layouts)
@@ -105,11 +113,59 @@ __global__ void qft_strided_copy(const vec2<T> *__restrict__ src, vec2<T> *__res
     }
 }
 
+// ---------------------------------------------------------------- input generator
+// Counter-based N(0,1) generator of the benchmark inputs, keyed on (seed, global
+// transform index, n) so a shard equals the same rows of a 1-GPU run.  Box-Muller
+// with ln / sin / cos evaluated by fixed polynomials in explicitly rounded IEEE
+// double ops (no library transcendentals, no FMA): the numpy twin
+// paper_1301_0763_b200/workloads.py:keyed_normal_rows performs the same op
+// sequence and reproduces every value bit for bit on the host.
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
     z += 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
     return z ^ (z >> 31);
+}
+// 1/(2k+1); (-1)^k/(2k+1)!; (-1)^k/(2k)!  (hex literals shared with the twin)
+__constant__ double kGenLn[12] = {0x1.0000000000000p+0, 0x1.5555555555555p-2, 0x1.999999999999ap-3,
+                                  0x1.2492492492492p-3, 0x1.c71c71c71c71cp-4, 0x1.745d1745d1746p-4,
+                                  0x1.3b13b13b13b14p-4, 0x1.1111111111111p-4, 0x1.e1e1e1e1e1e1ep-5,
+                                  0x1.af286bca1af28p-5, 0x1.8618618618618p-5, 0x1.642c8590b2164p-5};
+__constant__ double kGenSin[12] = {0x1.0000000000000p+0,  -0x1.5555555555555p-3, 0x1.1111111111111p-7,
+                                   -0x1.a01a01a01a01ap-13, 0x1.71de3a556c734p-19, -0x1.ae64567f544e4p-26,
+                                   0x1.6124613a86d09p-33,  -0x1.ae7f3e733b81fp-41, 0x1.952c77030ad4ap-49,
+                                   -0x1.2f49b46814157p-57, 0x1.71b8ef6dcf572p-66, -0x1.761b41316381ap-75};
+__constant__ double kGenCos[12] = {0x1.0000000000000p+0,  -0x1.0000000000000p-1, 0x1.5555555555555p-5,
+                                   -0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-16, -0x1.27e4fb7789f5cp-22,
+                                   0x1.1eed8eff8d898p-29,  -0x1.93974a8c07c9dp-37, 0x1.ae7f3e733b81fp-45,
+                                   -0x1.6827863b97d97p-53, 0x1.e542ba4020225p-62, -0x1.0ce396db7f853p-70};
+__device__ __forceinline__ double gen_ln(double u) {  // u in (0, 1]
+    const unsigned long long b = (unsigned long long)__double_as_longlong(u);
+    long long e = (long long)((b >> 52) & 0x7ff) - 1023;
+    double m = __longlong_as_double((long long)((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
+    if (m > 0x1.6a09e667f3bcdp+0) {  // sqrt(2)
+        m = __dmul_rn(m, 0.5);
+        e += 1;
+    }
+    const double s = __ddiv_rn(__dsub_rn(m, 1.0), __dadd_rn(m, 1.0)), s2 = __dmul_rn(s, s);
+    double p = kGenLn[11];
+#pragma unroll
+    for (int k = 10; k >= 0; --k) p = __dadd_rn(__dmul_rn(p, s2), kGenLn[k]);
+    return __dadd_rn(__dmul_rn((double)e, 0x1.62e42fefa39efp-1), __dmul_rn(__dmul_rn(s, p), 2.0));
+}
+__device__ __forceinline__ void gen_sincos2pi(double u, double &sn, double &cs) {  // u in [0, 1)
+    const double t = __dmul_rn(u, 4.0), qd = floor(t), f = __dsub_rn(t, qd);
+    const double x = __dmul_rn(f, 0x1.921fb54442d18p+0), x2 = __dmul_rn(x, x);  // f * pi/2
+    double ps = kGenSin[11], pc = kGenCos[11];
+#pragma unroll
+    for (int k = 10; k >= 0; --k) {
+        ps = __dadd_rn(__dmul_rn(ps, x2), kGenSin[k]);
+        pc = __dadd_rn(__dmul_rn(pc, x2), kGenCos[k]);
+    }
+    const double s = __dmul_rn(ps, x), c = pc;
+    const int q = (int)qd;
+    sn = q == 0 ? s : (q == 1 ? c : (q == 2 ? -s : -c));
+    cs = q == 0 ? c : (q == 1 ? -s : (q == 2 ? -c : s));
 }
 template <typename T>
 __global__ void qft_fill_normal_kernel(vec2<T> *out, long long batch, int N, long long first, uint64_t seed) {
@@ -119,12 +175,15 @@ __global__ void qft_fill_normal_kernel(vec2<T> *out, long long batch, int N, lon
         long long b = idx / N, n = idx % N;
         uint64_t key = splitmix64(seed ^ splitmix64((uint64_t)(first + b) * 0x100000001B3ull + (uint64_t)n));
         uint64_t k2 = splitmix64(key);
-        double u1 = ((key >> 11) + 1) * (1.0 / 9007199254740993.0);  // (0, 1]
-        double u2 = (k2 >> 11) * (1.0 / 9007199254740992.0);         // [0, 1)
-        double r = sqrt(-2.0 * log(u1));
+        const double u1 = __dmul_rn((double)((key >> 11) + 1), 0x1p-53);  // (0, 1]
+        const double u2 = __dmul_rn((double)(k2 >> 11), 0x1p-53);         // [0, 1)
+        const double r = __dsqrt_rn(__dmul_rn(-2.0, gen_ln(u1)));
         double s, c;
-        sincospi(2.0 * u2, &s, &c);
-        out[idx] = {(T)(r * c), (T)(r * s)};
+        gen_sincos2pi(u2, s, c);
+        if constexpr (sizeof(T) == 4)
+            out[idx] = {__double2float_rn(__dmul_rn(r, c)), __double2float_rn(__dmul_rn(r, s))};
+        else
+            out[idx] = {__dmul_rn(r, c), __dmul_rn(r, s)};
     }
 }
 
@@ -154,7 +213,45 @@ struct qft_plan {
     size_t arena_bytes = 0;
     void *d_lscratch = nullptr; // its scratch (two buffers of N+2 cells per signal of a chunk)
     size_t lscratch_bytes = 0;
+    // Recorded on the exec stream after the last kernel of every call; the next
+    // call's stream waits on it before its first kernel.  Calls on one plan from
+    // different streams therefore never overlap on the plan-owned scratch
+    // (d_scratch, d_lscratch, d_arena, d_host), and qft_plan_set_table waits on it
+    // before it overwrites the constants that earlier kernels may still read.
+    cudaEvent_t ev_use = nullptr;
 };
+
+// Switch to the plan's device for one ABI call and restore the caller's device
+// on every return path.
+struct DevGuard {
+    int prev = -1;
+    bool switched = false;
+    cudaError_t err = cudaSuccess;
+    explicit DevGuard(int dev) {
+        err = cudaGetDevice(&prev);
+        if (err == cudaSuccess && prev != dev) {
+            err = cudaSetDevice(dev);
+            switched = err == cudaSuccess;
+        }
+    }
+    ~DevGuard() {
+        if (switched) cudaSetDevice(prev);
+    }
+};
+#define DEV_GUARD(p)                                                                     \
+    DevGuard _dg((p)->device);                                                           \
+    if (_dg.err != cudaSuccess)                                                          \
+        return fail(QFT_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(_dg.err))
+
+// stream-order one call on the plan: wait for the previous call before, mark after
+static int use_begin(qft_plan *p, cudaStream_t st) {
+    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_use, 0));
+    return 0;
+}
+static int use_end(qft_plan *p, cudaStream_t st) {
+    CUDA_TRY(cudaEventRecord(p->ev_use, st));
+    return 0;
+}
 
 // per-instance launchers, one translation unit each (qft_inst.cu)
 #define QFT_DECL(P, L) int qft_inst_launch_##P##_##L(const LaunchArgs *, int); void qft_inst_cfg_##P##_##L(int *);
@@ -213,7 +310,10 @@ static int launch_large(qft_plan *p, int mode, const void *in, void *out, long l
     if (chunk < 1) chunk = 1;
     if (chunk > batch) chunk = batch;
     if (p->lscratch_bytes < per * (size_t)chunk) {
-        if (p->d_lscratch) cudaFree(p->d_lscratch);
+        if (p->d_lscratch) {  // grown: earlier calls may still use the old buffer
+            cudaEventSynchronize(p->ev_use);
+            cudaFree(p->d_lscratch);
+        }
         p->d_lscratch = nullptr;
         p->lscratch_bytes = 0;
         CUDA_TRY(cudaMalloc(&p->d_lscratch, per * (size_t)chunk));
@@ -250,7 +350,10 @@ static int launch_classical(qft_plan *p, int mode, const void *in, void *out, lo
     if (warps < 1) warps = 1;
     const size_t need = (size_t)warps * (size_t)cells * vb;
     if (p->arena_bytes < need) {
-        if (p->d_arena) cudaFree(p->d_arena);
+        if (p->d_arena) {  // grown: earlier calls may still use the old buffer
+            cudaEventSynchronize(p->ev_use);
+            cudaFree(p->d_arena);
+        }
         p->d_arena = nullptr;
         p->arena_bytes = 0;
         CUDA_TRY(cudaMalloc(&p->d_arena, need));
@@ -302,7 +405,8 @@ int qft_plan_create(qft_plan **out, int log2n, int prec, int algo, int device) {
     int ndev = 0;
     CUDA_TRY(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(QFT_EINVAL, "bad device ordinal");
-    CUDA_TRY(cudaSetDevice(device));
+    DevGuard _dg(device);
+    if (_dg.err != cudaSuccess) return fail(QFT_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(_dg.err));
     qft_plan *p = new qft_plan();
     p->log2n = log2n;
     p->N = 1 << log2n;
@@ -316,6 +420,8 @@ int qft_plan_create(qft_plan **out, int log2n, int prec, int algo, int device) {
     }
     cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
     int rc = 0;
+    if (cudaEventCreateWithFlags(&p->ev_use, cudaEventDisableTiming) != cudaSuccess)
+        rc = fail(QFT_ECUDA, "event creation failed");
     if (prec == QFT_PREC_F64) {
         std::vector<double> U;
         if (p->N >= 8) natural_table_f64(p->N, p->t64);
@@ -358,7 +464,11 @@ int qft_plan_create(qft_plan **out, int log2n, int prec, int algo, int device) {
 
 int qft_plan_destroy(qft_plan *p) {
     if (!p) return 0;
-    cudaSetDevice(p->device);
+    DevGuard _dg(p->device);
+    if (p->ev_use) {
+        cudaEventSynchronize(p->ev_use);
+        cudaEventDestroy(p->ev_use);
+    }
     if (p->d_U) cudaFree(p->d_U);
     if (p->d_scratch) cudaFree(p->d_scratch);
     if (p->d_lscratch) cudaFree(p->d_lscratch);
@@ -426,7 +536,9 @@ int qft_plan_set_table(qft_plan *p, const void *h_table) {
     if (!p || !h_table) return fail(QFT_EINVAL, "NULL argument");
     if (p->N < 8) return 0;
     std::lock_guard<std::mutex> lk(p->mu);
-    CUDA_TRY(cudaSetDevice(p->device));
+    DEV_GUARD(p);
+    // kernels enqueued by earlier calls (on any stream) may still read d_U / d_T
+    CUDA_TRY(cudaEventSynchronize(p->ev_use));
     if (p->prec == QFT_PREC_F64) {
         const double *t = (const double *)h_table;
         p->t64.assign(t, t + p->N / 4);
@@ -449,7 +561,10 @@ int qft_plan_set_table(qft_plan *p, const void *h_table) {
 
 static int ensure_scratch(qft_plan *p, size_t bytes) {
     if (p->scratch_bytes >= bytes) return 0;
-    if (p->d_scratch) cudaFree(p->d_scratch);
+    if (p->d_scratch) {  // grown: earlier calls may still use the old buffer
+        cudaEventSynchronize(p->ev_use);
+        cudaFree(p->d_scratch);
+    }
     p->d_scratch = nullptr;
     p->scratch_bytes = 0;
     CUDA_TRY(cudaMalloc(&p->d_scratch, bytes));
@@ -465,11 +580,11 @@ static int layout_copy(const void *src, void *dst, long long batch, int N, long 
         return 0;
     }
     if (ses == batch && sbs == 1 && dbs == N && des == 1) {  // (N, B) -> (B, N)
-        dim3 grid((unsigned)((batch + 31) / 32), (unsigned)((N + 31) / 32));
-        qft_transpose<T><<<grid, dim3(32, 8), 0, st>>>((const vec2<T> *)src, (vec2<T> *)dst, N, batch);
+        qft_transpose<T><<<transpose_grid(N, batch), dim3(32, 8), 0, st>>>((const vec2<T> *)src, (vec2<T> *)dst, N,
+                                                                           batch);
     } else if (sbs == N && ses == 1 && des == batch && dbs == 1) {  // (B, N) -> (N, B)
-        dim3 grid((unsigned)((N + 31) / 32), (unsigned)((batch + 31) / 32));
-        qft_transpose<T><<<grid, dim3(32, 8), 0, st>>>((const vec2<T> *)src, (vec2<T> *)dst, batch, N);
+        qft_transpose<T><<<transpose_grid(batch, N), dim3(32, 8), 0, st>>>((const vec2<T> *)src, (vec2<T> *)dst, batch,
+                                                                           N);
     } else {
         qft_strided_copy<T><<<num_sms * 8, 256, 0, st>>>((const vec2<T> *)src, (vec2<T> *)dst, batch, N, sbs, ses,
                                                           dbs, des);
@@ -523,9 +638,13 @@ int qft_exec_cdft(const qft_plan *cp, const void *d_in, void *d_out, int64_t bat
     if (!p || (!d_in && batch) || (!d_out && batch)) return fail(QFT_EINVAL, "NULL argument");
     if (batch < 0) return fail(QFT_EINVAL, "negative batch");
     if (d_in == d_out && batch) return fail(QFT_EINVAL, "transform is out-of-place: d_in must differ from d_out");
-    CUDA_TRY(cudaSetDevice(p->device));
+    DEV_GUARD(p);
     std::lock_guard<std::mutex> lk(p->mu);
-    return exec_impl(p, d_in, d_out, batch, ibs, ies, obs, oes, (cudaStream_t)stream);
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = use_begin(p, st);
+    if (!rc) rc = exec_impl(p, d_in, d_out, batch, ibs, ies, obs, oes, st);
+    const int rc2 = use_end(p, st);
+    return rc ? rc : rc2;
 }
 
 int qft_exec_real(const qft_plan *cp, int kind, const void *d_in, void *d_out, int64_t nrows, void *stream) {
@@ -536,23 +655,31 @@ int qft_exec_real(const qft_plan *cp, int kind, const void *d_in, void *d_out, i
     if (kind == QFT_KIND_DST0 && p->log2n < 2) return fail(QFT_EINVAL, "the sine transform needs N >= 4");
     if (nrows == 0) return 0;
     if (d_in == d_out) return fail(QFT_EINVAL, "transform is out-of-place: d_in must differ from d_out");
-    CUDA_TRY(cudaSetDevice(p->device));
+    DEV_GUARD(p);
     std::lock_guard<std::mutex> lk(p->mu);
-    if (p->algo == QFT_ALGO_CLASSICAL) return launch_classical(p, kind, d_in, d_out, (nrows + 1) / 2, nrows, (cudaStream_t)stream);
-    if (p->multipass) return launch_large(p, kind, d_in, d_out, (nrows + 1) / 2, nrows, (cudaStream_t)stream);
-    LaunchArgs a{d_in, d_out, (nrows + 1) / 2, p->d_U,
-                 p->prec == QFT_PREC_F32 ? (const void *)p->uhead32 : (const void *)p->uhead64, p->num_sms,
-                 (cudaStream_t)stream, nrows};
-    int e = kLaunch[p->prec == QFT_PREC_F32 ? 0 : 1][p->log2n](&a, kind);
-    if (e != 0) return fail(QFT_ECUDA, std::string("kernel launch: ") + cudaGetErrorString((cudaError_t)e));
-    return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = use_begin(p, st);
+    if (rc) return rc;
+    if (p->algo == QFT_ALGO_CLASSICAL) {
+        rc = launch_classical(p, kind, d_in, d_out, (nrows + 1) / 2, nrows, st);
+    } else if (p->multipass) {
+        rc = launch_large(p, kind, d_in, d_out, (nrows + 1) / 2, nrows, st);
+    } else {
+        LaunchArgs a{d_in, d_out, (nrows + 1) / 2, p->d_U,
+                     p->prec == QFT_PREC_F32 ? (const void *)p->uhead32 : (const void *)p->uhead64, p->num_sms, st,
+                     nrows};
+        int e = kLaunch[p->prec == QFT_PREC_F32 ? 0 : 1][p->log2n](&a, kind);
+        if (e != 0) rc = fail(QFT_ECUDA, std::string("kernel launch: ") + cudaGetErrorString((cudaError_t)e));
+    }
+    const int rc2 = use_end(p, st);
+    return rc ? rc : rc2;
 }
 
 int qft_exec_cdft_host(qft_plan *p, const void *h_in, void *h_out, int64_t batch, int64_t ibs, int64_t ies,
                        int64_t obs, int64_t oes) {
     if (!p || (batch && (!h_in || !h_out))) return fail(QFT_EINVAL, "NULL argument");
     if (batch <= 0) return batch == 0 ? 0 : fail(QFT_EINVAL, "negative batch");
-    CUDA_TRY(cudaSetDevice(p->device));
+    DEV_GUARD(p);
     std::lock_guard<std::mutex> lk(p->mu);
     const int N = p->N;
     const size_t esz = p->prec == QFT_PREC_F32 ? 8 : 16;
@@ -572,7 +699,10 @@ int qft_exec_cdft_host(qft_plan *p, const void *h_in, void *h_out, int64_t batch
     const size_t cbytes = (size_t)chunk * N * esz;
     // per stream: in, out, 2x layout scratch; kept in the plan across calls
     if (p->host_bytes < cbytes * 4 * NS) {
-        if (p->d_host) cudaFree(p->d_host);
+        if (p->d_host) {  // grown: earlier calls may still use the old buffer
+            cudaEventSynchronize(p->ev_use);
+            cudaFree(p->d_host);
+        }
         p->d_host = nullptr;
         p->host_bytes = 0;
         CUDA_TRY(cudaMalloc(&p->d_host, cbytes * 4 * NS));
@@ -582,6 +712,9 @@ int qft_exec_cdft_host(qft_plan *p, const void *h_in, void *h_out, int64_t batch
     // three streams: H2D copies, transforms (serialised: the plan's scratch is
     // shared), D2H copies; chunk k uses buffer slot k % NS, events chain the stages
     cudaStream_t sin = p->streams[0], scomp = p->streams[1], sout = p->streams[2];
+    // earlier device-path calls on other streams may still use the plan's scratch
+    CUDA_TRY(cudaStreamWaitEvent(sin, p->ev_use, 0));
+    CUDA_TRY(cudaStreamWaitEvent(scomp, p->ev_use, 0));
     cudaEvent_t ev_in[NS], ev_out[NS], ev_free[NS];
     for (int i = 0; i < NS; ++i) {
         CUDA_TRY(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
@@ -626,6 +759,7 @@ int qft_exec_cdft_host(qft_plan *p, const void *h_in, void *h_out, int64_t batch
         if (e == cudaSuccess) e = cudaEventRecord(ev_free[slot], sout);
         if (e != cudaSuccess) rc = fail(QFT_ECUDA, std::string("D2H: ") + cudaGetErrorString(e));
     }
+    if (cudaEventRecord(p->ev_use, sout) != cudaSuccess && !rc) rc = fail(QFT_ECUDA, "event record failed");
     for (auto &st : p->streams) {
         cudaError_t e = cudaStreamSynchronize(st);
         if (e != cudaSuccess && !rc) rc = fail(QFT_ECUDA, std::string("sync: ") + cudaGetErrorString(e));
@@ -641,7 +775,7 @@ int qft_exec_cdft_host(qft_plan *p, const void *h_in, void *h_out, int64_t batch
 int qft_fill_normal(const qft_plan *p, void *d_out, int64_t batch, int64_t first_index, uint64_t seed, void *stream) {
     if (!p || (!d_out && batch)) return fail(QFT_EINVAL, "NULL argument");
     if (batch <= 0) return 0;
-    CUDA_TRY(cudaSetDevice(p->device));
+    DEV_GUARD(p);
     cudaStream_t st = (cudaStream_t)stream;
     if (p->prec == QFT_PREC_F32)
         qft_fill_normal_kernel<float><<<p->num_sms * 16, 256, 0, st>>>((vec2<float> *)d_out, batch, p->N, first_index,

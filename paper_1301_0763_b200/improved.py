@@ -154,27 +154,50 @@ def cdft(values, table=None, counter=None):
     return _cdft_numpy(values, table, counter, ALGO)
 
 
-def cdft_rows(x, table=None, counter=None, out=None):
-    """Batch-major fast path: x is a (batch, N) CUDA tensor (complex64 or
-    complex128); the transform runs along the last axis.  Returns ``out``."""
+def _check_rows(x, out):
+    """Validate the batch-major operands of cdft_rows: a (batch, N) complex64 /
+    complex128 CUDA tensor and, if given, an ``out`` of the same dtype, shape
+    and device (the kernels write batch * N elements of x's dtype)."""
     import torch
     if not (_is_torch(x) and x.is_cuda):
         raise TypeError("cdft_rows expects a CUDA torch.Tensor of shape (batch, N)")
     if x.dtype not in (torch.complex64, torch.complex128):
         raise TypeError("cdft_rows expects complex64 or complex128")
+    if x.dim() != 2:
+        raise ValueError(f"cdft_rows expects a 2-D (batch, N) tensor, got shape {tuple(x.shape)}")
     B, N = x.shape
     _check_n(N)
-    dtype = np.float32 if x.dtype == torch.complex64 else np.float64
     if out is None:
-        out = torch.empty((B, N), dtype=x.dtype, device=x.device)
-    p = _native.plan(N.bit_length() - 1, 32 if dtype == np.float32 else 64, ALGO, x.device.index or 0)
+        return torch.empty((B, N), dtype=x.dtype, device=x.device)
+    if not (_is_torch(out) and out.is_cuda):
+        raise TypeError("out must be a CUDA torch.Tensor")
+    if out.dtype != x.dtype or tuple(out.shape) != (B, N) or out.device != x.device:
+        raise ValueError(f"out must be a {x.dtype} tensor of shape {(B, N)} on {x.device}, "
+                         f"got {out.dtype} {tuple(out.shape)} on {out.device}")
+    if B and out.data_ptr() == x.data_ptr():
+        raise ValueError("cdft_rows is out-of-place: out must not alias x")
+    return out
+
+
+def _exec_rows(x, out, table, counter, algo):
+    import torch
+    out = _check_rows(x, out)
+    B, N = x.shape
+    dtype = np.float32 if x.dtype == torch.complex64 else np.float64
+    p = _native.plan(N.bit_length() - 1, 32 if dtype == np.float32 else 64, algo, x.device.index or 0)
     stream = torch.cuda.current_stream(x.device).cuda_stream
     with p.lock:
         _apply_table(p, table, dtype, N)
         p.exec_device(x.data_ptr(), out.data_ptr(), B, (x.stride(0), x.stride(1)),
                       (out.stride(0), out.stride(1)), stream)
-    _count(counter, N, B)
+    _count(counter, N, B, algo)
     return out
+
+
+def cdft_rows(x, table=None, counter=None, out=None):
+    """Batch-major fast path: x is a (batch, N) CUDA tensor (complex64 or
+    complex128); the transform runs along the last axis.  Returns ``out``."""
+    return _exec_rows(x, out, table, counter, ALGO)
 
 
 _KINDS = {"rdft": (_native.QFT_KIND_RDFT, 2), "dct0": (_native.QFT_KIND_DCT0, 2), "dst0": (_native.QFT_KIND_DST0, 4)}

@@ -20,6 +20,7 @@ REF_SRC = "/root/reference/pkg/src"
 REF_TESTS = "/root/reference/pkg/tests"
 OUT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REF_SRC)
+sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))  # the repo (workloads generators)
 
 from quickfourier import classical, improved, reference  # noqa: E402
 from quickfourier.counting import OpCounter, TrigTable, build_trig_table  # noqa: E402
@@ -47,6 +48,11 @@ def golden_input(N, B, dt, seed):
     re = rng.standard_normal((N, B))
     im = rng.standard_normal((N, B))
     return (re + 1j * im).astype(dt)
+
+
+def real_input(n_vals, B, dt, seed):
+    """Seeded real input of the rdft / dct0 / dst0 cases: (n_vals, B), N(0,1)."""
+    return np.random.default_rng(seed).standard_normal((n_vals, B)).astype(dt)
 
 
 def config1_input():
@@ -138,6 +144,57 @@ def main():
     table = build_trig_table("improved", 64, np.float64)
     improved.cdft(golden_input(64, 1, np.complex128, 1)[:, 0], table=table, counter=OpCounter())
     meta["touched_64"] = sorted([list(k) for k in table.touched])
+
+    # 6. large improved cdft (2^17 .. 2^20) and classical cdft up to 2^16: digests
+    for dt, tag in ((np.complex128, "c128"), (np.complex64, "c64")):
+        for lg in range(17, 21):
+            N = 1 << lg
+            B = 2 if lg <= 18 else 1
+            z = golden_input(N, B, dt, 1000 + lg)
+            meta["cdft_sha256"][f"improved_{tag}_{N}"] = {"seed": 1000 + lg, "batch": B,
+                                                          "sha256": sha(improved.cdft(z))}
+        for lg in range(13, 17):
+            N = 1 << lg
+            B = 2 if lg <= 14 else 1
+            z = golden_input(N, B, dt, 1000 + lg)
+            meta["cdft_sha256"][f"classical_{tag}_{N}"] = {"seed": 1000 + lg, "batch": B,
+                                                           "sha256": sha(classical.cdft(z))}
+
+    # 7. real-input entry points rdft / dct0 / dst0 (improved.py:117-136,
+    #    classical.py:134-153): raw outputs up to 2^10, digests up to 2^16
+    meta["real_sha256"] = {}
+    for dt, tag in ((np.float64, "f64"), (np.float32, "f32")):
+        for kind in ("rdft", "dct0", "dst0"):
+            for lg in range(1 if kind != "dst0" else 2, 17):
+                N = 1 << lg
+                n_vals = {"rdft": N, "dct0": N // 2 + 1, "dst0": N // 2 - 1}[kind]
+                B = 3 if lg <= 10 else (2 if lg <= 14 else 1)
+                x = real_input(n_vals, B, dt, 2000 + lg)
+                for algo, mod in (("improved", improved), ("classical", classical)):
+                    y = getattr(mod, kind)(x)
+                    key = f"{algo}_{kind}_{tag}_{N}"
+                    if lg <= 10:
+                        arrays[f"in_{kind}_{tag}_{N}"] = x
+                        arrays[key] = y
+                    meta["real_sha256"][key] = {"seed": 2000 + lg, "batch": B, "n_vals": n_vals, "sha256": sha(y)}
+
+    # 8. the BASELINE configurations' own inputs (rows 0 and 1 of each, from the
+    #    generators bench.py and the -m gpu tests use): input and reference-output
+    #    digests, batch-major rows transformed as (N, 2) columns
+    from paper_1301_0763_b200 import workloads
+    meta["config_rows"] = {}
+    rows = {
+        2: workloads.keyed_normal_rows(1 << 12, 2, 0, workloads.SEEDS[2], np.complex64),
+        3: workloads.config3_rows(1 << 16, 2, 0, workloads.SEEDS[3]),
+        4: workloads.uniform_rows(1 << 20, 2, workloads.SEEDS[4], np.complex128),
+        5: workloads.keyed_normal_rows(1 << 14, 2, 0, workloads.SEEDS[5], np.complex64),
+    }
+    for c, x in rows.items():
+        y = improved.cdft(np.ascontiguousarray(x.T)).T
+        meta["config_rows"][str(c)] = {"N": int(x.shape[1]), "rows": [0, 1], "seed": workloads.SEEDS[c],
+                                       "input_sha256": sha(x), "improved_sha256": sha(np.ascontiguousarray(y))}
+    meta["config_rows"]["4"]["classical_sha256"] = sha(np.ascontiguousarray(
+        classical.cdft(np.ascontiguousarray(rows[4].T)).T))
 
     np.savez_compressed(os.path.join(OUT, "golden.npz"), **arrays)
     with open(os.path.join(OUT, "golden.json"), "w") as fh:
