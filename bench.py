@@ -414,13 +414,13 @@ def main():
                        "chunk-pipelined on three event-chained streams)"}
         # the reference-facing drop-in on an ordinary numpy array in the reference's (N, batch) layout
         zn = np.ascontiguousarray(hin.numpy().T)  # pageable, (N, hb)
-        improved.cdft(zn[:, :2])
+        improved.cdft(zn)  # warm: sizes the plan's pinned staging ring for this batch
         t0 = time.perf_counter()
         reps_d = 2
         for _ in range(reps_d):
             yn = improved.cdft(zn)
         eld = (time.perf_counter() - t0) / reps_d
-        ok = bool(np.array_equal(yn.T.view(np.uint8), hout.numpy().view(np.uint8)))
+        ok = bool(np.ascontiguousarray(yn.T).tobytes() == hout.numpy().tobytes())
         e2e_dropin = {"value": hb / eld, "unit": UNIT, "ms_per_step": eld * 1000.0, "batch_per_step": hb,
                       "h2d_bytes_per_step": hb * N * esz, "d2h_bytes_per_step": hb * N * esz,
                       "equals_c_abi_result": ok,

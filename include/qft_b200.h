@@ -111,9 +111,12 @@ int qft_exec_cdft_host(qft_plan *plan, const void *h_in, void *h_out, int64_t ba
                        int64_t in_batch_stride, int64_t in_elem_stride,
                        int64_t out_batch_stride, int64_t out_elem_stride);
 
-/* Device-side seeded input generator for the sharded benchmark (config 5):
- * re, im ~ N(0,1) from a counter-based hash of (seed, global transform index,
- * n), with a numpy twin in paper_1301_0763_b200/sharding.py. */
+/* Device-side seeded input generator of the benchmark inputs (configs 2, 5):
+ * re, im ~ N(0,1) by Box-Muller from a counter-based hash (splitmix64) of
+ * (seed, global transform index first_index + b, n), with ln / sin / cos as fixed
+ * polynomials in explicitly rounded double ops.  Its numpy twin
+ * paper_1301_0763_b200/workloads.py:keyed_normal_rows reproduces every value bit
+ * for bit on the host, so any shard or sampled row regenerates there. */
 int qft_fill_normal(const qft_plan *plan, void *d_out, int64_t batch, int64_t first_index,
                     uint64_t seed, void *stream);
 

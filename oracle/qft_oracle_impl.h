@@ -34,7 +34,7 @@ static void FN(imp_dst)(CTX *c, const R *x, int N, R *out);
 static void FN(imp_dst_ot)(CTX *c, const R *x, int N, R *out);
 static void FN(imp_dst_oo)(CTX *c, const R *x, int N, R *out);
 
-/* improved.py:36-46 with elaborations.py:58-59 (forward) and :329-334 (backward) */
+/* improved.py:36-46 with elaborations.py:58-59 (forward) and :78-83 (backward) */
 static void FN(imp_dct)(CTX *c, const R *x, int N, R *out) {
     if (N == 2) {
         out[0] = x[0] + x[1];
@@ -55,7 +55,7 @@ static void FN(imp_dct)(CTX *c, const R *x, int N, R *out) {
     c->ar->used = mark;
 }
 
-/* improved.py:49-56 with elaborations.py:364-367 (fold) and :388-391 (interleave) */
+/* improved.py:49-56 with elaborations.py:113-116 (fold) and :137-140 (interleave) */
 static void FN(imp_dct_ot)(CTX *c, const R *x, int N, R *out) {
     int q = N / 4;
     if (N == 4) {
@@ -96,7 +96,7 @@ static void FN(imp_dct_oo)(CTX *c, const R *x, int N, R *out) {
     c->ar->used = mark;
 }
 
-/* improved.py:77-84 with elaborations.py:60-62 (forward) and :335-340 (backward) */
+/* improved.py:77-84 with elaborations.py:60-62 (forward) and :84-89 (backward) */
 static void FN(imp_dst)(CTX *c, const R *x, int N, R *out) {
     if (N == 4) {
         out[0] = x[0];
@@ -117,7 +117,7 @@ static void FN(imp_dst)(CTX *c, const R *x, int N, R *out) {
     c->ar->used = mark;
 }
 
-/* improved.py:87-94 with elaborations.py:374-377 and :396-399 */
+/* improved.py:87-94 with elaborations.py:123-126 and :145-148 */
 static void FN(imp_dst_ot)(CTX *c, const R *x, int N, R *out) {
     int q = N / 4;
     if (N == 4) {
@@ -164,7 +164,7 @@ static void FN(cla_dct_odd)(CTX *c, const R *x, int N, R *out);
 static void FN(cla_dst)(CTX *c, const R *x, int N, R *out);
 static void FN(cla_dst_odd)(CTX *c, const R *x, int N, R *out);
 
-/* classical.py:64-74 with elaborations.py:347-352 and :384-387 */
+/* classical.py:64-74 with elaborations.py:96-101 and :133-136 */
 static void FN(cla_dct)(CTX *c, const R *x, int N, R *out) {
     if (N == 2) {
         out[0] = x[0] + x[1];
@@ -188,7 +188,7 @@ static void FN(cla_dct)(CTX *c, const R *x, int N, R *out) {
     c->ar->used = mark;
 }
 
-/* classical.py:77-99 with elaborations.py:353-363 (dc_t1t fold) */
+/* classical.py:77-99 with elaborations.py:102-112 (dc_t1t fold) */
 static void FN(cla_dct_odd)(CTX *c, const R *x, int N, R *out) {
     if (N == 4) {
         out[0] = x[0];
@@ -226,7 +226,7 @@ static void FN(cla_dct_odd)(CTX *c, const R *x, int N, R *out) {
     c->ar->used = mark;
 }
 
-/* classical.py:102-109 with elaborations.py:368-373 and :392-395 */
+/* classical.py:102-109 with elaborations.py:117-122 and :141-144 */
 static void FN(cla_dst)(CTX *c, const R *x, int N, R *out) {
     if (N == 4) {
         out[0] = x[0];

@@ -10,8 +10,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/qft_b200.h"
@@ -201,9 +204,12 @@ struct qft_plan {
     void *d_scratch = nullptr;
     size_t scratch_bytes = 0;
     static constexpr int kHostStreams = 3;
+    static constexpr int kHostSlots = 4;  // host path: chunks in flight
     cudaStream_t streams[kHostStreams] = {nullptr, nullptr, nullptr};
-    void *d_host = nullptr;     // host path staging (per stream: in, out, 2x layout scratch)
+    void *d_host = nullptr;     // host path device buffers (per slot: in, out, 2x layout scratch)
     size_t host_bytes = 0;
+    void *h_pin = nullptr;      // host path pinned staging ring for pageable buffers (per slot: in, out)
+    size_t pin_bytes = 0;
     std::mutex mu;
     void *large = nullptr;      // multi-pass schedule
     void *large_real = nullptr; // its real-mode variant (fold pass over every block), built on first use
@@ -307,6 +313,13 @@ static int launch_large(qft_plan *p, int mode, const void *in, void *out, long l
     const long long cells = p->prec == QFT_PREC_F32 ? qft_large_scratch_cells_f32(lp) : qft_large_scratch_cells_f64(lp);
     const size_t per = 2 * (size_t)cells * esz;
     long long chunk = (long long)(((size_t)6 << 30) / per);
+#ifdef QFT_LARGE_L2_MB
+    // experiment: sub-batches whose scratch stays L2-resident across the passes
+    {
+        const long long l2c = (long long)(((size_t)QFT_LARGE_L2_MB << 20) / per);
+        if (l2c < chunk) chunk = l2c;
+    }
+#endif
     if (chunk < 1) chunk = 1;
     if (chunk > batch) chunk = batch;
     if (p->lscratch_bytes < per * (size_t)chunk) {
@@ -475,6 +488,7 @@ int qft_plan_destroy(qft_plan *p) {
     if (p->d_T) cudaFree(p->d_T);
     if (p->d_arena) cudaFree(p->d_arena);
     if (p->d_host) cudaFree(p->d_host);
+    if (p->h_pin) cudaFreeHost(p->h_pin);
     for (void *lp : {p->large, p->large_real}) {
         if (!lp) continue;
         if (p->prec == QFT_PREC_F32) qft_large_destroy_f32(lp);
@@ -675,6 +689,97 @@ int qft_exec_real(const qft_plan *cp, int kind, const void *d_in, void *d_out, i
     return rc ? rc : rc2;
 }
 
+// ============================================================== host path
+// Host worker pool for the pageable-memory host path: the calling thread plus
+// up to 15 workers run one parallel_for at a time (the copies between ordinary
+// pageable host memory and the plan's pinned staging ring).
+class HostPool {
+  public:
+    static HostPool &get() {
+        static HostPool pool;
+        return pool;
+    }
+    int size() const { return (int)th_.size() + 1; }
+    // f(part, nparts) on every thread of the pool (part 0 on the caller)
+    void run(const std::function<void(int, int)> &f) {
+        std::lock_guard<std::mutex> one(run_mu_);
+        const int n = size();
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            job_ = &f;
+            pending_ = n - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        f(0, n);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto &t : th_) t.join();
+    }
+
+  private:
+    HostPool() {
+        int hw = (int)std::thread::hardware_concurrency();
+        int n = hw < 2 ? 1 : (hw > 16 ? 16 : hw);
+        for (int i = 1; i < n; ++i) th_.emplace_back([this, i] { loop(i); });
+    }
+    void loop(int idx) {
+        int seen = 0;
+        for (;;) {
+            const std::function<void(int, int)> *job;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+                job = job_;
+            }
+            (*job)(idx, size());
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex mu_, run_mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int, int)> *job_ = nullptr;
+    int gen_ = 0, pending_ = 0;
+    bool stop_ = false;
+};
+
+// rows x width bytes: dst[r*dpitch ..] <- src[r*spitch ..], split over the pool
+static void parallel_copy2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t rows) {
+    if (rows == 1) {  // one contiguous run: split it by bytes
+        HostPool::get().run([&](int part, int n) {
+            const size_t lo = width * part / n, hi = width * (part + 1) / n;
+            if (hi > lo) memcpy((char *)dst + lo, (const char *)src + lo, hi - lo);
+        });
+        return;
+    }
+    HostPool::get().run([&](int part, int n) {
+        const size_t lo = rows * part / n, hi = rows * (part + 1) / n;
+        for (size_t r = lo; r < hi; ++r) memcpy((char *)dst + r * dpitch, (const char *)src + r * spitch, width);
+    });
+}
+
+static bool is_pinned(const void *h) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+        cudaGetLastError();  // clear: an unknown host pointer is pageable memory
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
 int qft_exec_cdft_host(qft_plan *p, const void *h_in, void *h_out, int64_t batch, int64_t ibs, int64_t ies,
                        int64_t obs, int64_t oes) {
     if (!p || (batch && (!h_in || !h_out))) return fail(QFT_EINVAL, "NULL argument");
@@ -687,17 +792,20 @@ int qft_exec_cdft_host(qft_plan *p, const void *h_in, void *h_out, int64_t batch
     const bool ref_in = (ies == batch && ibs == 1), ref_out = (oes == batch && obs == 1);
     if (!(batch_major_in || ref_in) || !(batch_major_out || ref_out))
         return fail(QFT_EINVAL, "host path supports batch-major or (N, batch) layouts only");
+    // pageable host buffers are staged through the plan's pinned ring by the
+    // host worker pool (a driver-staged pageable DMA runs at ~1/5 of PCIe)
+    const bool stage_in = !is_pinned(h_in), stage_out = !is_pinned(h_out);
     for (auto &s : p->streams)
         if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    // chunk the batch over kHostStreams streams: the H2D copy, transform and D2H
-    // copy of different chunks overlap (both copy directions run concurrently)
-    constexpr int NS = qft_plan::kHostStreams;
+    // chunk the batch over NS buffer slots: the host copies, H2D copy, transform
+    // and D2H copy of different chunks overlap (both copy directions run concurrently)
+    constexpr int NS = qft_plan::kHostSlots;
     const size_t target = (size_t)32 << 20;  // bytes per chunk
     long long chunk = (long long)(target / ((size_t)N * esz));
     if (chunk < 1) chunk = 1;
     if (chunk > batch) chunk = batch;
     const size_t cbytes = (size_t)chunk * N * esz;
-    // per stream: in, out, 2x layout scratch; kept in the plan across calls
+    // per slot: in, out, 2x layout scratch; kept in the plan across calls
     if (p->host_bytes < cbytes * 4 * NS) {
         if (p->d_host) {  // grown: earlier calls may still use the old buffer
             cudaEventSynchronize(p->ev_use);
@@ -708,9 +816,16 @@ int qft_exec_cdft_host(qft_plan *p, const void *h_in, void *h_out, int64_t batch
         CUDA_TRY(cudaMalloc(&p->d_host, cbytes * 4 * NS));
         p->host_bytes = cbytes * 4 * NS;
     }
-    void *bufs = p->d_host;
-    // three streams: H2D copies, transforms (serialised: the plan's scratch is
-    // shared), D2H copies; chunk k uses buffer slot k % NS, events chain the stages
+    if ((stage_in || stage_out) && p->pin_bytes < cbytes * 2 * NS) {
+        if (p->h_pin) cudaFreeHost(p->h_pin);  // the previous call synchronised before returning
+        p->h_pin = nullptr;
+        p->pin_bytes = 0;
+        CUDA_TRY(cudaHostAlloc(&p->h_pin, cbytes * 2 * NS, cudaHostAllocPortable));
+        p->pin_bytes = cbytes * 2 * NS;
+    }
+    char *bufs = (char *)p->d_host;
+    // streams: H2D copies, transforms (serialised: the plan's scratch is shared),
+    // D2H copies; chunk k uses buffer slot k % NS, events chain the stages
     cudaStream_t sin = p->streams[0], scomp = p->streams[1], sout = p->streams[2];
     // earlier device-path calls on other streams may still use the plan's scratch
     CUDA_TRY(cudaStreamWaitEvent(sin, p->ev_use, 0));
@@ -721,20 +836,47 @@ int qft_exec_cdft_host(qft_plan *p, const void *h_in, void *h_out, int64_t batch
         CUDA_TRY(cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming));
         CUDA_TRY(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming));
     }
+    const long long nchunks = (batch + chunk - 1) / chunk;
+    auto cols = [&](long long k) { return (batch - k * chunk) < chunk ? (batch - k * chunk) : chunk; };
+    // host side of chunk k's output: pinned staging slot -> the caller's buffer
+    auto copy_out = [&](long long k) -> int {
+        const int slot = (int)(k % NS);
+        const long long b0 = k * chunk, nb = cols(k);
+        CUDA_TRY(cudaEventSynchronize(ev_free[slot]));
+        const char *src = (const char *)p->h_pin + (2 * slot + 1) * cbytes;
+        if (batch_major_out)
+            parallel_copy2d((char *)h_out + (size_t)b0 * N * esz, 0, src, 0, (size_t)nb * N * esz, 1);
+        else
+            parallel_copy2d((char *)h_out + (size_t)b0 * esz, (size_t)batch * esz, src, (size_t)nb * esz,
+                            (size_t)nb * esz, (size_t)N);
+        return 0;
+    };
+    constexpr int LAG = NS - 1;  // chunks in flight between the host copy-in and copy-out
     int rc = 0;
-    for (long long b0 = 0, it = 0; b0 < batch && !rc; b0 += chunk, ++it) {
-        const long long nb = (batch - b0) < chunk ? (batch - b0) : chunk;
+    for (long long it = 0; it < nchunks && !rc; ++it) {
+        const long long b0 = it * chunk, nb = cols(it);
         const int slot = (int)(it % NS);
-        char *din = (char *)bufs + slot * 4 * cbytes, *dout = din + cbytes, *dscr = din + 2 * cbytes;
+        char *din = bufs + slot * 4 * cbytes, *dout = din + cbytes, *dscr = din + 2 * cbytes;
         cudaError_t e = cudaSuccess;
         if (it >= NS) e = cudaStreamWaitEvent(sin, ev_free[slot], 0);  // slot's previous D2H done
         if (e == cudaSuccess) {
-            if (batch_major_in)
-                e = cudaMemcpyAsync(din, (const char *)h_in + (size_t)b0 * N * esz, (size_t)nb * N * esz,
-                                    cudaMemcpyHostToDevice, sin);
-            else  // columns [b0, b0+nb) of the (N, batch) array -> (N, nb) pitched
-                e = cudaMemcpy2DAsync(din, (size_t)nb * esz, (const char *)h_in + (size_t)b0 * esz,
-                                      (size_t)batch * esz, (size_t)nb * esz, (size_t)N, cudaMemcpyHostToDevice, sin);
+            const char *hsrc = (const char *)h_in + (batch_major_in ? (size_t)b0 * N * esz : (size_t)b0 * esz);
+            if (stage_in) {
+                // the staging slot's previous H2D copy must be done before the host rewrites it
+                char *pin = (char *)p->h_pin + 2 * slot * cbytes;
+                if (it >= NS) e = cudaEventSynchronize(ev_in[slot]);
+                if (batch_major_in)
+                    parallel_copy2d(pin, 0, hsrc, 0, (size_t)nb * N * esz, 1);
+                else  // columns [b0, b0+nb) of the (N, batch) array -> (N, nb) contiguous
+                    parallel_copy2d(pin, (size_t)nb * esz, hsrc, (size_t)batch * esz, (size_t)nb * esz, (size_t)N);
+                if (e == cudaSuccess)
+                    e = cudaMemcpyAsync(din, pin, (size_t)nb * N * esz, cudaMemcpyHostToDevice, sin);
+            } else if (batch_major_in) {
+                e = cudaMemcpyAsync(din, hsrc, (size_t)nb * N * esz, cudaMemcpyHostToDevice, sin);
+            } else {  // columns [b0, b0+nb) of the (N, batch) array -> (N, nb) pitched
+                e = cudaMemcpy2DAsync(din, (size_t)nb * esz, hsrc, (size_t)batch * esz, (size_t)nb * esz, (size_t)N,
+                                      cudaMemcpyHostToDevice, sin);
+            }
         }
         if (e == cudaSuccess) e = cudaEventRecord(ev_in[slot], sin);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(scomp, ev_in[slot], 0);
@@ -749,7 +891,10 @@ int qft_exec_cdft_host(qft_plan *p, const void *h_in, void *h_out, int64_t batch
         e = cudaEventRecord(ev_out[slot], scomp);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, ev_out[slot], 0);
         if (e == cudaSuccess) {
-            if (batch_major_out)
+            if (stage_out)  // contiguous into the pinned slot; copy_out scatters it later
+                e = cudaMemcpyAsync((char *)p->h_pin + (2 * slot + 1) * cbytes, dout, (size_t)nb * N * esz,
+                                    cudaMemcpyDeviceToHost, sout);
+            else if (batch_major_out)
                 e = cudaMemcpyAsync((char *)h_out + (size_t)b0 * N * esz, dout, (size_t)nb * N * esz,
                                     cudaMemcpyDeviceToHost, sout);
             else
@@ -757,8 +902,15 @@ int qft_exec_cdft_host(qft_plan *p, const void *h_in, void *h_out, int64_t batch
                                       (size_t)nb * esz, (size_t)N, cudaMemcpyDeviceToHost, sout);
         }
         if (e == cudaSuccess) e = cudaEventRecord(ev_free[slot], sout);
-        if (e != cudaSuccess) rc = fail(QFT_ECUDA, std::string("D2H: ") + cudaGetErrorString(e));
+        if (e != cudaSuccess) {
+            rc = fail(QFT_ECUDA, std::string("D2H: ") + cudaGetErrorString(e));
+            break;
+        }
+        // the output slot of chunk it-LAG+NS ... is reused NS chunks later: drain chunk it-LAG now
+        if (stage_out && it >= LAG) rc = copy_out(it - LAG);
     }
+    if (stage_out && !rc)
+        for (long long k = nchunks > LAG ? nchunks - LAG : 0; k < nchunks && !rc; ++k) rc = copy_out(k);
     if (cudaEventRecord(p->ev_use, sout) != cudaSuccess && !rc) rc = fail(QFT_ECUDA, "event record failed");
     for (auto &st : p->streams) {
         cudaError_t e = cudaStreamSynchronize(st);

@@ -49,7 +49,7 @@ __device__ void cl_dct_odd(Ctx &c, const V *x, int N, V *out);
 __device__ void cl_dst(Ctx &c, const V *x, int N, V *out);
 __device__ void cl_dst_odd(Ctx &c, const V *x, int N, V *out);
 
-// classical._dct (classical.py:64-74): harmonic split of dc_tt (elaborations.py:347-352)
+// classical._dct (classical.py:64-74): harmonic split of dc_tt (elaborations.py:96-101)
 __device__ __noinline__ void cl_dct(Ctx &c, const V *x, int N, V *out) {
     const int L = c.lane;
     if (N == 2) {
@@ -105,7 +105,7 @@ __device__ __noinline__ void cl_dct_odd(Ctx &c, const V *x, int N, V *out) {
     const int q2 = N / 8, m2 = N / 4;
     V *even = alloc(c, q2 + 1), *odd = alloc(c, q2);
     if (L == 0) {
-        even[0] = vadd(conv[0], V{(Real)0, (Real)0});  // the explicit zero pair (elaborations.py:358-359)
+        even[0] = vadd(conv[0], V{(Real)0, (Real)0});  // the explicit zero pair (elaborations.py:107-108)
         odd[0] = vsub(conv[0], V{(Real)0, (Real)0});
         even[q2] = conv[q2];
     }
@@ -127,7 +127,7 @@ __device__ __noinline__ void cl_dct_odd(Ctx &c, const V *x, int N, V *out) {
     c.used = mark;
 }
 
-// classical._dst (classical.py:102-109): harmonic split of ds_tt (elaborations.py:368-373)
+// classical._dst (classical.py:102-109): harmonic split of ds_tt (elaborations.py:117-122)
 __device__ __noinline__ void cl_dst(Ctx &c, const V *x, int N, V *out) {
     const int L = c.lane;
     if (N == 4) {

@@ -143,7 +143,7 @@ QFT_HD int ctz32(uint32_t v) {
 
 // Position of element `t` of input slot `s` of an r-level reflection group
 // of a Lee block of size L is c + sg*t.  Restates the fold pairing of
-// elaborations.py:364-377 (element i with L-1-i) applied r times; every slot
+// elaborations.py:113-126 (element i with L-1-i) applied r times; every slot
 // is a contiguous (possibly reversed) run, and the runs tile the block.
 QFT_HD void run_of(int r, int L, int s, int &c, int &sg) {
     int A = 0, B = 1;

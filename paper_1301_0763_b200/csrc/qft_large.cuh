@@ -13,7 +13,7 @@
 //   B(d)   backward levels (neighbour sums + interleave), deepest first,
 //          ping-pong W0 <-> W1, output in natural spectrum order
 //   chain  time-split chain levels J0-1 .. 0 + complex recombination -> y
-//          (elaborations.py:329-340, shared.py:58-72)
+//          (elaborations.py:78-89, shared.py:58-72)
 // The host plan builder (qft_large_plan.h) compiles the decomposition tree of
 // the reference recursion into these task lists.
 #pragma once

@@ -93,7 +93,7 @@ QFT_HD void lee_fwd(vec2<T> *v, int t, const T *U) {
 // ---------------------------------------------------------------------------
 // R backward levels for column i of 2^R sub-block spectra (the neighbour sums
 // of improved.py:72-73 / :110-111 and the free interleaves of
-// elaborations.py:388-399).  v[p] = Z_p[i] (p relative to absolute index pofs);
+// elaborations.py:137-148).  v[p] = Z_p[i] (p relative to absolute index pofs);
 // halo(p) returns Z_p[i+1] (DCT) or Z_p[i-1] (DST) for absolute p -- the halo is
 // always a raw sub-block value because the first element of the next column's
 // range is reached through copies only.  edge: i is the last (DCT) / first
@@ -176,7 +176,7 @@ QFT_HD void dst0_reg(const vec2<T> *x, vec2<T> *out, const T *U) {
     }
 }
 
-// Complex recombination of one harmonic pair (shared.py:214-221):
+// Complex recombination of one harmonic pair (shared.py:64-71):
 // cv = (C1(k), C2(k)) cosine spectra of the Re/Im parts, sv = (S1(k), S2(k))
 // sine spectra.  The reference forms Re S(k) = C1 - (-S2) etc.; x - (-y) is
 // x + y bit for bit in IEEE arithmetic.

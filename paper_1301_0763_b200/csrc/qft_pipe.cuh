@@ -35,6 +35,26 @@
 #ifndef QFT_PIPE_NWA
 #define QFT_PIPE_NWA 5  // warps running the in-place A0 of the next batch during D
 #endif
+#ifndef QFT_PIPE_TMA_EARLY
+// refill TMA of the consumed buffer set issued by warp 0 as soon as the D warps
+// are done (named barrier), instead of after the CTA barrier at the head of the
+// next units phase (where warp 0 runs a unit on the critical path)
+#define QFT_PIPE_TMA_EARLY 0
+#endif
+#ifndef QFT_PIPE_UMAP
+#define QFT_PIPE_UMAP 1  // measured +0.3 % (55.13 vs 54.91M tr/s, 3 interleaved rounds)
+#endif
+#ifndef QFT_PIPE_TMA_WARP
+// warp issuing the refill TMA after the phase-2 barrier: an A0 warp has no
+// outstanding global stores for its fence.proxy.async to drain (a D warp does)
+#define QFT_PIPE_TMA_WARP 0
+#endif
+#ifndef QFT_PIPE_ITEMS
+// A0 items n = 64c: their samples x[64c] / x[N-64c] come from the chunk loads
+// (chunk c lane 0 / chunk c-1 lane 31) through a small per-slot array, instead of
+// 32 loads at stride 64 cells (all in one bank: 16-way conflicts)
+#define QFT_PIPE_ITEMS 0  // measured -6 % (51.6 vs 54.9M tr/s): the items then wait on the named barrier
+#endif
 
 // probe marks of the dataflow kernel, individually selectable (tools/probe)
 #if defined(QFT_PROBE) && !defined(QFT_PMASK)
@@ -91,7 +111,9 @@ struct PCfg {
     static constexpr int RA = (NC64 + NWA - 1) / NWA;
     static constexpr int X_OFF = 0;
     static constexpr int U_OFF = 2 * (TT > 0 ? TT : 1) * PER_W;
-    static constexpr int BAR_OFF = (U_OFF + UB + 15) / 16 * 16;
+    static constexpr int ITM_OFF = (U_OFF + UB + 15) / 16 * 16;  // per slot: x[64c], x[N-64c], c < NC64
+    static constexpr int ITM_BYTES = QFT_PIPE_ITEMS ? (TT > 0 ? TT : 1) * 2 * (P::m / 64) * VB : 0;
+    static constexpr int BAR_OFF = (ITM_OFF + ITM_BYTES + 15) / 16 * 16;
     static constexpr int SMEM = BAR_OFF + 64;  // 5 mbarriers
 };
 
@@ -135,7 +157,7 @@ QFT_DEV void tma_load_slots(vec2<T> *X, const vec2<T> *src, int ntr, uint64_t *b
 // (chunks of 64 samples + the items n = 64c) into registers, named barrier,
 // every store (same fold / route as a0_complex).
 template <int LOG2N, typename T>
-QFT_DEV void a0_inplace(vec2<T> *X, int ntr, int ga, const A0Lane64 &a0l64) {
+QFT_DEV void a0_inplace(vec2<T> *X, int ntr, int ga, const A0Lane64 &a0l64, vec2<T> *itm = nullptr) {
     using P = SPlan<LOG2N>;
     using C = PCfg<LOG2N, T>;
     constexpr int NWA = C::NWA, NC64 = C::NC64, RA = C::RA;
@@ -151,11 +173,30 @@ QFT_DEV void a0_inplace(vec2<T> *X, int ntr, int ga, const A0Lane64 &a0l64) {
         }
         const bool item = ga < NC64;  // n = 64 ga (ga = 0: the base pair)
         vec2<T> ia, ib;
-        if (item) {
-            ia = s[64 * ga];
-            ib = s[ga == 0 ? P::m : P::N - 64 * ga];
+        if constexpr (QFT_PIPE_ITEMS) {
+            // chunk c: lane 0 loaded x[64c] (xe), lane 31 loaded x[N - 64(c+1)] (mn),
+            // the mirror of item c+1 (item 0's partner is x[m] = chunk NC64-1's mn)
+            vec2<T> *ia_s = itm + tau * 2 * NC64, *ib_s = ia_s + NC64;
+#pragma unroll
+            for (int r = 0; r < RA; ++r) {
+                const int c = gw + r * NWA;
+                if (c < NC64) {
+                    if (lane == 0) ia_s[c] = ch[r].xe;
+                    if (lane == 31) ib_s[c + 1 < NC64 ? c + 1 : 0] = ch[r].mn;
+                }
+            }
+            named_bar(1, NWA * 32);
+            if (item) {
+                ia = ia_s[ga];
+                ib = ib_s[ga];
+            }
+        } else {
+            if (item) {
+                ia = s[64 * ga];
+                ib = s[ga == 0 ? P::m : P::N - 64 * ga];
+            }
+            named_bar(1, NWA * 32);
         }
-        named_bar(1, NWA * 32);
 #pragma unroll
         for (int r = 0; r < RA; ++r) {
             const int c = gw + r * NWA;  // warp-uniform: the store's shuffle sees the whole warp
@@ -186,6 +227,7 @@ __global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     vec2<T> *X0 = reinterpret_cast<vec2<T> *>(smem_raw + C::X_OFF);
     T *U = reinterpret_cast<T *>(smem_raw + C::U_OFF);
+    vec2<T> *itm = reinterpret_cast<vec2<T> *>(smem_raw + C::ITM_OFF);
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::BAR_OFF);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool a0_warp = warp >= NWD && warp < NWD + NWA;
@@ -194,6 +236,10 @@ __global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
     const long long nbatch = (batch + TT - 1) / TT, G = gridDim.x;
     auto ntr_of = [&](long long b) { return (int)((batch - b * TT) < TT ? (batch - b * TT) : TT); };
     auto set = [&](int s) { return X0 + s * TT * P::PADDED; };
+    // unit of this warp in the units phase: warp w runs on SM sub-partition w % 4;
+    // QFT_PIPE_UMAP rotates the unit kind (big cos / big sin / rest cos / rest sin)
+    // by the signal index so no sub-partition gets three of the heavier rest units
+    const int uwarp = (QFT_PIPE_UMAP && C::NU == 4 && NW == TT * 4) ? ((warp & ~3) | ((warp + (warp >> 2)) & 3)) : warp;
 
     for (int i = tid; i < P::UCELLS; i += NT) U[i] = Ug[i];
     if (tid == 0) {
@@ -211,7 +257,7 @@ __global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
     // prologue: A0 of the first batch
     if (a0_warp) {
         mbar_wait(&bar[0], ph0);
-        a0_inplace<LOG2N, T>(set(0), ntr_of(bt), ga, a0l64);
+        a0_inplace<LOG2N, T>(set(0), ntr_of(bt), ga, a0l64, itm);
     }
     ph0 ^= 1u;
     __syncthreads();
@@ -221,7 +267,7 @@ __global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
         vec2<T> *W = set(cur);
         QFT_MARK(1);
         QFT_PMARK24();
-        fused_units<LOG2N, T, 0, TT, NW>(W, U, kc.u, ntr, warp, lane);
+        fused_units<LOG2N, T, 0, TT, NW>(W, U, kc.u, ntr, uwarp, lane);
         QFT_WMARK();
         __syncthreads();
         QFT_MARK(3);
@@ -238,11 +284,18 @@ __global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
                 }
             }
             QFT_PMARK52();
+#if QFT_PIPE_TMA_EARLY
+            // the D warps are the only readers of set cur in this phase: once
+            // they are all done, warp 0 refills it while the A0 group finishes
+            named_bar(2, NWD * 32);
+            if (warp == 0 && bt + 2 * G < nbatch)
+                tma_load_slots<LOG2N, T>(W, in + (bt + 2 * G) * TT * P::N, ntr_of(bt + 2 * G), &bar[cur], lane);
+#endif
         } else if (a0_warp && bt + G < nbatch) {
             uint32_t &ph = cur ? ph0 : ph1;  // the next batch sits in set cur^1
             mbar_wait(&bar[cur ^ 1], ph);
             QFT_PMARK40();
-            a0_inplace<LOG2N, T>(set(cur ^ 1), ntr_of(bt + G), ga, a0l64);
+            a0_inplace<LOG2N, T>(set(cur ^ 1), ntr_of(bt + G), ga, a0l64, itm);
             QFT_PMARK52();
         }
         if (bt + G < nbatch) {
@@ -253,7 +306,7 @@ __global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
         __syncthreads();
         QFT_MARK(5);
         // set cur is free: bring in batch bt + 2G
-        if (warp == 0 && bt + 2 * G < nbatch)
+        if (!QFT_PIPE_TMA_EARLY && warp == QFT_PIPE_TMA_WARP && bt + 2 * G < nbatch)
             tma_load_slots<LOG2N, T>(W, in + (bt + 2 * G) * TT * P::N, ntr_of(bt + 2 * G), &bar[cur], lane);
         QFT_MARK(6);
         cur ^= 1;

@@ -16,7 +16,7 @@
 //       are written sub-block-major                                 W -> W
 //   B   full Lee DCT-II/DST-II of every 32-cell chunk; small blocks  W -> W
 //   C   backward levels of the big blocks (halo = neighbour lane)   W -> W
-//   D   time-split chain (elaborations.py:329-340) + complex
+//   D   time-split chain (elaborations.py:78-89) + complex
 //       recombination (shared.py:58-72)                          W -> global
 // N > 4096: the "huge" Lee blocks (L > 1024) first get RT = n-12-j top fold
 // levels from the whole CTA (TF, W -> W, 1024-cell sub-blocks written
