@@ -7,7 +7,9 @@
 // RG fold levels, tracking where each sub-block's cells are (runs) and in which
 // scratch buffer each spectrum ends up.  This is the "fixed kernel schedule"
 // compiled from the decomposition tree (SURVEY.md §2 plan builder).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstring>
@@ -248,8 +250,37 @@ struct ItemCfg {
     static constexpr int WCELLS = P::PADDED > LPAD ? P::PADDED : LPAD;
     static constexpr int UCELLS = L;  // level constants of every block size <= L
     static constexpr int U_OFF = WCELLS * VB;
-    static constexpr int SMEM = U_OFF + UCELLS * (int)sizeof(T);
+    static constexpr int BAR_OFF = (U_OFF + UCELLS * (int)sizeof(T) + 15) / 16 * 16;
+    static constexpr int SMEM = BAR_OFF + 16;
 };
+
+// ------------------------------------------------------------------ TMA tiles (fp64)
+// W0 viewed as a 2-D tensor of 32-cell rows (64 doubles; the per-signal stride Ws
+// is a multiple of 32 cells, and every leaf run / sub-signal range starts on a
+// row).  A box of kTmaBoxCols = 66 doubles x kTmaRows rows reads each row plus 2
+// out-of-bounds doubles that the TMA unit zero-fills: in shared memory every
+// row lands at a pitch of 33 cells, which is exactly the padded working layout
+// (cell p at p + p/32) -- the tile arrives conflict-free-padded with no
+// per-thread copies (cp.async.bulk.tensor, UTMALDG).
+constexpr int kTmaRows = 64, kTmaBoxCols = 66;
+constexpr unsigned kTmaBoxBytes = kTmaRows * kTmaBoxCols * 8;
+
+QFT_DEV void tma_tile_load(void *dst, const CUtensorMap *map, int row, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(dst)),
+        "l"(map), "r"(0), "r"(row), "r"((uint32_t)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+// one thread: load `cells` (a multiple of 32 * kTmaRows) consecutive W0 cells from
+// row0 into the padded layout at dst, completing on bar
+QFT_DEV void tma_cells(vec2<double> *dst, const CUtensorMap *map, long long row0, int cells, uint64_t *bar) {
+    const int rows = cells / 32;
+    for (int r = 0; r < rows; r += kTmaRows) tma_tile_load(dst + 33 * r, map, (int)(row0 + r), bar);
+}
+QFT_DEV void tma_expect(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
 
 // async 8/16-byte global -> shared copies (no registers, all in flight at once)
 template <typename T>
@@ -289,14 +320,41 @@ QFT_DEV int item_runs(const Item &it, const LeafTask *tasks, int N, long long *l
 // Leaf item: K leaves of 2^A cells from W0 runs -> their spectra along the runs.
 template <int A, typename T, int NT, int NW>
 QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const T *kcu, vec2<T> *wb, int tid,
-                       const vec2<T> *xb, int N) {
+                       const vec2<T> *xb, int N, const CUtensorMap *tmap = nullptr, long long wrow = 0,
+                       uint64_t *bar = nullptr, uint32_t *phase = nullptr) {
     constexpr int L = 1 << A;
     const int warp = tid >> 5, lane = tid & 31;
+    // fp64 with a tensor map: the runs arrive by TMA in memory order (a reversed
+    // run's element e at position L-1-e, handled by the TF loads)
+    const bool use_tma = tmap != nullptr;
+    if (use_tma) {
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            uint32_t bytes = 0;
+            for (int k = 0; k < K; ++k)
+                if (tks[k].j < 0) bytes += (uint32_t)(L / 32 / kTmaRows) * kTmaBoxBytes;
+            if (bytes) {
+                tma_expect(bar, bytes);
+                for (int k = 0; k < K; ++k) {
+                    const LeafTask tk = tks[k];
+                    if (tk.j >= 0) continue;
+                    const int lo = tk.sg > 0 ? tk.c : tk.c - (L - 1);
+                    tma_cells(reinterpret_cast<vec2<double> *>(S + padx(k * L)), tmap, wrow + lo / 32, L, bar);
+                }
+            }
+        }
+        bool any = false;
+        for (int k = 0; k < K; ++k) any |= tks[k].j < 0;
+        if (any) {
+            mbar_wait(bar, *phase);
+            *phase ^= 1u;
+        }
+    }
     // load: async cell copies along the (forward or reversed) runs; with NT a
     // multiple of 32 dividing L, thread tid's cells are tid + k NT and their padded
     // addresses advance by NT + NT/32: pointer increments only
     constexpr bool LIN = (L % NT) == 0 && (NT % 32) == 0;
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < K && !use_tma; ++k) {
         const LeafTask tk = tks[k];
         if (tk.j >= 0) continue;  // whole Lee block j: TF reads (and folds) x directly
         vec2<T> *s = S + padx(k * L);
@@ -328,8 +386,9 @@ QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const
                     if (tks[k].dst) LeafTop<A, true, T>::tf_load_x(xb, N, j, U, t, v[r]);
                     else LeafTop<A, false, T>::tf_load_x(xb, N, j, U, t, v[r]);
                 } else {
-                    if (tks[k].dst) LeafTop<A, true, T>::tf_load(s, U, t, v[r]);
-                    else LeafTop<A, false, T>::tf_load(s, U, t, v[r]);
+                    const bool rev = use_tma && tks[k].sg < 0;
+                    if (tks[k].dst) LeafTop<A, true, T>::tf_load(s, U, t, v[r], rev);
+                    else LeafTop<A, false, T>::tf_load(s, U, t, v[r], rev);
                 }
             }
         }
@@ -400,7 +459,8 @@ QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const
 
 template <int SUBLOG, typename T>
 QFT_DEV void sub_item(const vec2<T> *w0b, int m, vec2<T> *W, const T *U, const T *kcu, vec2<T> *cbuf, vec2<T> *sbuf,
-                      int tid, const vec2<T> *xb) {
+                      int tid, const vec2<T> *xb, const CUtensorMap *tmap = nullptr, long long wrow = 0,
+                      uint64_t *bar = nullptr, uint32_t *phase = nullptr) {
     using P = SPlan<SUBLOG>;
     using C = ItemCfg<SUBLOG, T>;
     constexpr int NT = C::NT, NW = C::NW;
@@ -426,6 +486,19 @@ QFT_DEV void sub_item(const vec2<T> *w0b, int m, vec2<T> *W, const T *U, const T
                 }
             }
         }
+    } else if (tmap) {
+        // fp64: the cosine cells [m - m', m) and the sine cells [N - m', N) (whose
+        // last cell is the base s(0)) by TMA into the padded sub-signal layout
+        constexpr int MP = P::m;
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tma_expect(bar, 2u * (uint32_t)(MP / 32 / kTmaRows) * kTmaBoxBytes);
+            tma_cells(reinterpret_cast<vec2<double> *>(W), tmap, wrow + (m - MP) / 32, MP, bar);
+            tma_cells(reinterpret_cast<vec2<double> *>(W + padx(P::S0)), tmap, wrow + (2 * m - MP) / 32, MP, bar);
+        }
+        if (tid == 32) W[padx(P::BASE + 1)] = w0b[2 * m];  // s(m')
+        mbar_wait(bar, *phase);
+        *phase ^= 1u;
     } else {
         // the folded blocks j >= J0 are contiguous in W0: cosine cells [m - m', m-1),
         // sine cells [N - m', N-1), base pair N-1, N  ->  the sub-signal's layout
@@ -468,16 +541,21 @@ template <int SUBLOG, typename T>
 __global__ void __launch_bounds__(ItemCfg<SUBLOG, T>::NT, 1)
     lg_item_kernel(vec2<T> *W0, long long Ws, int log2n, const Item *__restrict__ items, int ni,
                    const LeafTask *__restrict__ tasks, long long batch, const T *__restrict__ Ug,
-                   const __grid_constant__ LeeConstL<T> kc, const vec2<T> *__restrict__ x, int fold_x) {
+                   const __grid_constant__ LeeConstL<T> kc, const vec2<T> *__restrict__ x, int fold_x,
+                   const __grid_constant__ CUtensorMap tmap, int use_tma) {
     using C = ItemCfg<SUBLOG, T>;
     constexpr int NT = C::NT, NW = C::NW;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     vec2<T> *S = reinterpret_cast<vec2<T> *>(smem_raw);
     T *U = reinterpret_cast<T *>(smem_raw + C::U_OFF);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::BAR_OFF);
+    uint32_t phase = 0;
+    const CUtensorMap *tm = (sizeof(T) == 8 && use_tma && !fold_x) ? &tmap : nullptr;
     const int tid = threadIdx.x;
     const int N = 1 << log2n;
     const int nu = C::UCELLS < N / 4 ? C::UCELLS : N / 4;
     for (int i = tid; i < nu; i += NT) U[i] = Ug[i];
+    if (tid == 0) mbar_init(bar, 1);
     __syncthreads();
     for (long long g = blockIdx.x; g < batch * ni; g += gridDim.x) {
         const long long b = g / ni;
@@ -497,14 +575,16 @@ __global__ void __launch_bounds__(ItemCfg<SUBLOG, T>::NT, 1)
                 for (int r = 0; r < nr; ++r) l2_prefetch(W0 + b2 * Ws + lo[r], (uint32_t)(cnt[r] * sizeof(vec2<T>)));
             }
         }
+        const long long wrow = b * (Ws / 32);  // first tensor-map row of signal b
         if (it.kind == 0) {
             vec2<T> *cbuf = wb + (N + 2);
             sub_item<SUBLOG, T>(wb, N / 2, S, U, kc.u, cbuf, cbuf + SPlan<SUBLOG>::m + 1, tid,
-                                fold_x ? x + b * N : nullptr);
+                                fold_x ? x + b * N : nullptr, tm, wrow, bar, &phase);
         } else if (it.kind == 1) {
-            leaf_item<SUBLOG, T, NT, NW>(tasks + it.k0, 1, S, U, kc.u, wb, tid, x + b * N, N);
+            leaf_item<SUBLOG, T, NT, NW>(tasks + it.k0, 1, S, U, kc.u, wb, tid, x + b * N, N, tm, wrow, bar, &phase);
         } else {
-            leaf_item<SUBLOG - 1, T, NT, NW>(tasks + it.k0, 2, S, U, kc.u, wb, tid, x + b * N, N);
+            leaf_item<SUBLOG - 1, T, NT, NW>(tasks + it.k0, 2, S, U, kc.u, wb, tid, x + b * N, N, tm, wrow, bar,
+                                             &phase);
         }
         __syncthreads();
     }
@@ -574,6 +654,41 @@ static cudaError_t launch(K k, dim3 g, dim3 bl, size_t smem, cudaStream_t st, A.
 }
 
 static unsigned ybatch(long long batch) { return (unsigned)std::min<long long>(batch, 65535); }
+
+// Tensor map of W0 (fp64) as rows of 32 cells: dims {64 doubles, rows}, box
+// {kTmaBoxCols, kTmaRows} (the 2 columns past each row are out of bounds and
+// zero-filled: the padded shared layout).  cuTensorMapEncodeTiled comes from the
+// driver through the runtime's entry-point query (no -lcuda).  Returns 0 when
+// TMA is unavailable (the item kernel then uses per-thread async copies).
+static int tma_map_w0(CUtensorMap *map, void *w0, long long cells) {
+#if QFT_LARGE_PREC == 64
+#ifdef QFT_NO_TMA
+    (void)map; (void)w0; (void)cells;
+    return 0;
+#else
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return 0;
+        encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    const cuuint64_t dims[2] = {64, (cuuint64_t)(cells / 32)};
+    const cuuint64_t strides[1] = {64 * sizeof(double)};
+    const cuuint32_t box[2] = {kTmaBoxCols, kTmaRows};
+    const cuuint32_t es[2] = {1, 1};
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, w0, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 1 : 0;
+#endif
+#else
+    (void)map; (void)w0; (void)cells;
+    return 0;
+#endif
+}
 
 extern "C++" {
 
@@ -665,8 +780,10 @@ void QFT_LG(qft_large_info)(void *pp, int *passes, int *launches) {
 
 long long QFT_LG(qft_large_scratch_cells)(void *pp) {
     auto *p = (QFT_LG(LargePlan) *)pp;
-    // per signal and buffer: N+2 cells + C_J0 / S_J0 of the sub-signal
-    return (long long)p->s.N + 2 + 2 * ((1ll << (p->sublog - 1)) + 1);
+    // per signal and buffer: N+2 cells + C_J0 / S_J0 of the sub-signal, rounded
+    // up to whole 32-cell rows (the TMA tile view of W0)
+    const long long c = (long long)p->s.N + 2 + 2 * ((1ll << (p->sublog - 1)) + 1);
+    return (c + 31) / 32 * 32;
 }
 
 int QFT_LG(qft_large_exec)(void *pp, int mode, const void *d_in, void *d_out, long long batch, long long nreal,
@@ -723,11 +840,14 @@ int QFT_LG(qft_large_exec)(void *pp, int mode, const void *d_in, void *d_out, lo
         const unsigned grid = (unsigned)std::min<long long>(work, sms);
         const Item *it = (const Item *)p->d_items;
         const LeafTask *lv = (const LeafTask *)p->d_leaves;
+        CUtensorMap tmap;
+        memset(&tmap, 0, sizeof(tmap));
+        const int use_tma = QFT_LARGE_PREC == 64 && S.fold && tma_map_w0(&tmap, W0, batch * Ws);
         auto run = [&](auto kern, int nt, int smem) -> cudaError_t {
             cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (e2) return e2;
             return launch(kern, dim3(grid), dim3(nt), (size_t)smem, st, W0, Ws, S.n, it, p->nitems, lv, batch, U, kc, x,
-                          (int)!S.fold);
+                          (int)!S.fold, tmap, use_tma);
         };
         switch (p->sublog) {
 #define QFT_IT(SL) \

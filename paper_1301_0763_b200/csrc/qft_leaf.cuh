@@ -24,12 +24,14 @@ struct LeafTop {
     // TF item t in [0, 1024): reflection group t, RT levels (slot p = element t
     // of sub-block p); the caller holds v across a CTA barrier, then stores
     // sub-block-major (sub-block p at cells [1024p, 1024p + 1024))
-    QFT_HD static void tf_load(const vec2<T> *s, const T *U, int t, vec2<T> *v) {
+    // rev: the run was loaded in memory order and is reversed (element e at L-1-e)
+    QFT_HD static void tf_load(const vec2<T> *s, const T *U, int t, vec2<T> *v, bool rev = false) {
 #pragma unroll
         for (int q = 0; q < G; ++q) {
             int c, sg;
             run_of(RT, L, q, c, sg);
-            v[q] = s[padx(c + sg * t)];
+            const int e = c + sg * t;
+            v[q] = s[padx(rev ? L - 1 - e : e)];
         }
         lee_fwd<RT, L, DST, T>(v, t, U);
     }

@@ -4,6 +4,7 @@ value is one IEEE-rounded add/sub/mul as in the reference's counted primitives
 (counting.py:40-81).  Also checks the kernels really are sm_100a code and that
 the fp32 path uses the packed FADD2 pipe.  CPU only (cuobjdump)."""
 
+import functools
 import os
 import re
 import shutil
@@ -16,6 +17,7 @@ from conftest import ROOT
 LIB = os.path.join(ROOT, "paper_1301_0763_b200", "libqftb200.so")
 
 
+@functools.lru_cache(maxsize=1)
 def sass_by_function():
     exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
     if not os.path.exists(exe):
@@ -89,3 +91,18 @@ def test_sm100a_and_packed_fp32():
     ops = [o for o, _, _ in funcs[pipe]]
     assert any(o.startswith("UBLKCP") or o.startswith("UTMALDG") or "BLK" in o for o in ops), \
         "the pipelined kernel should issue TMA bulk copies"
+
+
+def test_multipass_fp64_items_use_tensor_map_tma():
+    """North-star item (4): the multi-pass path moves its fp64 tiles (leaf runs
+    and sub-signal ranges of W0) HBM -> shared memory with tensor-map TMA
+    (cp.async.bulk.tensor -> UTMALDG) into the padded layout; the single-pass
+    kernels stage raw signals with bulk TMA copies (UBLKCP)."""
+    funcs, _ = sass_by_function()
+    items64 = [k for k in funcs if "lg_item_kernel" in k and ("Ed" in k.split("lg_item_kernel")[1][:12])]
+    assert items64, "fp64 item kernels not found"
+    for k in items64:
+        ops = [o for o, _, _ in funcs[k]]
+        assert any(o.startswith("UTMALDG") for o in ops), f"{k}: no tensor-map TMA load"
+    pipe = [k for k in funcs if "qft_cdft_pipe" in k]
+    assert pipe and all(any(o.startswith("UBLKCP") for o, _, _ in funcs[k]) for k in pipe)
