@@ -35,6 +35,11 @@ void smem_cfg(int *cfg) {
             cfg[0] = C::SMEM;
             cfg[1] = C::NT;
             cfg[2] = C::TT;
+            if constexpr (QFT_PIPE == 3 && qft::GCfg<L, R>::FITS) {
+                cfg[0] = qft::GCfg<L, R>::SMEM;
+                cfg[1] = qft::GCfg<L, R>::NT;
+                cfg[2] = qft::GCfg<L, R>::NG;
+            }
         }
     } else {
         cfg[0] = cfg[1] = cfg[2] = 0;

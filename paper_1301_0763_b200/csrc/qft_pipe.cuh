@@ -415,8 +415,171 @@ __global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Group-pipelined variant (QFT_PIPE == 3): the CTA is NG independent groups of
+// GW = 4 warps (one warp per fused unit of a signal); each group streams its
+// own signals through two slots with named barriers of its own, so the groups
+// drift out of phase and one group's shared-memory-heavy units overlap another
+// group's latency-bound chain phase D (the lock-step kernels above leave the
+// shared-memory pipe idle during D and at every CTA barrier).
+//
+//   per group, iteration k (signal s_k in slot k & 1):
+//     wait TMA(s_k); A0 loads (registers)
+//     group barrier      -- every A0 load done, every D(s_{k-1}) read done
+//     TMA(s_{k+1}) -> slot (k+1) & 1; A0 stores (in place)
+//     group barrier
+//     units(s_k): one warp per unit
+//     group barrier
+//     D(s_k) on the warps that own items; the others go straight on to the
+//     A0 loads of s_{k+1}
+// ---------------------------------------------------------------------------
+#ifndef QFT_GPIPE_NG
+#define QFT_GPIPE_NG 3
+#endif
+#ifndef QFT_GPIPE_STAGGER
+#define QFT_GPIPE_STAGGER 0  // ns group g waits before its first signal (g * this)
+#endif
+template <int LOG2N, typename T>
+struct GCfg {
+    using P = SPlan<LOG2N>;
+    static constexpr int VB = (int)sizeof(vec2<T>);
+    static constexpr int UB = P::UCELLS * (int)sizeof(T);
+    static constexpr int PER_W = P::PADDED * VB;
+    static constexpr int GW = 2 * (P::NU1 + 1);  // warps per group = fused units per signal
+    static constexpr int NG = QFT_GPIPE_NG;
+    static constexpr int NW = NG * GW, NT = NW * 32;
+    static constexpr int NC64 = P::m / 64;
+    static constexpr int RA = (NC64 + GW - 1) / GW;
+    static constexpr int U_OFF = NG * 2 * PER_W;
+    static constexpr int BAR_OFF = (U_OFF + UB + 15) / 16 * 16;
+    static constexpr int SMEM = BAR_OFF + NG * 2 * 8;
+    static constexpr bool FITS = P::n <= 12 && P::JF >= 1 && GW == 4 && PER_W % 16 == 0 && SMEM <= 227 * 1024 &&
+                                 NW <= 16 && P::DT <= GW * 32;
+};
+
+// in-place A0 of one signal by the NWA warps of a group, split at the barrier
+template <int LOG2N, typename T, int NWA>
+struct A0Group {
+    using P = SPlan<LOG2N>;
+    static constexpr int NC64 = P::m / 64, RA = (NC64 + NWA - 1) / NWA;
+    A0Chunk64<T> ch[RA];
+    vec2<T> ia, ib;
+    QFT_DEV void load(const vec2<T> *s, int ga) {
+        const int lane = ga & 31, gw = ga >> 5;
+#pragma unroll
+        for (int r = 0; r < RA; ++r) {
+            const int c = gw + r * NWA;
+            if (c < NC64) ch[r].template load<LOG2N>(s, c, lane);
+        }
+        if (ga < NC64) {
+            ia = s[64 * ga];
+            ib = s[ga == 0 ? P::m : P::N - 64 * ga];
+        }
+    }
+    QFT_DEV void store(vec2<T> *s, int ga, const A0Lane64 &a0l64) const {
+        const int lane = ga & 31, gw = ga >> 5;
+        auto shfl_up = [](vec2<T> v) { return shfl_vec(v, false); };
+#pragma unroll
+        for (int r = 0; r < RA; ++r) {
+            const int c = gw + r * NWA;
+            if (c < NC64) ch[r].template store<LOG2N>(s, c, lane, a0l64, shfl_up);
+        }
+        if (ga < NC64) {
+            if (ga == 0) {
+                s[padx(P::BASE)] = ia;
+                s[padx(P::BASE + 1)] = ib;
+            } else {
+                const int n = 64 * ga, j = ctz32((uint32_t)n);
+                const int cell = P::m - (1 << (LOG2N - 1 - j)) + (n >> (j + 1));
+                s[padx(cell)] = vadd(ia, ib);
+                s[padx(P::S0 + cell)] = vsub(ia, ib);
+            }
+        }
+    }
+};
+
+template <int LOG2N, typename T>
+__global__ void __launch_bounds__(GCfg<LOG2N, T>::NT, 1)
+    qft_cdft_gpipe(const vec2<T> *__restrict__ in, vec2<T> *__restrict__ out, long long batch,
+                   const T *__restrict__ Ug, const __grid_constant__ LeeConst<T> kc) {
+    using P = SPlan<LOG2N>;
+    using C = GCfg<LOG2N, T>;
+    constexpr int GW = C::GW, NG = C::NG, NT = C::NT;
+    constexpr uint32_t BYTES = P::N * (uint32_t)sizeof(vec2<T>);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T *U = reinterpret_cast<T *>(smem_raw + C::U_OFF);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + C::BAR_OFF);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = warp / GW, gw = warp - g * GW, gt = tid - g * GW * 32;
+    vec2<T> *slot0 = reinterpret_cast<vec2<T> *>(smem_raw) + (2 * g) * P::PADDED;
+    uint64_t *bar = bars + 2 * g;
+    const int bid = 1 + g;  // named barrier of the group
+    const A0Lane64 a0l64 = a0_lane64<LOG2N>(lane);
+    // the unit kind and the phase-D warps rotate with the group, so the heavier
+    // units and the D warps spread over the four SM sub-partitions (warp w runs on w % 4)
+    const int kind = (gw + g) % GW;
+    const int ditem = ((gw - g + GW) % GW) * 32 + lane;
+
+    for (int i = tid; i < P::UCELLS; i += NT) U[i] = Ug[i];
+    if (tid < 2 * NG) mbar_init(&bars[tid], 1);
+    __syncthreads();
+    const long long G = gridDim.x;
+    auto sig = [&](long long k) { return (blockIdx.x + k * G) * NG + g; };
+    if (sig(0) >= batch) return;
+    if (QFT_GPIPE_STAGGER && g > 0) __nanosleep(QFT_GPIPE_STAGGER * g);
+    if (gt == 0) tma_bulk_load(slot0, in + sig(0) * P::N, BYTES, &bar[0]);
+    uint32_t ph = 0;  // bit s: parity of slot s
+    for (long long k = 0; sig(k) < batch; ++k) {
+        const int s = (int)(k & 1);
+        vec2<T> *W = slot0 + s * P::PADDED;
+        mbar_wait(&bar[s], (ph >> s) & 1u);
+        ph ^= 1u << s;
+        {
+            A0Group<LOG2N, T, GW> a0;
+            a0.load(W, gt);
+            named_bar(bid, GW * 32);
+            // every read of the other slot (D of s_{k-1}) is done: refill it
+            if (gt == 0 && sig(k + 1) < batch)
+                tma_bulk_load(slot0 + (s ^ 1) * P::PADDED, in + sig(k + 1) * P::N, BYTES, &bar[s ^ 1]);
+            a0.store(W, gt, a0l64);
+        }
+        named_bar(bid, GW * 32);
+        {
+            const bool dst = kind & 1;
+            if ((kind >> 1) < P::NU1) {
+                vec2<T> *wb = W + padx((dst ? P::S0 : 0) + P::big_cell(kind >> 1));
+                if (dst) unit_big<P::LB, P::RB, T, true>(wb, U, kc.u, lane);
+                else unit_big<P::LB, P::RB, T, false>(wb, U, kc.u, lane);
+            } else {
+                if (dst) unit_rest<LOG2N, T, true>(W, U, kc.u, lane);
+                else unit_rest<LOG2N, T, false>(W, U, kc.u, lane);
+            }
+        }
+        named_bar(bid, GW * 32);
+        if (ditem < P::DT) Chain<LOG2N, T>::unit(W, out + sig(k) * P::N, ditem);
+    }
+}
+
+template <int LOG2N, typename T>
+cudaError_t launch_gpipe(const LaunchArgs &a) {
+    using C = GCfg<LOG2N, T>;
+    auto kern = qft_cdft_gpipe<LOG2N, T>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    const long long ngroups = (a.batch + C::NG - 1) / C::NG;
+    long long grid = a.num_sms;
+    if (grid > ngroups) grid = ngroups;
+    if (grid < 1) grid = 1;
+    LeeConst<T> kc;
+    for (int i = 0; i < 32; ++i) kc.u[i] = ((const T *)a.Uhead)[i];
+    kern<<<(unsigned)grid, C::NT, C::SMEM, a.stream>>>((const vec2<T> *)a.in, (vec2<T> *)a.out, a.batch,
+                                                       (const T *)a.U, kc);
+    return cudaGetLastError();
+}
+
 template <int LOG2N, typename T>
 cudaError_t launch_pipe(const LaunchArgs &a) {
+    if constexpr (QFT_PIPE == 3 && GCfg<LOG2N, T>::FITS) return launch_gpipe<LOG2N, T>(a);
     using C = PCfg<LOG2N, T>;
     auto kern = QFT_PIPE == 2 ? qft_cdft_pipe2<LOG2N, T> : qft_cdft_pipe<LOG2N, T>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
