@@ -38,7 +38,7 @@ namespace {
 
 // largest single-pass sub-signal / leaf: 2^14 cells fp32, 2^13 fp64 (128 KiB)
 constexpr int kSubLogMax = QFT_LARGE_PREC == 32 ? 14 : 13;
-constexpr int kRG = QFT_LARGE_PREC == 32 ? 5 : 4;         // fold levels per F/B pass
+constexpr int kRG = 5;  // fold levels per F/B pass (fp64 R = 5: lane pairs, lg_f_pair5 / lg_b_pair5_out)
 constexpr int kRC = 4;                                    // chain levels unfolded per thread
 constexpr int kChunk = 256;
 constexpr int kBChunk = 128;  // columns per CTA of a backward pass (outputs staged in shared memory)
@@ -183,6 +183,16 @@ __global__ void __launch_bounds__(kChunk) lg_f_kernel(vec2<T> *__restrict__ W0, 
         const bool dst = dsts[ch.task];
         vec2<T> *w = W0 + b * Ws;
         const vec2<T> *xb = x + b * N;
+#if QFT_LARGE_PREC == 64
+        if (rs[ch.task] == 5) {  // lane pairs: lanes l and l+16 share reflection group t
+            const int tp = ch.t0 + (threadIdx.x >> 5) * 16 + (threadIdx.x & 15), h = (threadIdx.x >> 4) & 1;
+            if (tp < (tk.L >> 5)) {  // both lanes of a pair agree (warp-uniform per half)
+                if (dst) lg_f_pair5<T, true>(w, tk, tp, h, U, xb, N);
+                else lg_f_pair5<T, false>(w, tk, tp, h, U, xb, N);
+            }
+            continue;
+        }
+#endif
         switch (rs[ch.task]) {
             case 1: lg_f_dispatch_r<1, T>(w, tk, t, dst, U, xb, N); break;
             case 2: lg_f_dispatch_r<2, T>(w, tk, t, dst, U, xb, N); break;
@@ -223,6 +233,39 @@ __global__ void __launch_bounds__(kBChunk) lg_b_kernel(vec2<T> *W0, vec2<T> *W1,
         for (int p = threadIdx.x; p < ncols * G; p += kBChunk) dst[p] = stg[p + (p >> 5)];
         __syncthreads();
         (void)CELLS;
+    }
+}
+
+// fp64 R = 5 backward levels: lanes l and l+16 share column i (lg_b_pair5_out);
+// a CTA of kBChunk threads covers kBChunk / 2 columns
+template <typename T>
+__global__ void __launch_bounds__(kBChunk) lg_b_pair_kernel(vec2<T> *W0, vec2<T> *W1, const BTask *__restrict__ tasks,
+                                                           const Chunk *__restrict__ chunks, long long batch,
+                                                           long long Ws) {
+    constexpr int G = 32, COLS = kBChunk / 2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    vec2<T> *stg = reinterpret_cast<vec2<T> *>(smem_raw);  // padded: cell p at p + p/32
+    const Chunk ch = chunks[blockIdx.x];
+    const BTask tk = tasks[ch.task];
+    const int lc = (threadIdx.x >> 5) * 16 + (threadIdx.x & 15), h = (threadIdx.x >> 4) & 1;
+    const int i = ch.t0 + lc;
+    const int ncols = min(COLS, (tk.L >> 5) - ch.t0);
+    for (long long b = blockIdx.y; b < batch; b += gridDim.y) {
+        vec2<T> *W[2] = {W0 + b * Ws, W1 + b * Ws};
+        if (lc < ncols) {  // ncols is a multiple of 16: whole warps agree
+            vec2<T> out[G / 2];
+            if (tk.dst) lg_b_pair5_out<T, true>(W, tk, i, h, out);
+            else lg_b_pair5_out<T, false>(W, tk, i, h, out);
+#pragma unroll
+            for (int q = 0; q < G / 2; ++q) {
+                const int p = lc * G + h * (G / 2) + q;
+                stg[p + (p >> 5)] = out[q];
+            }
+        }
+        __syncthreads();
+        vec2<T> *dst = W[tk.out_buf] + tk.out0 + ch.t0 * G;
+        for (int p = threadIdx.x; p < ncols * G; p += kBChunk) dst[p] = stg[p + (p >> 5)];
+        __syncthreads();
     }
 }
 
@@ -711,7 +754,9 @@ int QFT_LG(qft_large_create)(int log2n, int real_modes, void **out) {
                     ds.push_back(kv.second[i].second);
                     rs.push_back(kv.first);
                     const int groups = kv.second[i].first.L >> kv.first;
-                    for (int t0 = 0; t0 < groups; t0 += kChunk) ch.push_back({id, t0});
+                    // fp64 R = 5: two threads per reflection group
+                    const int step = (QFT_LARGE_PREC == 64 && kv.first == 5) ? kChunk / 2 : kChunk;
+                    for (int t0 = 0; t0 < groups; t0 += step) ch.push_back({id, t0});
                 }
             ts.ntasks = (int)tk.size();
             ts.nchunks = (int)ch.size();
@@ -722,9 +767,10 @@ int QFT_LG(qft_large_create)(int log2n, int real_modes, void **out) {
             TaskSet ts;
             ts.R = kv.first;
             std::vector<Chunk> ch;
+            const int step = (QFT_LARGE_PREC == 64 && kv.first == 5) ? kBChunk / 2 : kBChunk;
             for (size_t i = 0; i < kv.second.size(); ++i) {
                 const int cols = kv.second[i].L >> kv.first;
-                for (int t0 = 0; t0 < cols; t0 += kBChunk) ch.push_back({(int)i, t0});
+                for (int t0 = 0; t0 < cols; t0 += step) ch.push_back({(int)i, t0});
             }
             ts.ntasks = (int)kv.second.size();
             ts.nchunks = (int)ch.size();
@@ -873,6 +919,9 @@ int QFT_LG(qft_large_exec)(void *pp, int mode, const void *d_in, void *d_out, lo
                 case 2: e = launch(lg_b_kernel<2, T>, g, dim3(kBChunk), bsm(2), st, W0, W1, tk, ch, batch, Ws); break;
                 case 3: e = launch(lg_b_kernel<3, T>, g, dim3(kBChunk), bsm(3), st, W0, W1, tk, ch, batch, Ws); break;
                 case 4: e = launch(lg_b_kernel<4, T>, g, dim3(kBChunk), bsm(4), st, W0, W1, tk, ch, batch, Ws); break;
+#if QFT_LARGE_PREC == 64
+                case 5: e = launch(lg_b_pair_kernel<T>, g, dim3(kBChunk), bsm(4), st, W0, W1, tk, ch, batch, Ws); break;
+#endif
 #if QFT_LARGE_PREC == 32
                 case 5: e = launch(lg_b_kernel<5, T>, g, dim3(kBChunk), bsm(5), st, W0, W1, tk, ch, batch, Ws); break;
 #endif

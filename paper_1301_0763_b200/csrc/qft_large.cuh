@@ -6,7 +6,7 @@
 // blocks of 2^SUBLOG cells or less are CTA-resident leaves (qft_leaf.cuh), and
 // only blocks larger than that are cut in HBM by the passes here:
 //   fold   x -> W0: x[n] +- x[N-n] routed to Lee block j = ctz(n) (shared.py:28-35)
-//   F(d)   in-place forward fold levels (r <= 5 fp32 / 4 fp64 per pass) of every
+//   F(d)   in-place forward fold levels (r <= 5 per pass; fp64 r = 5 on lane pairs) of every
 //          block larger than the leaf size; the first touch folds x on load;
 //          each pass leaves 2^r sub-blocks as contiguous (possibly reversed)
 //          runs of the same cells
@@ -111,6 +111,43 @@ QFT_HD void lg_f_group(vec2<T> *w, const FTask &tk, int t, const T *U, const vec
     }
 }
 
+#if defined(__CUDACC__)
+// Five forward levels split over a lane pair (fp64: 32 cells of one thread would
+// not fit its registers).  lee_fwd_rt<5> is the top fold of every slot pair
+// (s, 31-s) followed by two independent 4-level problems on the even child
+// (slots 0..15) and the odd child (slots 16..31); thread h of the pair forms
+// child h of the top fold and runs its four levels -- the same operations on
+// the same operands as lg_f_group<5>.  Both lanes of a pair must be in one warp.
+template <typename T, bool DST>
+QFT_DEV void lg_f_pair5(vec2<T> *w, const FTask &tk, int t, int h, const T *U, const vec2<T> *x, int N) {
+    constexpr int R = 5, G = 32, H = 16;
+    const int L = tk.L;
+    auto at = [&](int s) {
+        int c, sg;
+        run_of(R, L, s, c, sg);
+        return c + sg * t;
+    };
+    vec2<T> nv[H];
+#pragma unroll
+    for (int s = 0; s < H; ++s) {
+        const int ea = at(s), eb = at(G - 1 - s);
+        const vec2<T> a = tk.j >= 0 ? fold_load<T, DST>(x, N, tk.j, ea) : w[tk.c + tk.sg * ea];
+        const vec2<T> b = tk.j >= 0 ? fold_load<T, DST>(x, N, tk.j, eb) : w[tk.c + tk.sg * eb];
+        int c, sg;
+        run_of(R - 1, L / 2, s, c, sg);
+        const T k = U[L / 2 + c + sg * t];
+        const vec2<T> sum = vadd(a, b), dif = vsub(a, b);
+        if constexpr (!DST) nv[s] = h ? vmul(dif, k) : sum;
+        else nv[s] = h ? vmul(sum, k) : dif;
+    }
+    lee_fwd_rt<R - 1, T, DST>(nv, t, L / 2, U);
+    __syncwarp();  // every lane's loads of the run precede the in-place stores
+#pragma unroll
+    for (int s = 0; s < H; ++s) w[tk.c + tk.sg * at(h * H + s)] = nv[s];
+}
+
+#endif  // __CUDACC__
+
 // ----------------------------------------------------------------- B pass
 template <int R, typename T, bool DST>
 QFT_HD void lg_b_column_out(vec2<T> *const *W, const BTask &tk, int i, vec2<T> *out) {
@@ -139,6 +176,79 @@ QFT_HD void lg_b_column_out(vec2<T> *const *W, const BTask &tk, int i, vec2<T> *
     const bool edge = DST ? (i == 0) : (i == S - 1);
     lee_bwd_fn<R, DST, T>(own, 0, halo, edge, out);
 }
+#if defined(__CUDACC__)
+// Five backward levels of column i split over a lane pair (the inverse of
+// lg_f_pair5): thread h runs the four levels of child h (sub-blocks 16h..16h+15),
+// the pair swaps the halves the top level's interleave needs (shfl_xor 16), and
+// thread h emits the block spectrum slots [16h, 16h+16) of the column -- the
+// same operations on the same operands as lg_b_column_out<5>.
+template <typename T, bool DST>
+QFT_DEV void lg_b_pair5_out(vec2<T> *const *W, const BTask &tk, int i, int h, vec2<T> *out) {
+    constexpr int R = 5, H = 16;
+    const int S = tk.L >> R;
+    const vec2<T> *src = W[tk.in_buf];
+    const int ih = DST ? (i > 0 ? i - 1 : i) : (i < S - 1 ? i + 1 : i);
+    auto addr = [&](int p, int col) {
+        int c, sg;
+        run_of(R, tk.L, p, c, sg);
+        const int rc = tk.c + tk.sg * c, rs = tk.sg * sg;
+        return tk.leaf ? rc + rs * col : (rs > 0 ? rc : rc - (S - 1)) + col;
+    };
+    vec2<T> own[H], hal[H];
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+        own[q] = src[addr(h * H + q, i)];
+        hal[q] = src[addr(h * H + q, ih)];
+    }
+    // the top level's halo: the leftmost leaf of the odd child (thread 1 has it)
+    const vec2<T> hv = DST ? src[addr(H, ih)] : hal[0];
+    auto halo = [&](int p) { return hal[p - h * H]; };
+    const bool edge = DST ? (i == 0) : (i == S - 1);
+    vec2<T> r[H];  // child h: e (h = 0) or o (h = 1)
+    lee_bwd_fn<R - 1, DST, T>(own, h * H, halo, edge, r);
+    // swap: thread 0 gets o[0..8], thread 1 gets e[8..16)
+    vec2<T> rcv[H / 2 + 1];
+#pragma unroll
+    for (int q = 0; q <= H / 2; ++q) {
+        const vec2<T> snd = h ? r[q] : r[q < H / 2 ? H / 2 + q : H - 1];
+        rcv[q].x = __shfl_xor_sync(0xffffffffu, snd.x, 16);
+        rcv[q].y = __shfl_xor_sync(0xffffffffu, snd.y, 16);
+    }
+    if constexpr (!DST) {
+        // out[2t] = e[t], out[2t+1] = o[t] + o[t+1], out[31] = o[15] (+ halo)
+        if (h == 0) {
+#pragma unroll
+            for (int t = 0; t < H / 2; ++t) {
+                out[2 * t] = r[t];
+                out[2 * t + 1] = vadd(rcv[t], rcv[t + 1]);
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < H / 2; ++t) {
+                out[2 * t] = rcv[t];
+                out[2 * t + 1] = t < H / 2 - 1 ? vadd(r[H / 2 + t], r[H / 2 + t + 1]) : (edge ? r[H - 1] : vadd(r[H - 1], hv));
+            }
+        }
+    } else {
+        // out[2t+1] = e[t], out[2t] = o[t-1] + o[t], out[0] = (halo +) o[0]
+        if (h == 0) {
+            out[0] = edge ? rcv[0] : vadd(hv, rcv[0]);
+#pragma unroll
+            for (int t = 1; t < H / 2; ++t) out[2 * t] = vadd(rcv[t - 1], rcv[t]);
+#pragma unroll
+            for (int t = 0; t < H / 2; ++t) out[2 * t + 1] = r[t];
+        } else {
+#pragma unroll
+            for (int t = 0; t < H / 2; ++t) {
+                out[2 * t] = vadd(r[H / 2 + t - 1], r[H / 2 + t]);
+                out[2 * t + 1] = rcv[t];
+            }
+        }
+    }
+}
+
+#endif  // __CUDACC__
+
 template <int R, typename T, bool DST>
 QFT_HD void lg_b_column(vec2<T> *const *W, const BTask &tk, int i) {
     constexpr int G = 1 << R;

@@ -284,7 +284,7 @@ static void emu_sub(const vec2<T> *w0, int m, vec2<T> *cb, vec2<T> *sb, const T 
 
 template <typename T, int SUBLOG>
 static int emu_large(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
-    const int J0 = log2n - SUBLOG, RG = sizeof(T) == 4 ? 5 : 4;
+    const int J0 = log2n - SUBLOG, RG = 5;
     // complex plans fold on load (no fold pass) for fp32 with J0 <= 2 (qft_large.cu fold_on_load)
     LargeSchedule S(log2n, SUBLOG, RG, J0, !(sizeof(T) == 4 && J0 <= 2));
     const int N = S.N, mj0 = 1 << (SUBLOG - 1);
@@ -351,7 +351,7 @@ static int emu_large(int log2n, const vec2<T> *x, vec2<T> *y, const T *U) {
 // first touch), same items / B passes, real-mode chain emit
 template <typename T, int SUBLOG, int MODE>
 static int emu_large_real(int log2n, const T *xa, const T *xb, T *ya, T *yb, const T *U) {
-    const int J0 = log2n - SUBLOG, RG = sizeof(T) == 4 ? 5 : 4;
+    const int J0 = log2n - SUBLOG, RG = 5;
     LargeSchedule S(log2n, SUBLOG, RG, J0, true, false);
     const int N = S.N, mj0 = 1 << (SUBLOG - 1);
     const long long Ws = N + 2 + 2 * (mj0 + 1);
