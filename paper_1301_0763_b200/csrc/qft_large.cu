@@ -525,7 +525,7 @@ QFT_DEV void sub_item(const vec2<T> *w0b, int m, vec2<T> *W, const T *U, const T
                     const int jj = ctz32((uint32_t)k);
                     const int cell = P::m - (1 << (SUBLOG - 1 - jj)) + (k >> (jj + 1));
                     W[padx(cell)] = vadd(a, b);
-                    W[padx(P::S0 + cell)] = vsub(a, b);
+                    W[padx(P::S0 + cell)] = sine_cell(a, b, cell);
                 }
             }
         }
@@ -568,6 +568,15 @@ QFT_DEV void sub_item(const vec2<T> *w0b, int m, vec2<T> *W, const T *U, const T
         cp_async_wait_all();
     }
     __syncthreads();
+    if (QFT_SC && !xb) {
+        // cells copied from W0 (natural order): the single-pass layout holds the
+        // odd sine cells negated (qft_smem.cuh QFT_SC)
+        for (int c = 2 * tid + 1; c < P::m - 1; c += 2 * NT) {
+            const vec2<T> v = W[padx(P::S0 + c)];
+            W[padx(P::S0 + c)] = vec2<T>{-v.x, -v.y};
+        }
+        __syncthreads();
+    }
     if constexpr (P::JH > 0) top_f<SUBLOG, T, 0>(W, U, 1, tid);
     fused_units<SUBLOG, T, 0, 1, NW>(W, U, kcu, 1, warp, lane);
     __syncthreads();

@@ -353,7 +353,7 @@ QFT_DEV void run_c_blocks(vec2<T> *w, bool dst, int lane) {
 // big unit: a block of L = 32 << R cells at padded pointer wb (block 0 for
 // N <= 4096, a 1024-cell (sub-)block for N > 4096): one Lee-32 per lane
 template <int L, int R, typename T, bool DST, bool REV = false>
-QFT_DEV void unit_big(vec2<T> *wb, const T *U, const T *kcu, int lane) {
+QFT_DEV void unit_big(vec2<T> *wb, const T *U, const T *kcu, int lane, int ub = DST ? 1 : 0) {
     QFT_UMARK(0);
     FBlockP<L, R, DST, T> f;
     f.template load<REV>(wb, U, lane);
@@ -362,7 +362,7 @@ QFT_DEV void unit_big(vec2<T> *wb, const T *U, const T *kcu, int lane) {
     f.store(wb, lane);
     __syncwarp();
     QFT_UMARK(2);
-    if (lane < (1 << R)) b_l32p<DST, T>(wb + 33 * lane, kcu);
+    if (lane < (1 << R)) b_l32p<DST, T>(wb + 33 * lane, kcu, ub);
     __syncwarp();
     QFT_UMARK(3);
     run_c_blockp<R, DST, T>(wb, lane);
@@ -416,7 +416,7 @@ struct CRest<LOG2N, T, DST, J, true> {
     }
 };
 template <int LOG2N, typename T, bool DST>
-QFT_DEV void unit_rest(vec2<T> *w, const T *U, const T *kcu, int lane) {
+QFT_DEV void unit_rest(vec2<T> *w, const T *U, const T *kcu, int lane, int ub = DST ? 1 : 0) {
     using P = SPlan<LOG2N>;
     constexpr int sb = DST ? P::S0 : 0;
     constexpr int CNT = P::NL32 - P::K0;
@@ -431,8 +431,8 @@ QFT_DEV void unit_rest(vec2<T> *w, const T *U, const T *kcu, int lane) {
     run_f_blocks<LOG2N, T, P::JR>(w, U, DST, lane);
 #endif
     __syncwarp();
-    if (lane < CNT) b_l32<DST, T>(w, sb + 32 * (P::K0 + lane), kcu);
-    else if (lane == CNT) b_small<LOG2N, DST, T>(w, kcu);
+    if (lane < CNT) b_l32<DST, T>(w, sb + 32 * (P::K0 + lane), kcu, ub);
+    else if (lane == CNT) b_small<LOG2N, DST, T>(w, kcu, ub);
     __syncwarp();
 #if QFT_REST_FUSED
     {
@@ -460,7 +460,9 @@ QFT_DEV void top_f_sig(vec2<T> *w, const T *U, int tid) {
         __syncthreads();
     } else {
         using TC = Top<LOG2N, J, false, T>;
-        using TS = Top<LOG2N, J, true, T>;
+        // QFT_SC: the sine side runs the cosine code on the sine region
+        using TS = Top<LOG2N, J, !QFT_SC, T>;
+        vec2<T> *const wsn = QFT_SC ? w + padx(P::S0) : w;
         constexpr int G = TC::G, IT = K::TIT, NT = K::NT;
         constexpr bool DOC = MODE != 3, DOS = MODE != 2;
         vec2<T> vc[IT][G], vs[IT][G];
@@ -469,7 +471,7 @@ QFT_DEV void top_f_sig(vec2<T> *w, const T *U, int tid) {
             const int t = tid + k * NT;
             if (t < 1024) {
                 if (DOC) TC::f_load(w, U, t, vc[k]);
-                if (DOS) TS::f_load(w, U, t, vs[k]);
+                if (DOS) TS::f_load(wsn, U, t, vs[k]);
             }
         }
         top_f_sig<LOG2N, T, MODE, J + 1>(w, U, tid);
@@ -478,7 +480,7 @@ QFT_DEV void top_f_sig(vec2<T> *w, const T *U, int tid) {
             const int t = tid + k * NT;
             if (t < 1024) {
                 if (DOC) TC::f_store(w, t, vc[k]);
-                if (DOS) TS::f_store(w, t, vs[k]);
+                if (DOS) TS::f_store(wsn, t, vs[k]);
             }
         }
     }
@@ -491,7 +493,8 @@ QFT_DEV void top_b_sig(vec2<T> *w, int tid) {
         __syncthreads();
     } else {
         using TC = Top<LOG2N, J, false, T>;
-        using TS = Top<LOG2N, J, true, T>;
+        using TS = Top<LOG2N, J, !QFT_SC, T>;
+        vec2<T> *const wsn = QFT_SC ? w + padx(P::S0) : w;
         constexpr int G = TC::G, IT = K::TIT, NT = K::NT;
         constexpr bool DOC = MODE != 3, DOS = MODE != 2;
         vec2<T> oc[IT][G], os[IT][G];
@@ -500,7 +503,7 @@ QFT_DEV void top_b_sig(vec2<T> *w, int tid) {
             const int i = tid + k * NT;
             if (i < 1024) {
                 if (DOC) TC::b_compute(w, i, oc[k]);
-                if (DOS) TS::b_compute(w, i, os[k]);
+                if (DOS) TS::b_compute(wsn, i, os[k]);
             }
         }
         top_b_sig<LOG2N, T, MODE, J + 1>(w, tid);
@@ -509,7 +512,7 @@ QFT_DEV void top_b_sig(vec2<T> *w, int tid) {
             const int i = tid + k * NT;
             if (i < 1024) {
                 if (DOC) TC::b_store(w, i, oc[k]);
-                if (DOS) TS::b_store(w, i, os[k]);
+                if (DOS) TS::b_store(wsn, i, os[k]);
             }
         }
     }
@@ -526,6 +529,28 @@ QFT_DEV void top_b(vec2<T> *W, int ntr, int tid) {
     __syncthreads();
 }
 
+// fused unit `kind` of the signal at w: side kind & 1, big unit kind >> 1 (or
+// the rest unit when kind >> 1 == NU1)
+template <int LOG2N, typename T, int MODE>
+QFT_DEV void run_unit(vec2<T> *w, int kind, const T *U, const T *kcu, int lane) {
+    using P = SPlan<LOG2N>;
+    const bool dst = kind & 1;
+    if ((MODE == 2 && dst) || (MODE == 3 && !dst)) return;  // side not needed
+    const int bu = kind >> 1;
+    if constexpr (QFT_SC) {  // both sides through the cosine code (qft_smem.cuh QFT_SC)
+        vec2<T> *ws = w + (dst ? padx(P::S0) : 0);
+        if (bu < P::NU1) unit_big<P::LB, P::RB, T, false>(ws + padx(P::big_cell(bu)), U, kcu, lane, dst);
+        else unit_rest<LOG2N, T, false>(ws, U, kcu, lane, dst);
+    } else if (bu < P::NU1) {
+        vec2<T> *wb = w + padx((dst ? P::S0 : 0) + P::big_cell(bu));
+        if (dst) unit_big<P::LB, P::RB, T, true>(wb, U, kcu, lane);
+        else unit_big<P::LB, P::RB, T, false>(wb, U, kcu, lane);
+    } else {
+        if (dst) unit_rest<LOG2N, T, true>(w, U, kcu, lane);
+        else unit_rest<LOG2N, T, false>(w, U, kcu, lane);
+    }
+}
+
 // A+B+C of TT signals, one warp per (signal, side, unit)
 template <int LOG2N, typename T, int MODE, int TT, int NW>
 QFT_DEV void fused_units(vec2<T> *W, const T *U, const T *kcu, int ntr, int warp, int lane) {
@@ -534,18 +559,7 @@ QFT_DEV void fused_units(vec2<T> *W, const T *U, const T *kcu, int ntr, int warp
     for (int u = warp; u < TT * NU; u += NW) {
         const int tau = u / NU, kind = u - tau * NU;
         if (tau >= ntr) continue;
-        vec2<T> *w = W + tau * P::PADDED;
-        const bool dst = kind & 1;
-        if ((MODE == 2 && dst) || (MODE == 3 && !dst)) continue;  // side not needed
-        const int bu = kind >> 1;
-        if (bu < P::NU1) {
-            vec2<T> *wb = w + padx((dst ? P::S0 : 0) + P::big_cell(bu));
-            if (dst) unit_big<P::LB, P::RB, T, true>(wb, U, kcu, lane);
-            else unit_big<P::LB, P::RB, T, false>(wb, U, kcu, lane);
-        } else {
-            if (dst) unit_rest<LOG2N, T, true>(w, U, kcu, lane);
-            else unit_rest<LOG2N, T, false>(w, U, kcu, lane);
-        }
+        run_unit<LOG2N, T, MODE>(W + tau * P::PADDED, kind, U, kcu, lane);
         __syncwarp();
     }
 }

@@ -20,8 +20,10 @@ namespace qft {
 // In: v[i] = x_i (odd-time samples in slot order).  Out: v[k] = spectrum slot k
 // (DCT: harmonic k; DST: harmonic k+1).
 // ---------------------------------------------------------------------------
+// ub: index of the L == 2 base constant -- 0 for the DCT, 1 for the DST; the
+// DCT code run on a sine block stored "as cosine" (QFT_SC, qft_smem.cuh) passes 1.
 template <int L, bool DST, typename T>
-QFT_HD void lee_full(vec2<T> *v, const T *U) {
+QFT_HD void lee_full(vec2<T> *v, const T *U, int ub = DST ? 1 : 0) {
     if constexpr (L > 1) {
         constexpr int H = L / 2;
         vec2<T> e[H], o[H];
@@ -30,7 +32,7 @@ QFT_HD void lee_full(vec2<T> *v, const T *U) {
             vec2<T> a = v[i], b = v[L - 1 - i];
             // L == 2 is the eight-point base: DCT uses the named cos(2pi/8)
             // (improved.py:63), DST the half-secant at 1/8 (improved.py:102).
-            T c = (L == 2) ? (DST ? U[1] : U[0]) : U[H + i];
+            T c = (L == 2) ? U[ub] : U[H + i];
             if constexpr (!DST) {
                 e[i] = vadd(a, b);
                 o[i] = vmul(vsub(a, b), c);
@@ -39,8 +41,8 @@ QFT_HD void lee_full(vec2<T> *v, const T *U) {
                 o[i] = vmul(vadd(a, b), c);
             }
         }
-        lee_full<H, DST, T>(e, U);
-        lee_full<H, DST, T>(o, U);
+        lee_full<H, DST, T>(e, U, ub);
+        lee_full<H, DST, T>(o, U, ub);
         if constexpr (!DST) {
 #pragma unroll
             for (int i = 0; i < H; ++i) v[2 * i] = e[i];

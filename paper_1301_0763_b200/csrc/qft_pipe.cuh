@@ -210,7 +210,7 @@ QFT_DEV void a0_inplace(vec2<T> *X, int ntr, int ga, const A0Lane64 &a0l64, vec2
                 const int n = 64 * ga, j = ctz32((uint32_t)n);
                 const int cell = P::m - (1 << (LOG2N - 1 - j)) + (n >> (j + 1));
                 s[padx(cell)] = vadd(ia, ib);
-                s[padx(P::S0 + cell)] = vsub(ia, ib);
+                s[padx(P::S0 + cell)] = sine_cell(ia, ib, cell);
             }
         }
         // the next signal's loads read another slot: no barrier needed here
@@ -492,7 +492,7 @@ struct A0Group {
                 const int n = 64 * ga, j = ctz32((uint32_t)n);
                 const int cell = P::m - (1 << (LOG2N - 1 - j)) + (n >> (j + 1));
                 s[padx(cell)] = vadd(ia, ib);
-                s[padx(P::S0 + cell)] = vsub(ia, ib);
+                s[padx(P::S0 + cell)] = sine_cell(ia, ib, cell);
             }
         }
     }
@@ -544,17 +544,7 @@ __global__ void __launch_bounds__(GCfg<LOG2N, T>::NT, 1)
             a0.store(W, gt, a0l64);
         }
         named_bar(bid, GW * 32);
-        {
-            const bool dst = kind & 1;
-            if ((kind >> 1) < P::NU1) {
-                vec2<T> *wb = W + padx((dst ? P::S0 : 0) + P::big_cell(kind >> 1));
-                if (dst) unit_big<P::LB, P::RB, T, true>(wb, U, kc.u, lane);
-                else unit_big<P::LB, P::RB, T, false>(wb, U, kc.u, lane);
-            } else {
-                if (dst) unit_rest<LOG2N, T, true>(W, U, kc.u, lane);
-                else unit_rest<LOG2N, T, false>(W, U, kc.u, lane);
-            }
-        }
+        run_unit<LOG2N, T, 0>(W, kind, U, kc.u, lane);
         named_bar(bid, GW * 32);
         if (ditem < P::DT) Chain<LOG2N, T>::unit(W, out + sig(k) * P::N, ditem);
     }

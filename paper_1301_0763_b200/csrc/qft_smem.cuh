@@ -38,9 +38,34 @@
 #define QFT_RC_BIG 5  // phase-D unfold depth for N >= 2^13 (257 items at 2^14)
 #endif
 
+#ifndef QFT_SC
+// Sine side stored "as cosine": the sine cell of odd index (its element index
+// within the Lee block has the same parity) holds -ds instead of ds, the
+// cosine-side code runs on it (with the DST's L = 2 base constant), and each
+// sine block's spectrum lands reversed (slot k at L-1-k).  Exact: negation
+// commutes with IEEE rounding, the DCT fold of (a, -b) is the DST fold of
+// (a, b) (x - y == x + (-y)), and the DCT-II of ((-1)^i x_i) is the reversed
+// DST-II of x operation for operation (tests/emu checks it bit for bit).  One
+// code path for both sides halves the warp-unit code the instruction cache
+// must hold (ncu: no_instruction was the top stall of the unit phase).
+#define QFT_SC 1
+#endif
+
 namespace qft {
 
 QFT_HD constexpr int padx(int p) { return p + (p >> 5); }
+
+// the sine cell with index `cell` (relative to the sine region) of the fold
+// a = x[n], b = x[N-n]: ds = a - b, negated on odd cells when QFT_SC
+template <typename T>
+QFT_HD vec2<T> sine_cell(vec2<T> a, vec2<T> b, int cell) {
+    return (QFT_SC && (cell & 1)) ? vsub(b, a) : vsub(a, b);
+}
+// a value placed on the sine side as is (dst0 input), negated on odd cells when QFT_SC
+template <typename T>
+QFT_HD vec2<T> sine_val(vec2<T> v, int cell) {
+    return (QFT_SC && (cell & 1)) ? vec2<T>{-v.x, -v.y} : v;
+}
 
 template <int LOG2N>
 struct SPlan {
@@ -111,8 +136,8 @@ QFT_HD void a0_item(const vec2<T> *x, vec2<T> *w, int n) {
         vec2<T> a = x[n], b = x[P::N - n];
         const int j = ctz32((uint32_t)n);
         const int cell = P::m - (1 << (LOG2N - 1 - j)) + (n >> (j + 1));  // off_j + i
-        w[padx(cell)] = vadd(a, b);              // dc[n]   = x[n] + x[N-n]
-        w[padx(P::S0 + cell)] = vsub(a, b);      // ds[n-1] = x[n] - x[N-n]
+        w[padx(cell)] = vadd(a, b);                       // dc[n]   = x[n] + x[N-n]
+        w[padx(P::S0 + cell)] = sine_cell(a, b, cell);    // ds[n-1] = x[n] - x[N-n]
     }
 }
 
@@ -122,6 +147,7 @@ QFT_HD void a0_item(const vec2<T> *x, vec2<T> *w, int n) {
 // x[N - 64c - 2l] is the first element of lane l-1's mirror pair.
 struct A0Lane64 {
     int A, B, sh;  // padded cosine cell of the even sample of chunk c: A + c*B + (c >> sh)
+    int lj;        // its unpadded cell is off + c*B + lj (parity: (c*B + lj) & 1)
 };
 template <int LOG2N>
 QFT_HD A0Lane64 a0_lane64(int l) {
@@ -132,6 +158,7 @@ QFT_HD A0Lane64 a0_lane64(int l) {
     r.A = off + (off >> 5) + (l >> j);
     r.B = 32 >> j;
     r.sh = j;
+    r.lj = l >> j;
     return r;
 }
 template <typename T>
@@ -157,12 +184,13 @@ struct A0Chunk64 {
         const vec2<T> me = shfl_up(mn);                  // x[N - n_e] from lane l-1
         const int po = 33 * c + l;                       // block 0 cell 32c + l, padded
         w[po] = vadd(xo, mo);
-        w[po + PS] = vsub(xo, mo);
+        w[po + PS] = sine_cell(xo, mo, l);  // cell 32c + l
         const int pe = a.A + c * a.B + (c >> a.sh);
+        const int pc = c * a.B + a.lj;      // parity of the even sample's cell
 #if QFT_A0_SPLIT
         if (l & 1) {
             w[pe] = vadd(xe, me);
-            w[pe + PS] = vsub(xe, me);
+            w[pe + PS] = sine_cell(xe, me, pc);
         }
 #if defined(__CUDA_ARCH__)
         __syncwarp();
@@ -172,7 +200,7 @@ struct A0Chunk64 {
         if (l > 0) {
 #endif
             w[pe] = vadd(xe, me);
-            w[pe + PS] = vsub(xe, me);
+            w[pe + PS] = sine_cell(xe, me, pc);
         } else if (QFT_A0_LANE0 && l == 0) {
             if (c == 0) {
                 w[padx(P::BASE)] = xe;      // dc[0] = x[0]
@@ -181,7 +209,7 @@ struct A0Chunk64 {
                 const int n = 64 * c, j = ctz32((uint32_t)n);
                 const int cell = P::m - (1 << (LOG2N - 1 - j)) + (n >> (j + 1));
                 w[padx(cell)] = vadd(xe, m0);
-                w[padx(P::S0 + cell)] = vsub(xe, m0);
+                w[padx(P::S0 + cell)] = sine_cell(xe, m0, cell);
             }
         }
     }
@@ -213,14 +241,14 @@ QFT_HD void a0_item_real(const T *xa, const T *xb, vec2<T> *w, int n) {
             const vec2<T> a = at(n), b = at(P::N - n);
             const int c = cell_of(n);
             w[padx(c)] = vadd(a, b);
-            w[padx(P::S0 + c)] = vsub(a, b);
+            w[padx(P::S0 + c)] = sine_cell(a, b, c);
         }
     } else if constexpr (MODE == 2) {  // dct0: values s(0..m) are the cosine signal
         if (n == 0) w[padx(P::BASE)] = at(0);
         else if (n == P::m) w[padx(P::BASE + 1)] = at(P::m);
         else w[padx(cell_of(n))] = at(n);
     } else {  // dst0: values s(1..m-1) are the sine signal (slot n-1)
-        if (n > 0 && n < P::m) w[padx(P::S0 + cell_of(n))] = at(n - 1);
+        if (n > 0 && n < P::m) w[padx(P::S0 + cell_of(n))] = sine_val(at(n - 1), cell_of(n));
     }
 }
 
@@ -307,22 +335,23 @@ struct Top {
 
 // ---------------------------------------------------------------- phase B
 // Lee-32 on the 32-cell chunk at padded pointer c; in place.
+// ub: the L = 2 base constant index (lee_full)
 template <bool DST, typename T>
-QFT_HD void b_l32p(vec2<T> *c, const T *U) {
+QFT_HD void b_l32p(vec2<T> *c, const T *U, int ub = DST ? 1 : 0) {
     vec2<T> v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = c[e];
-    lee_full<32, DST, T>(v, U);
+    lee_full<32, DST, T>(v, U, ub);
 #pragma unroll
     for (int e = 0; e < 32; ++e) c[e] = v[e];
 }
 template <bool DST, typename T>
-QFT_HD void b_l32(vec2<T> *w, int chunk_base, const T *U) {
-    b_l32p<DST, T>(w + padx(chunk_base), U);
+QFT_HD void b_l32(vec2<T> *w, int chunk_base, const T *U, int ub = DST ? 1 : 0) {
+    b_l32p<DST, T>(w + padx(chunk_base), U, ub);
 }
 
 template <int LOG2N, bool DST, typename T, int J>
-QFT_HD void b_small_rec(vec2<T> *w, const T *U) {
+QFT_HD void b_small_rec(vec2<T> *w, const T *U, int ub) {
     using P = SPlan<LOG2N>;
     if constexpr (J <= LOG2N - 2) {
         constexpr int L = P::L(J);
@@ -330,17 +359,17 @@ QFT_HD void b_small_rec(vec2<T> *w, const T *U) {
         constexpr int b0 = (DST ? P::S0 : 0) + P::off(J);
 #pragma unroll
         for (int e = 0; e < L; ++e) v[e] = w[padx(b0 + e)];
-        lee_full<L, DST, T>(v, U);
+        lee_full<L, DST, T>(v, U, ub);
 #pragma unroll
         for (int e = 0; e < L; ++e) w[padx(b0 + e)] = v[e];
-        b_small_rec<LOG2N, DST, T, J + 1>(w, U);
+        b_small_rec<LOG2N, DST, T, J + 1>(w, U, ub);
     }
 }
 // all blocks with L <= 16 of one side
 template <int LOG2N, bool DST, typename T>
-QFT_HD void b_small(vec2<T> *w, const T *U) {
+QFT_HD void b_small(vec2<T> *w, const T *U, int ub = DST ? 1 : 0) {
     constexpr int J0 = SPlan<LOG2N>::JS > 0 ? SPlan<LOG2N>::JS : 0;
-    b_small_rec<LOG2N, DST, T, J0>(w, U);
+    b_small_rec<LOG2N, DST, T, J0>(w, U, ub);
 }
 
 // ---------------------------------------------------------------- phase C
@@ -394,7 +423,10 @@ struct Chain {
     // cosine spectrum of Lee block j, slot k
     static QFT_HD vec2<T> OC(const vec2<T> *w, int j, int k) { return w[padx(P::off(j) + k)]; }
     // sine spectrum of Lee block j, harmonic h (slot h-1)
-    static QFT_HD vec2<T> OS(const vec2<T> *w, int j, int h) { return w[padx(P::S0 + P::off(j) + h - 1)]; }
+    // (QFT_SC: the block spectrum is stored reversed, slot h-1 at L_j - h)
+    static QFT_HD vec2<T> OS(const vec2<T> *w, int j, int h) {
+        return w[padx(P::S0 + P::off(j) + (QFT_SC ? P::L(j) - h : h - 1))];
+    }
 
     // ---- uniform phase-D thread (t in [0, MRC], no special path) ----------
     // index of thread t's chain value at level J > RC: the distance of t to the

@@ -27,11 +27,11 @@ static void build_U(int N, const T *Tnat, std::vector<T> &U) {
 
 // big warp unit (unit_big in qft_launch.cuh) on the block at padded pointer wb
 template <int L, int R, typename T, bool DST, bool REV = false>
-static void emu_unit_big(vec2<T> *wb, const T *U) {
+static void emu_unit_big(vec2<T> *wb, const T *U, int ub = DST ? 1 : 0) {
     std::vector<FBlockP<L, R, DST, T>> f(32);
     for (int t = 0; t < 32; ++t) f[t].template load<REV>(wb, U, t);   // all lanes load ...
     for (int t = 0; t < 32; ++t) f[t].store(wb, t);     // ... __syncwarp ... store
-    for (int p = 0; p < (1 << R); ++p) b_l32p<DST, T>(wb + 33 * p, U);
+    for (int p = 0; p < (1 << R); ++p) b_l32p<DST, T>(wb + 33 * p, U, ub);
     using CB = CBlockP<R, DST, T>;
     std::vector<CB> c(32);
     std::vector<std::vector<vec2<T>>> outs(32, std::vector<vec2<T>>(CB::G));
@@ -81,11 +81,11 @@ static void emu_rest_c(vec2<T> *w) {
     }
 }
 template <int LOG2N, typename T, bool DST>
-static void emu_unit_rest(vec2<T> *w, const T *U) {
+static void emu_unit_rest(vec2<T> *w, const T *U, int ub = DST ? 1 : 0) {
     using P = SPlan<LOG2N>;
     emu_rest_f<LOG2N, T, P::JR, DST>(w, U);
-    for (int k = P::K0; k < P::NL32; ++k) b_l32<DST, T>(w, (DST ? P::S0 : 0) + 32 * k, U);
-    b_small<LOG2N, DST, T>(w, U);
+    for (int k = P::K0; k < P::NL32; ++k) b_l32<DST, T>(w, (DST ? P::S0 : 0) + 32 * k, U, ub);
+    b_small<LOG2N, DST, T>(w, U, ub);
     emu_rest_c<LOG2N, T, P::JR, DST>(w);
 }
 // top levels (top_f / top_b): every item loads before any store
@@ -111,13 +111,19 @@ static void emu_top_b(vec2<T> *w) {
 }
 // TF -> fused units -> TB of one side, in the kernel's order
 template <int LOG2N, typename T, bool DST>
-static void emu_side(vec2<T> *w, const T *U) {
+static void emu_side_impl(vec2<T> *w, const T *U, int ub) {
     using P = SPlan<LOG2N>;
     emu_top_f<LOG2N, T, 0, DST>(w, U);
     for (int bu = 0; bu < P::NU1; ++bu)
-        emu_unit_big<P::LB, P::RB, T, DST>(w + padx((DST ? P::S0 : 0) + P::big_cell(bu)), U);
-    emu_unit_rest<LOG2N, T, DST>(w, U);
+        emu_unit_big<P::LB, P::RB, T, DST>(w + padx((DST ? P::S0 : 0) + P::big_cell(bu)), U, ub);
+    emu_unit_rest<LOG2N, T, DST>(w, U, ub);
     emu_top_b<LOG2N, T, 0, DST>(w);
+}
+// QFT_SC: the sine side is the cosine code on the sine region (qft_launch.cuh run_unit)
+template <int LOG2N, typename T, bool DST>
+static void emu_side(vec2<T> *w, const T *U) {
+    if (QFT_SC && DST) emu_side_impl<LOG2N, T, false>(w + padx(SPlan<LOG2N>::S0), U, 1);
+    else emu_side_impl<LOG2N, T, DST>(w, U, DST ? 1 : 0);
 }
 
 template <int LOG2N, typename T>
@@ -261,7 +267,7 @@ static void emu_sub(const vec2<T> *w0, int m, vec2<T> *cb, vec2<T> *sb, const T 
                 const int jj = ctz32((uint32_t)k);
                 const int cell = P::m - (1 << (SUBLOG - 1 - jj)) + (k >> (jj + 1));
                 w[padx(cell)] = vadd(a, b);
-                w[padx(P::S0 + cell)] = vsub(a, b);
+                w[padx(P::S0 + cell)] = sine_cell(a, b, cell);
             }
         }
     } else {
@@ -272,6 +278,8 @@ static void emu_sub(const vec2<T> *w0, int m, vec2<T> *cb, vec2<T> *sb, const T 
     }
     w[padx(P::BASE)] = w0[2 * m - 1];
     w[padx(P::BASE + 1)] = w0[2 * m];
+    if (QFT_SC)  // the single-pass layout holds the odd sine cells negated (sub_item)
+        for (int c = 1; c < P::m - 1; c += 2) w[padx(P::S0 + c)] = vec2<T>{-w[padx(P::S0 + c)].x, -w[padx(P::S0 + c)].y};
     }
     emu_side<SUBLOG, T, false>(w, U);
     emu_side<SUBLOG, T, true>(w, U);
