@@ -14,9 +14,13 @@
 #if defined(__CUDACC__)
 #define QFT_HD __host__ __device__ __forceinline__
 #define QFT_DEV __device__ __forceinline__
+// a real call on the device: one copy of a large body shared by its callers
+// (instruction-cache footprint), inlined on the host
+#define QFT_HD_CALL __host__ __device__ __noinline__
 #else
 #define QFT_HD inline
 #define QFT_DEV inline
+#define QFT_HD_CALL inline
 #endif
 
 #if defined(__CUDACC__)

@@ -335,9 +335,18 @@ struct Top {
 
 // ---------------------------------------------------------------- phase B
 // Lee-32 on the 32-cell chunk at padded pointer c; in place.
-// ub: the L = 2 base constant index (lee_full)
+// ub: the L = 2 base constant index (lee_full).  QFT_L32_CALL: one copy of the
+// Lee-32 body for the big and the rest units (instruction-cache footprint)
+#ifndef QFT_L32_CALL
+#define QFT_L32_CALL 0  // measured slower (54.0 vs 58.3M tr/s, config 2): the call boundary costs more than the saved instruction fetch
+#endif
+#if QFT_L32_CALL
+#define QFT_L32_ATTR QFT_HD_CALL
+#else
+#define QFT_L32_ATTR QFT_HD
+#endif
 template <bool DST, typename T>
-QFT_HD void b_l32p(vec2<T> *c, const T *U, int ub = DST ? 1 : 0) {
+QFT_L32_ATTR void b_l32p(vec2<T> *c, const T *U, int ub = DST ? 1 : 0) {
     vec2<T> v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = c[e];
