@@ -341,11 +341,21 @@ def main():
     N, lg, prec, cfg, metric = config_meta(args.config)
     ws, rank, local = dist_env()
     dist = None
+    # QFT_BENCH_BACKEND=gloo + QFT_BENCH_DEVICE=0: run the multi-rank path on one GPU (functional
+    # check of the sharding / barrier / max-over-ranks logic -- the ranks never wait on each
+    # other's kernels, the only cross-rank traffic is the timing reduction)
+    backend = os.environ.get("QFT_BENCH_BACKEND", "nccl")
+    if os.environ.get("QFT_BENCH_DEVICE") is not None:
+        local = int(os.environ["QFT_BENCH_DEVICE"])
     if ws > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
+    cdev = dev if backend == "nccl" else torch.device("cpu")  # where the timing collectives run
     torch.cuda.set_device(dev)
     if args.config == 5:  # the box-wide batch 2^18 is split evenly (strong scaling, no collective)
         from paper_1301_0763_b200.sharding import shard_bounds
@@ -379,7 +389,7 @@ def main():
     ms_local = ev0.elapsed_time(ev1) / args.steps
     ms, per_rank = ms_local, [ms_local]
     if dist:
-        t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms_local], device=cdev, dtype=torch.float64)
         allt = [torch.empty_like(t) for _ in range(ws)]
         dist.all_gather(allt, t)
         per_rank = [float(a.item()) for a in allt]
@@ -405,7 +415,7 @@ def main():
             plan.exec_host(hin.data_ptr(), hout.data_ptr(), hb, (N, 1), (N, 1))
         el = (time.perf_counter() - t0) / reps
         if dist:
-            t = torch.tensor([el], device=dev, dtype=torch.float64)
+            t = torch.tensor([el], device=cdev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
         e2e = {"value": ws * hb / el, "unit": UNIT, "h2d_bytes_per_step": hb * N * esz,
@@ -435,7 +445,7 @@ def main():
         thr = max(1, oracle.max_threads() // ws)
         parity = par.check_rows(x, y, nthreads=thr)
         if dist:
-            t = torch.tensor([parity["rows_checked"], parity["mismatches"]], device=dev, dtype=torch.int64)
+            t = torch.tensor([parity["rows_checked"], parity["mismatches"]], device=cdev, dtype=torch.int64)
             dist.all_reduce(t)
             parity["rows_checked"], parity["mismatches"] = int(t[0]), int(t[1])
         parity["against"] = "oracle/ (C restatement pinned to the reference by tests/golden)"
@@ -471,7 +481,9 @@ def main():
                        "parallelism": f"batch-sharded x{ws}, no collective",
                        "l2": ("input > 126 MB L2 (no flush needed)" if B * N * esz > (126 << 20)
                               else "input fits L2: steps re-read a warm L2 (small config)")},
-            "per_gpu": {"value": [B / (t / 1000.0) for t in per_rank], "ms_per_step": per_rank},
+            "per_gpu": {"value": [B / (t / 1000.0) for t in per_rank], "ms_per_step": per_rank,
+                        **({"note": f"{ws} ranks on one GPU ({backend}): functional run, not a scaling point"}
+                           if os.environ.get("QFT_BENCH_DEVICE") is not None and ws > 1 else {})},
             "e2e": e2e,
             "e2e_dropin": e2e_dropin,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

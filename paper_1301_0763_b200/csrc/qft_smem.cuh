@@ -31,6 +31,9 @@
 #ifndef QFT_A0_LANE0
 #define QFT_A0_LANE0 0  // A0 chunk lane 0 also folds n = 64c (else a separate pass)
 #endif
+#ifndef QFT_CHAIN_LIN
+#define QFT_CHAIN_LIN 0  // phase-D unfold with linear addresses (Chain::up_l); measured neutral (58.3 vs 58.5M, config 2)
+#endif
 #ifndef QFT_RC_SMALL
 #define QFT_RC_SMALL 5  // phase-D unfold depth for N <= 2^12
 #endif
@@ -497,11 +500,40 @@ struct Chain {
         }
     }
 
+    // ---- the same unfold with linear addresses (QFT_SC, L_{RC-1} >= 32) ----------
+    // Every index the unfold reads at level J is k = K + S*t with K a compile-time
+    // multiple of 32 (0, m_J - K, ...) and S = +-1, and every block it reads is
+    // 32-aligned, so the padded address is padx(cell(K)) + (S > 0 ? fwd : rev) with
+    // the per-thread constants fwd = padx(K0 + t) - padx(K0) = t + t/32 and
+    // rev = padx(K0 - t) - padx(K0) = -t - ceil(t/32) (any K0 = 0 mod 32): one
+    // shared load with an immediate offset per value instead of index arithmetic.
+    // Reads of a self-paired / harmonic-0 slot fall on a neighbouring cell of the
+    // working area and are discarded by the same selects as in up_e.
+    static constexpr bool LIN = QFT_CHAIN_LIN && QFT_SC && P::RC >= 1 && P::RC < n - 1 && (P::N >> (P::RC + 1)) >= 32;
+    template <int J, int K, int S, class Emit>
+    static QFT_HD void up_l(const vec2<T> *w, Emit &emit, int k, vec2<T> cv, vec2<T> sv, int fwd, int rev) {
+        if constexpr (J == 0) {
+            emit(k, cv, sv);
+        } else {
+            constexpr int q = qj(J - 1), mm = 2 * q;
+            constexpr int CB = P::off(J - 1) + K;                  // OC(J-1, K) cell
+            constexpr int SB = P::S0 + P::off(J - 1) + P::L(J - 1) - K;  // OS(J-1, K) cell (reversed)
+            static_assert(CB % 32 == 0 && SB % 32 == 0, "linear unfold needs 32-aligned cells");
+            const bool self = (k == q);
+            const vec2<T> o = w[padx(CB) + (S > 0 ? fwd : rev)];
+            const vec2<T> os = w[padx(SB) + (S > 0 ? rev : fwd)];
+            up_l<J - 1, K, S>(w, emit, k, self ? cv : vadd(cv, o), self ? os : vadd(os, sv), fwd, rev);
+            up_l<J - 1, mm - K, -S>(w, emit, self ? q : mm - k, self ? cv : vsub(cv, o), self ? os : vsub(os, sv),
+                                    fwd, rev);
+        }
+    }
+
     template <class Emit>
     static QFT_HD void unit_e(const vec2<T> *w, Emit &emit, int t) {
         vec2<T> cv, sv;
         if constexpr (P::RC < n - 1) desc2<P::RC>(w, t, cv, sv);
-        up_e<P::RC>(w, emit, t, cv, sv);
+        if constexpr (LIN) up_l<P::RC, 0, 1>(w, emit, t, cv, sv, t + (t >> 5), -t - ((t + 31) >> 5));
+        else up_e<P::RC>(w, emit, t, cv, sv);
     }
     static QFT_HD void unit(const vec2<T> *w, vec2<T> *y, int t) {
         auto emit = [&](int k, vec2<T> cv, vec2<T> sv) { emit_u(y, k, cv, sv); };
