@@ -44,6 +44,9 @@
 #ifndef QFT_PIPE_UMAP
 #define QFT_PIPE_UMAP 1  // measured +0.3 % (55.13 vs 54.91M tr/s, 3 interleaved rounds)
 #endif
+#ifndef QFT_PIPE_L2PF
+#define QFT_PIPE_L2PF 0  // L2 bulk prefetch of the batch after the next
+#endif
 #ifndef QFT_PIPE_TMA_WARP
 // warp issuing the refill TMA after the phase-2 barrier: an A0 warp has no
 // outstanding global stores for its fence.proxy.async to drain (a D warp does)
@@ -135,19 +138,26 @@ QFT_DEV void named_bar(int id, int nthreads) { asm volatile("bar.sync %0, %1;" :
 // parallel; each issuing lane first orders the CTA's earlier generic accesses
 // of the slots -- published to it by the preceding barrier -- before its
 // async-proxy writes)
+#ifndef QFT_PIPE_TMA_SPLIT
+#define QFT_PIPE_TMA_SPLIT 8  // bulk copies per signal (issued by parallel lanes): measured 1 / 2 / 4 / 8 = 58.5 / 58.7 / 58.8 / 59.1M tr/s
+#endif
 template <int LOG2N, typename T>
 QFT_DEV void tma_load_slots(vec2<T> *X, const vec2<T> *src, int ntr, uint64_t *bar, int lane) {
     using P = SPlan<LOG2N>;
-    constexpr uint32_t BYTES = P::N * (uint32_t)sizeof(vec2<T>);
+    constexpr int K = QFT_PIPE_TMA_SPLIT;
+    constexpr uint32_t BYTES = P::N * (uint32_t)sizeof(vec2<T>), PART = BYTES / K;
+    static_assert(BYTES % K == 0 && PART % 16 == 0 && K <= 8, "16-byte bulk-copy parts, <= 8 per signal");
     if (lane == 0)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(BYTES * ntr)
                      : "memory");
     __syncwarp();
-    if (lane < ntr) {
+    if (lane < ntr * K) {
+        const int tau = lane / K, k = lane - tau * K;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         smem_u32(X + lane * P::PADDED)),
-                     "l"(src + (long long)lane * P::N), "r"(BYTES), "r"(smem_u32(bar))
+                         smem_u32(X + tau * P::PADDED) + k * PART),
+                     "l"(reinterpret_cast<const char *>(src + (long long)tau * P::N) + (size_t)k * PART), "r"(PART),
+                     "r"(smem_u32(bar))
                      : "memory");
     }
 }
@@ -308,6 +318,11 @@ __global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
         // set cur is free: bring in batch bt + 2G
         if (!QFT_PIPE_TMA_EARLY && warp == QFT_PIPE_TMA_WARP && bt + 2 * G < nbatch)
             tma_load_slots<LOG2N, T>(W, in + (bt + 2 * G) * TT * P::N, ntr_of(bt + 2 * G), &bar[cur], lane);
+#if QFT_PIPE_L2PF
+        // the batch after that into L2, so its bulk copy one iteration later is served from L2
+        if (warp == QFT_PIPE_TMA_WARP + 1 && lane < TT && bt + 3 * G < nbatch && lane < ntr_of(bt + 3 * G))
+            l2_prefetch(in + ((bt + 3 * G) * TT + lane) * P::N, P::N * (uint32_t)sizeof(vec2<T>));
+#endif
         QFT_MARK(6);
         cur ^= 1;
     }

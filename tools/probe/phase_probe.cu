@@ -102,6 +102,27 @@ int main(int argc, char **argv) {
     }
 #endif
 
+#ifdef PIPE
+    {   // per warp: end of its phase-2 work (D or in-place A0) and, for A0 warps, the end of
+        // the TMA wait, relative to the phase-2 start (mark 3); medians over CTAs, iterations 2..13
+        printf("phase-2 per warp (median cycles after the units barrier): ");
+        for (int w = 0; w < K::NW; ++w) {
+            std::vector<double> e, wt;
+            for (int c = 0; c < sms; ++c)
+                for (int it = 2; it < 14; ++it) {
+                    long long *m = &b[(c * 16 + it) * 64];
+                    e.push_back(m[52 + w] - m[3]);
+                    wt.push_back(m[40 + w] - m[3]);
+                }
+            std::sort(e.begin(), e.end());
+            std::sort(wt.begin(), wt.end());
+            const bool a0 = w >= K::NWD && w < K::NWD + K::NWA;
+            if (a0) printf("w%d[A0 wait %.0f end %.0f] ", w, wt[wt.size() / 2], e[e.size() / 2]);
+            else printf("w%d[D end %.0f] ", w, e[e.size() / 2]);
+        }
+        printf("\n");
+    }
+#endif
     // per-phase durations over CTAs < sms, iterations 2..13
 #ifdef PIPE
     // pipe marks: 1 start, 3 after units, 4 D done (thread 0), 5 after phase-2 barrier
