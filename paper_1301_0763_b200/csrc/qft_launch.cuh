@@ -415,7 +415,10 @@ struct CRest<LOG2N, T, DST, J, true> {
         next.store(w, lane);
     }
 };
-template <int LOG2N, typename T, bool DST>
+// SMALL = false: the blocks with L <= 16 are left to the caller (the pipelined
+// kernel runs them in phase 2 on idle lanes: here lane CNT would diverge from the
+// Lee-32 lanes and serialise the warp)
+template <int LOG2N, typename T, bool DST, bool SMALL = true>
 QFT_DEV void unit_rest(vec2<T> *w, const T *U, const T *kcu, int lane, int ub = DST ? 1 : 0) {
     using P = SPlan<LOG2N>;
     constexpr int sb = DST ? P::S0 : 0;
@@ -432,7 +435,7 @@ QFT_DEV void unit_rest(vec2<T> *w, const T *U, const T *kcu, int lane, int ub = 
 #endif
     __syncwarp();
     if (lane < CNT) b_l32<DST, T>(w, sb + 32 * (P::K0 + lane), kcu, ub);
-    else if (lane == CNT) b_small<LOG2N, DST, T>(w, kcu, ub);
+    else if (SMALL && lane == CNT) b_small<LOG2N, DST, T>(w, kcu, ub);
     __syncwarp();
 #if QFT_REST_FUSED
     {
@@ -531,7 +534,7 @@ QFT_DEV void top_b(vec2<T> *W, int ntr, int tid) {
 
 // fused unit `kind` of the signal at w: side kind & 1, big unit kind >> 1 (or
 // the rest unit when kind >> 1 == NU1)
-template <int LOG2N, typename T, int MODE>
+template <int LOG2N, typename T, int MODE, bool SMALL = true>
 QFT_DEV void run_unit(vec2<T> *w, int kind, const T *U, const T *kcu, int lane) {
     using P = SPlan<LOG2N>;
     const bool dst = kind & 1;
@@ -540,7 +543,7 @@ QFT_DEV void run_unit(vec2<T> *w, int kind, const T *U, const T *kcu, int lane) 
     if constexpr (QFT_SC) {  // both sides through the cosine code (qft_smem.cuh QFT_SC)
         vec2<T> *ws = w + (dst ? padx(P::S0) : 0);
         if (bu < P::NU1) unit_big<P::LB, P::RB, T, false>(ws + padx(P::big_cell(bu)), U, kcu, lane, dst);
-        else unit_rest<LOG2N, T, false>(ws, U, kcu, lane, dst);
+        else unit_rest<LOG2N, T, false, SMALL>(ws, U, kcu, lane, dst);
     } else if (bu < P::NU1) {
         vec2<T> *wb = w + padx((dst ? P::S0 : 0) + P::big_cell(bu));
         if (dst) unit_big<P::LB, P::RB, T, true>(wb, U, kcu, lane);
@@ -552,14 +555,14 @@ QFT_DEV void run_unit(vec2<T> *w, int kind, const T *U, const T *kcu, int lane) 
 }
 
 // A+B+C of TT signals, one warp per (signal, side, unit)
-template <int LOG2N, typename T, int MODE, int TT, int NW>
+template <int LOG2N, typename T, int MODE, int TT, int NW, bool SMALL = true>
 QFT_DEV void fused_units(vec2<T> *W, const T *U, const T *kcu, int ntr, int warp, int lane) {
     using P = SPlan<LOG2N>;
     constexpr int NU = 2 * (P::NU1 + 1);
     for (int u = warp; u < TT * NU; u += NW) {
         const int tau = u / NU, kind = u - tau * NU;
         if (tau >= ntr) continue;
-        run_unit<LOG2N, T, MODE>(W + tau * P::PADDED, kind, U, kcu, lane);
+        run_unit<LOG2N, T, MODE, SMALL>(W + tau * P::PADDED, kind, U, kcu, lane);
         __syncwarp();
     }
 }

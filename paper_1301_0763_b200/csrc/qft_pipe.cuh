@@ -44,6 +44,9 @@
 #ifndef QFT_PIPE_UMAP
 #define QFT_PIPE_UMAP 1  // measured +0.3 % (55.13 vs 54.91M tr/s, 3 interleaved rounds)
 #endif
+#ifndef QFT_PIPE_SMALLD
+#define QFT_PIPE_SMALLD 1  // blocks with L <= 16 in phase 2 (idle D lanes) instead of a divergent rest-unit lane
+#endif
 #ifndef QFT_PIPE_L2PF
 #define QFT_PIPE_L2PF 0  // L2 bulk prefetch of the batch after the next
 #endif
@@ -112,6 +115,9 @@ struct PCfg {
     static constexpr int NT = NW * 32;
     static constexpr int NC64 = P::m / 64;  // A0 chunks per signal
     static constexpr int RA = (NC64 + NWA - 1) / NWA;
+    // small blocks in phase 2 on the D warps' idle lanes (QFT_PIPE_SMALLD)
+    static constexpr bool SMALLD = QFT_PIPE_SMALLD && !QFT_PIPE_DSPREAD && P::JS >= 0 &&
+                                   (TT > 0 ? TT : 1) * DI <= NWD * 32 - 2 * (TT > 0 ? TT : 1);
     static constexpr int X_OFF = 0;
     static constexpr int U_OFF = 2 * (TT > 0 ? TT : 1) * PER_W;
     static constexpr int ITM_OFF = (U_OFF + UB + 15) / 16 * 16;  // per slot: x[64c], x[N-64c], c < NC64
@@ -277,11 +283,23 @@ __global__ void __launch_bounds__(PCfg<LOG2N, T>::NT, 1)
         vec2<T> *W = set(cur);
         QFT_MARK(1);
         QFT_PMARK24();
-        fused_units<LOG2N, T, 0, TT, NW>(W, U, kc.u, ntr, uwarp, lane);
+        fused_units<LOG2N, T, 0, TT, NW, !C::SMALLD>(W, U, kc.u, ntr, uwarp, lane);
         QFT_WMARK();
         __syncthreads();
         QFT_MARK(3);
         if (warp < NWD) {
+            if constexpr (C::SMALLD) {
+                // the blocks with L <= 16 (both sides of every signal) on the last D warp's
+                // idle lanes, then the D warps meet: every phase-D item reads them
+                const int sl = tid - (NWD * 32 - 2 * TT);
+                if (sl >= 0 && (sl >> 1) < ntr) {
+                    vec2<T> *w = W + (sl >> 1) * P::PADDED;
+                    if (QFT_SC) b_small<LOG2N, false, T>(w + ((sl & 1) ? padx(P::S0) : 0), kc.u, sl & 1);
+                    else if (sl & 1) b_small<LOG2N, true, T>(w, kc.u);
+                    else b_small<LOG2N, false, T>(w, kc.u);
+                }
+                named_bar(2, NWD * 32);
+            }
             if (QFT_PIPE_DSPREAD) {
                 const int it = warp * C::DPW + lane;  // DPW <= 32 consecutive items per warp
                 const int tau = it / P::DT, ti = it - tau * P::DT;
