@@ -502,7 +502,11 @@ def main():
                              "source": tr.get("_file")},
                          "dominant_kernel": tr.get("dominant_kernel") if tr else None,
                          "dominant_share_of_step": tr.get("dominant_share_of_step") if tr else None,
-                         "algorithmic_bytes_per_transform": 2 * esz * N, "passes": info.passes},
+                         "algorithmic_bytes_per_transform": 2 * esz * N, "passes": info.passes,
+                         # also against the 8.0 TB/s nominal HBM3e figure, and the
+                         # paper's flop count 4N lgN - 6N + 8 per transform as GFLOP/s
+                         "frac_of_nominal_8tbs": achieved / 8000.0,
+                         "paper_gflops": (4 * N * lg - 6 * N + 8) * (B / (ms_local / 1000.0)) / 1e9},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": args.steps * info.kernel_launches,
