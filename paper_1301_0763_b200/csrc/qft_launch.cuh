@@ -27,6 +27,12 @@
 #ifndef QFT_MIXED_STAGE
 #define QFT_MIXED_STAGE 0  // see KCfg::MIXED
 #endif
+#ifndef QFT_A0_PRE
+#define QFT_A0_PRE 0  // next signal's A0 chunks loaded by idle phase-D warps: measured slower (config 5: 9.7 / 10.9 / 8.0M for 2 / 4 / 8 chunks per warp vs 11.06M)
+#endif
+#ifndef QFT_A0_PRE_UNR
+#define QFT_A0_PRE_UNR 4  // chunks per prefetching warp (8 spills at 128 registers)
+#endif
 #ifndef QFT_NW_MIN
 #define QFT_NW_MIN 4       // lower bound on warps per CTA
 #endif
@@ -569,15 +575,16 @@ QFT_DEV void fused_units(vec2<T> *W, const T *U, const T *kcu, int ntr, int warp
 
 // A0 of TT complex signals from src (staging buffer or global memory): chunks
 // of 64 consecutive n per warp, UNR chunks in flight; then the multiples of 64.
+// first: chunks [0, first) of a single signal (TTn == 1) were loaded ahead (QFT_A0_PRE)
 template <int LOG2N, typename T, int UNR>
 QFT_DEV void a0_complex(const vec2<T> *src, vec2<T> *W, int ntr, int TTn, int tid, int NT, int NW,
-                        const A0Lane64 &a0l64) {
+                        const A0Lane64 &a0l64, int first = 0) {
     using P = SPlan<LOG2N>;
     const int lane = tid & 31, warp = tid >> 5;
     if constexpr (P::m >= 64) {
         constexpr int NC64 = P::m / 64;
         auto shfl_up = [](vec2<T> v) { return shfl_vec(v, false); };
-        for (int u0 = warp; u0 < TTn * NC64; u0 += NW * UNR) {
+        for (int u0 = first + warp; u0 < TTn * NC64; u0 += NW * UNR) {
             A0Chunk64<T> ch[UNR];
 #pragma unroll
             for (int r = 0; r < UNR; ++r) {
@@ -640,6 +647,16 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
     if (TMA && tid == 0 && bt < nbatch)
         tma_bulk_load(stage, in + bt * tt * P::N, (uint32_t)(stage_count(bt) * P::N * K::VB), bar);
     uint32_t parity = 0;
+    // QFT_A0_PRE: one signal per iteration read from global memory (no staging room):
+    // the warps without a phase-D item load the first PRE_C A0 chunks of the next
+    // signal into registers during phase D, and store them at the next A0
+    constexpr int WD = (TT * K::DI + 31) / 32, NPW = NW > WD ? NW - WD : 0;
+    constexpr bool PRE = QFT_A0_PRE && MODE == 0 && TS == 0 && TT == 1 && sizeof(T) == 4 && P::m >= 64 && NPW > 0;
+    constexpr int PU = QFT_A0_PRE_UNR;  // chunks per prefetching warp
+    constexpr int PRE_C0 = PRE ? NPW * PU : 0;
+    constexpr int PRE_C = PRE_C0 < P::m / 64 ? PRE_C0 : P::m / 64;
+    A0Chunk64<T> pre[PRE ? PU : 1];
+    bool pre_ok = false;
     for (; bt < nbatch; bt += gridDim.x) {
         const int ntr = (int)((batch - bt * tt) < tt ? (batch - bt * tt) : tt);
         QFT_MARK(0);
@@ -665,7 +682,17 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
                     a0_item_real<LOG2N, T, MODE>(xr + ra * RL, xr + rb * RL, W + tau * P::PADDED, nn);
             }
         } else {
-            if constexpr (TS < TT) {
+            if constexpr (PRE) {
+                if (pre_ok && warp >= WD) {
+                    auto shfl_up = [](vec2<T> v) { return shfl_vec(v, false); };
+#pragma unroll
+                    for (int r = 0; r < PU; ++r) {
+                        const int c = (warp - WD) + r * NPW;
+                        if (c < PRE_C) pre[r].template store<LOG2N>(W, c, lane, a0l64, shfl_up);
+                    }
+                }
+                a0_complex<LOG2N, T, QFT_A0_UNR>(in + bt * P::N, W, 1, 1, tid, NT, NW, a0l64, pre_ok ? PRE_C : 0);
+            } else if constexpr (TS < TT) {
                 if (ntr > TS)
                     a0_complex<LOG2N, T, sizeof(T) == 8 ? 1 : QFT_A0_UNR>(in + (bt * tt + TS) * P::N,
                                                                           W + TS * P::PADDED, ntr - TS, TT - TS, tid,
@@ -726,6 +753,19 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
                 };
                 if constexpr (K::DHALF) Chain<LOG2N, T>::unit_e_half(W + tau * P::PADDED, emit, t, h);
                 else Chain<LOG2N, T>::unit_e(W + tau * P::PADDED, emit, t);
+            }
+        }
+        if constexpr (PRE) {
+            // warps with no phase-D item: the next signal's first A0 chunks into registers
+            // (its L2 prefetch was issued at the top of this iteration)
+            pre_ok = bt + gridDim.x < nbatch;
+            if (pre_ok && warp >= WD) {
+                const vec2<T> *nx = in + (bt + gridDim.x) * P::N;
+#pragma unroll
+                for (int r = 0; r < PU; ++r) {
+                    const int c = (warp - WD) + r * NPW;
+                    if (c < PRE_C) pre[r].template load<LOG2N>(nx, c, lane);
+                }
             }
         }
         QFT_MARK(4);
