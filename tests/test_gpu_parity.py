@@ -260,7 +260,7 @@ def test_real_entry_points_counts_and_errors(torch_cuda):
 
 
 @pytest.mark.parametrize("dt", [np.complex64, np.complex128])
-@pytest.mark.parametrize("lg", [1, 2, 3, 4, 5, 6, 8, 10, 12, 14])
+@pytest.mark.parametrize("lg", [1, 2, 3, 4, 5, 6, 8, 10, 12, 14, 15, 16])  # 15, 16: one CTA team per signal
 def test_classical_cdft_bitwise(torch_cuda, oracle_mod, dt, lg):
     """classical.cdft (classical.py:156-167) on the GPU, bit-identical to the oracle."""
     from paper_1301_0763_b200 import classical
@@ -292,7 +292,7 @@ def test_classical_golden_digests_and_semantics(golden, torch_cuda, oracle_mod):
 
 
 @pytest.mark.parametrize("kind", ["rdft", "dct0", "dst0"])
-@pytest.mark.parametrize("lg", [3, 7, 11])
+@pytest.mark.parametrize("lg", [3, 7, 11, 15])
 def test_classical_real_entry_points(torch_cuda, oracle_mod, kind, lg):
     from paper_1301_0763_b200 import classical
     N = 1 << lg
