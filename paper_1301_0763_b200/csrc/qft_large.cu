@@ -54,6 +54,7 @@ struct Chunk {
 
 struct TaskSet {  // one launch: tasks of one kind and one R (or log2 L for leaves)
     int R = 0;
+    int staged = 0;  // F: fp64 five-level first-touch tasks through lg_f_staged_kernel
     void *d_tasks = nullptr, *d_dsts = nullptr, *d_chunks = nullptr, *d_rs = nullptr;
     int ntasks = 0, nchunks = 0;
 };
@@ -337,6 +338,93 @@ QFT_DEV void cp_async_cell(vec2<T> *dst, const vec2<T> *src) {
 QFT_DEV void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// fp64 first-touch F tasks with their x samples staged in shared memory by
+// cp.async (QFT_F_STAGED).  The cosine and the sine task of a Lee block read the
+// same samples (dc = x[n] + x[N-n], ds = x[n] - x[N-n]), so a CTA takes both: the
+// strided first-touch gathers are L2-bound (ncu: ~2 L2 sectors per useful sample,
+// 5.8 GB of L2 reads for 1.1 GB of DRAM at N = 2^20), and staging once for both
+// sides halves them.  Chunks of one signal are adjacent in the grid, so the blocks'
+// gathers share x's sectors in L2.  A CTA of 256 threads takes GP reflection groups
+// of one (cosine, sine) task pair: R = 5, GP = 64, thread (role, g) is side role & 1,
+// child role >> 1 (lane pairs as lg_f_pair5); R <= 4, GP = 128, thread (side, g) does
+// the whole group (lg_f_group).  stage[s][g] = (x[n], x[N-n]), n = 2^j (2e+1).
+#ifndef QFT_F_STAGED
+#define QFT_F_STAGED 1
+#endif
+#ifndef QFT_F_STG_T
+#define QFT_F_STG_T 256
+#endif
+constexpr int kStgT = QFT_F_STG_T;  // threads per CTA
+constexpr int stg_groups(int R) { return R == 5 ? kStgT / 4 : kStgT / 2; }
+template <int R, typename T>
+__device__ __forceinline__ void f_staged_chunk(vec2<T> *stg, const int *runc, const int *runs, const FTask *tp,
+                                               int t0, vec2<T> *w, const vec2<T> *xb, int N, const T *U) {
+    constexpr int G = 1 << R, GP = stg_groups(R);
+    const int tid = threadIdx.x;
+    const int gg = tid & (GP - 1), role = tid / GP;
+    const bool dst = role & 1;
+    const FTask tk = tp[dst ? 1 : 0];  // cosine task, its sine partner next
+    const int ng = min(GP, (tk.L >> R) - t0);
+    for (int q = tid; q < G * GP * 2; q += kStgT) {
+        const int half = q & 1, g2 = (q >> 1) % GP, s = (q >> 1) / GP;
+        if (g2 < ng) {
+            const int e = runc[s] + runs[s] * (t0 + g2);
+            const int n = (2 * e + 1) << tk.j;
+            cp_async_cell<T>(stg + q, xb + (half ? N - n : n));
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (gg < ng) {
+        const int t = t0 + gg;
+        auto ld = [&](int s, int) {
+            const vec2<T> *p = stg + (s * GP + gg) * 2;
+            return dst ? vsub(p[0], p[1]) : vadd(p[0], p[1]);  // ds / dc fold (shared.py:28-35)
+        };
+        if constexpr (R == 5) {
+            const int h = role >> 1;
+            if (dst) lg_f_pair5_ld<T, true>(w, tk, t, h, U, ld);
+            else lg_f_pair5_ld<T, false>(w, tk, t, h, U, ld);
+        } else {
+            if (dst) lg_f_group_ld<R, T, true>(w, tk, t, U, ld);
+            else lg_f_group_ld<R, T, false>(w, tk, t, U, ld);
+        }
+    }
+}
+template <typename T>
+__global__ void __launch_bounds__(kStgT, 512 / kStgT) lg_f_staged_kernel(vec2<T> *__restrict__ W0, const FTask *__restrict__ tasks,
+                                                              const int *__restrict__ rs, const Chunk *__restrict__ chunks,
+                                                              int nchunks, const T *__restrict__ U, long long batch,
+                                                              long long Ws, const vec2<T> *__restrict__ x, int N) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    vec2<T> *stg = reinterpret_cast<vec2<T> *>(smem_raw);
+    __shared__ int runc[32], runs[32];
+    const int tid = threadIdx.x;
+    for (long long g = blockIdx.x; g < (long long)nchunks * batch; g += gridDim.x) {
+        const long long b = g / nchunks;
+        const Chunk ch = chunks[g - b * nchunks];
+        const int R = rs[ch.task];
+        const FTask *tp = tasks + ch.task;
+        if (tid < (1 << R)) {
+            int c, sg;
+            run_of(R, tp->L, tid, c, sg);
+            runc[tid] = c;
+            runs[tid] = sg;
+        }
+        __syncthreads();
+        vec2<T> *w = W0 + b * Ws;
+        const vec2<T> *xb = x + b * N;
+        switch (R) {
+            case 5: f_staged_chunk<5, T>(stg, runc, runs, tp, ch.t0, w, xb, N, U); break;
+            case 4: f_staged_chunk<4, T>(stg, runc, runs, tp, ch.t0, w, xb, N, U); break;
+            case 3: f_staged_chunk<3, T>(stg, runc, runs, tp, ch.t0, w, xb, N, U); break;
+            case 2: f_staged_chunk<2, T>(stg, runc, runs, tp, ch.t0, w, xb, N, U); break;
+            case 1: f_staged_chunk<1, T>(stg, runc, runs, tp, ch.t0, w, xb, N, U); break;
+        }
+        __syncthreads();  // the next chunk's copies overwrite the stage and the run table
+    }
 }
 
 // the W0 cells an item reads, as up to 3 runs (lowest cell, count) -- for the
@@ -751,22 +839,49 @@ int QFT_LG(qft_large_create)(int log2n, int real_modes, void **out) {
     p->fset.resize(S.f.size());
     p->bset.resize(S.b.size());
     for (size_t d = 0; d < S.f.size(); ++d) {
-        {
+        // staged tasks (lg_f_staged_kernel): fp64 first-touch cosine tasks and their sine
+        // partner (same R, block j and length), stored as adjacent pairs
+        auto partner = [&](int R, const FTask &f) -> const FTask * {
+            if (!(QFT_F_STAGED && QFT_LARGE_PREC == 64 && f.j >= 0)) return nullptr;
+            for (auto &q : S.f[d].at(R))
+                if (q.second == 1 && q.first.j == f.j && q.first.L == f.L) return &q.first;
+            return nullptr;
+        };
+        auto staged_task = [&](int R, const FTask &f, int side) {
+            if (side == 0) return partner(R, f) != nullptr;
+            for (auto &q : S.f[d].at(R))
+                if (q.second == 0 && q.first.j == f.j && q.first.L == f.L && partner(R, q.first)) return true;
+            return false;
+        };
+        for (int staged = 0; staged < 2; ++staged) {
             TaskSet ts;
+            ts.staged = staged;
             std::vector<FTask> tk;
             std::vector<int> ds, rs;
             std::vector<Chunk> ch;
             for (auto &kv : S.f[d])
                 for (size_t i = 0; i < kv.second.size(); ++i) {
+                    const FTask &f = kv.second[i].first;
+                    const int side = kv.second[i].second;
+                    const bool st = staged_task(kv.first, f, side);
+                    if (st != (staged == 1)) continue;
+                    if (st && side == 1) continue;  // pushed with its cosine partner
                     const int id = (int)tk.size();
-                    tk.push_back(kv.second[i].first);
-                    ds.push_back(kv.second[i].second);
+                    tk.push_back(f);
+                    ds.push_back(side);
                     rs.push_back(kv.first);
-                    const int groups = kv.second[i].first.L >> kv.first;
+                    if (st) {
+                        tk.push_back(*partner(kv.first, f));
+                        ds.push_back(1);
+                        rs.push_back(kv.first);
+                    }
+                    const int groups = f.L >> kv.first;
                     // fp64 R = 5: two threads per reflection group
-                    const int step = (QFT_LARGE_PREC == 64 && kv.first == 5) ? kChunk / 2 : kChunk;
+                    const int step = st ? stg_groups(kv.first)
+                                        : ((QFT_LARGE_PREC == 64 && kv.first == 5) ? kChunk / 2 : kChunk);
                     for (int t0 = 0; t0 < groups; t0 += step) ch.push_back({id, t0});
                 }
+            if (tk.empty()) continue;
             ts.ntasks = (int)tk.size();
             ts.nchunks = (int)ch.size();
             rc |= upload(tk, &ts.d_tasks) | upload(ds, &ts.d_dsts) | upload(rs, &ts.d_rs) | upload(ch, &ts.d_chunks);
@@ -881,9 +996,18 @@ int QFT_LG(qft_large_exec)(void *pp, int mode, const void *d_in, void *d_out, lo
         for (auto &ts : v) {
             const long long work = (long long)ts.nchunks * batch;
             const unsigned grid = (unsigned)std::min<long long>(work, 1 << 20);
-            e = launch(lg_f_kernel<T>, dim3(grid), dim3(kChunk), 0, st, W0, (const FTask *)ts.d_tasks,
-                       (const int *)ts.d_dsts, (const int *)ts.d_rs, (const Chunk *)ts.d_chunks, ts.nchunks, U, batch,
-                       Ws, x, S.N);
+            if (ts.staged) {
+                const int smem = 32 * stg_groups(5) * 2 * (int)sizeof(vec2<T>);  // the largest stage (R = 5, 4)
+                e = cudaFuncSetAttribute(lg_f_staged_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                if (!e)
+                    e = launch(lg_f_staged_kernel<T>, dim3(grid), dim3(kStgT), (size_t)smem, st, W0,
+                               (const FTask *)ts.d_tasks, (const int *)ts.d_rs, (const Chunk *)ts.d_chunks,
+                               ts.nchunks, U, batch, Ws, x, S.N);
+            } else {
+                e = launch(lg_f_kernel<T>, dim3(grid), dim3(kChunk), 0, st, W0, (const FTask *)ts.d_tasks,
+                           (const int *)ts.d_dsts, (const int *)ts.d_rs, (const Chunk *)ts.d_chunks, ts.nchunks, U,
+                           batch, Ws, x, S.N);
+            }
             if (e) return (int)e;
         }
     // sub-signal + leaves (one persistent launch)

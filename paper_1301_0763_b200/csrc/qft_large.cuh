@@ -92,6 +92,25 @@ QFT_HD void lg_fold_item(const vec2<T> *x, vec2<T> *w, int n, int N, int log2n) 
 }
 
 // ----------------------------------------------------------------- F pass
+// ld(s, e): the value of slot s (element e of the block) before the first level
+template <int R, typename T, bool DST, class Ld>
+QFT_HD void lg_f_group_ld(vec2<T> *w, const FTask &tk, int t, const T *U, Ld &&ld) {
+    constexpr int G = 1 << R;
+    vec2<T> v[G];
+#pragma unroll
+    for (int s = 0; s < G; ++s) {
+        int c, sg;
+        run_of(R, tk.L, s, c, sg);
+        v[s] = ld(s, c + sg * t);
+    }
+    lee_fwd_rt<R, T, DST>(v, t, tk.L, U);
+#pragma unroll
+    for (int s = 0; s < G; ++s) {  // slot s keeps its cells (in place)
+        int c, sg;
+        run_of(R, tk.L, s, c, sg);
+        w[tk.c + tk.sg * (c + sg * t)] = v[s];
+    }
+}
 template <int R, typename T, bool DST>
 QFT_HD void lg_f_group(vec2<T> *w, const FTask &tk, int t, const T *U, const vec2<T> *x = nullptr, int N = 0) {
     constexpr int G = 1 << R;
@@ -118,8 +137,9 @@ QFT_HD void lg_f_group(vec2<T> *w, const FTask &tk, int t, const T *U, const vec
 // (slots 0..15) and the odd child (slots 16..31); thread h of the pair forms
 // child h of the top fold and runs its four levels -- the same operations on
 // the same operands as lg_f_group<5>.  Both lanes of a pair must be in one warp.
-template <typename T, bool DST>
-QFT_DEV void lg_f_pair5(vec2<T> *w, const FTask &tk, int t, int h, const T *U, const vec2<T> *x, int N) {
+// ld(s, e): the value of slot s (element e of the block) before the first level
+template <typename T, bool DST, class Ld>
+QFT_DEV void lg_f_pair5_ld(vec2<T> *w, const FTask &tk, int t, int h, const T *U, Ld &&ld) {
     constexpr int R = 5, G = 32, H = 16;
     const int L = tk.L;
     auto at = [&](int s) {
@@ -131,8 +151,8 @@ QFT_DEV void lg_f_pair5(vec2<T> *w, const FTask &tk, int t, int h, const T *U, c
 #pragma unroll
     for (int s = 0; s < H; ++s) {
         const int ea = at(s), eb = at(G - 1 - s);
-        const vec2<T> a = tk.j >= 0 ? fold_load<T, DST>(x, N, tk.j, ea) : w[tk.c + tk.sg * ea];
-        const vec2<T> b = tk.j >= 0 ? fold_load<T, DST>(x, N, tk.j, eb) : w[tk.c + tk.sg * eb];
+        const vec2<T> a = ld(s, ea);
+        const vec2<T> b = ld(G - 1 - s, eb);
         int c, sg;
         run_of(R - 1, L / 2, s, c, sg);
         const T k = U[L / 2 + c + sg * t];
@@ -144,6 +164,12 @@ QFT_DEV void lg_f_pair5(vec2<T> *w, const FTask &tk, int t, int h, const T *U, c
     __syncwarp();  // every lane's loads of the run precede the in-place stores
 #pragma unroll
     for (int s = 0; s < H; ++s) w[tk.c + tk.sg * at(h * H + s)] = nv[s];
+}
+template <typename T, bool DST>
+QFT_DEV void lg_f_pair5(vec2<T> *w, const FTask &tk, int t, int h, const T *U, const vec2<T> *x, int N) {
+    lg_f_pair5_ld<T, DST>(w, tk, t, h, U, [&](int, int e) {
+        return tk.j >= 0 ? fold_load<T, DST>(x, N, tk.j, e) : w[tk.c + tk.sg * e];
+    });
 }
 
 #endif  // __CUDACC__
