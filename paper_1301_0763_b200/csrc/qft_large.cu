@@ -322,6 +322,20 @@ QFT_DEV void tma_cells(vec2<double> *dst, const CUtensorMap *map, long long row0
     const int rows = cells / 32;
     for (int r = 0; r < rows; r += kTmaRows) tma_tile_load(dst + 33 * r, map, (int)(row0 + r), bar);
 }
+// the reverse: padded shared-memory rows -> W0 rows (out-of-bounds box columns,
+// i.e. the pad cell of every row, are not written by a tensor store)
+#ifndef QFT_LEAF_TMA_STORE
+#define QFT_LEAF_TMA_STORE 1
+#endif
+QFT_DEV void tma_tile_store(const void *src, const CUtensorMap *map, int row) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(0),
+                 "r"(row), "r"((uint32_t)__cvta_generic_to_shared(src))
+                 : "memory");
+}
+QFT_DEV void tma_cells_store(const vec2<double> *src, const CUtensorMap *map, long long row0, int cells) {
+    const int rows = cells / 32;
+    for (int r = 0; r < rows; r += kTmaRows) tma_tile_store(src + 33 * r, map, (int)(row0 + r));
+}
 QFT_DEV void tma_expect(uint64_t *bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
@@ -559,18 +573,44 @@ QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const
             }
         }
         __syncthreads();
+        // QFT_LEAF_TMA_STORE: the spectrum is written in W0 memory order (a reversed
+        // run's slot e at L-1-e) and leaves by tensor-map TMA stores of the padded rows
+        const bool mo = QFT_LEAF_TMA_STORE && use_tma;
 #pragma unroll
         for (int r = 0; r < IT; ++r) {
             const int it = tid + r * NT;
             if (it < K * 1024) {
                 const int k = it >> 10, i = it & 1023;
-                vec2<T> *o = S + padx(k * L) + padx(i * G);  // G <= 32 slots inside one 32-cell row
+                if (mo && tks[k].sg < 0) {
+                    vec2<T> *o = S + padx(k * L) + padx(L - G - i * G);  // slots i*G+q at L-1-(i*G+q)
 #pragma unroll
-                for (int q = 0; q < G; ++q) o[q] = out[r][q];
+                    for (int q = 0; q < G; ++q) o[G - 1 - q] = out[r][q];
+                } else {
+                    vec2<T> *o = S + padx(k * L) + padx(i * G);  // G <= 32 slots inside one 32-cell row
+#pragma unroll
+                    for (int q = 0; q < G; ++q) o[q] = out[r][q];
+                }
             }
         }
     }
     __syncthreads();
+    if (QFT_LEAF_TMA_STORE && use_tma) {
+        // one thread: the generic-proxy writes of S (published by the barrier) before
+        // the async-proxy reads, the row boxes to W0 (the 2 pad doubles of every
+        // 66-double box row fall outside the tensor and are not written), then wait
+        // until the stores have read S -- the caller's barrier follows
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            for (int k = 0; k < K; ++k) {
+                const LeafTask tk = tks[k];
+                const int lo = tk.sg > 0 ? tk.c : tk.c - (L - 1);
+                tma_cells_store(reinterpret_cast<const vec2<double> *>(S + padx(k * L)), tmap, wrow + lo / 32, L);
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        return;
+    }
     for (int k = 0; k < K; ++k) {
         const LeafTask tk = tks[k];
         const vec2<T> *s = S + padx(k * L);
@@ -728,6 +768,8 @@ __global__ void __launch_bounds__(ItemCfg<SUBLOG, T>::NT, 1)
         }
         __syncthreads();
     }
+    // the leaves' tensor stores (QFT_LEAF_TMA_STORE) complete before the kernel ends
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 template <typename T, int LOG2N, int RC>

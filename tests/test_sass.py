@@ -104,5 +104,10 @@ def test_multipass_fp64_items_use_tensor_map_tma():
     for k in items64:
         ops = [o for o, _, _ in funcs[k]]
         assert any(o.startswith("UTMALDG") for o in ops), f"{k}: no tensor-map TMA load"
+        # the leaves' spectra leave by tensor-map TMA stores of the padded rows (round 2)
+        assert any(o.startswith("UTMASTG") for o in ops), f"{k}: no tensor-map TMA store"
+    # the fp64 F pass stages its first-touch gathers with cp.async (LDGSTS)
+    f64 = [k for k in funcs if "lg_f_staged_kernel" in k]
+    assert f64 and all(any(o.startswith("LDGSTS") for o, _, _ in funcs[k]) for k in f64)
     pipe = [k for k in funcs if "qft_cdft_pipe" in k]
     assert pipe and all(any(o.startswith("UBLKCP") for o, _, _ in funcs[k]) for k in pipe)
