@@ -328,6 +328,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="replay the step as a captured CUDA graph")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     args = ap.parse_args()
     if args.impl == "reference":
@@ -371,6 +372,27 @@ def main():
 
     def step():
         plan.exec_device(x.data_ptr(), y.data_ptr(), B, (N, 1), (N, 1), stream.cuda_stream)
+
+    # --graph (config 1 is launch-latency-bound, "time with CUDA graphs"):
+    # the step -- the same kernel launch on the same buffers -- is captured once into a
+    # CUDA graph and replayed; every replay does the full transform.  Measured no faster
+    # at config 1 (4.69 vs 4.77 M tr/s): the step is bound by the kernel's own latency
+    # (one signal per CTA through every phase), not by the host call.
+    graph = None
+    if args.graph:
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        gs = torch.cuda.Stream(dev)
+        gs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            plan.exec_device(x.data_ptr(), y.data_ptr(), B, (N, 1), (N, 1), gs.cuda_stream)
+        torch.cuda.synchronize()
+
+        def step():  # noqa: F811 -- replay on the timed stream
+            with torch.cuda.stream(stream):
+                graph.replay()
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -478,6 +500,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32" if prec == 32 else "f64", "data": "synthetic",
             "config": {"workload": f"config{args.config}: {cfg['desc']}", "N": N, "batch_per_gpu": B,
+                       "step": "CUDA-graph replay of the step's launch" if graph is not None else "direct launch",
                        "parallelism": f"batch-sharded x{ws}, no collective",
                        "l2": ("input > 126 MB L2 (no flush needed)" if B * N * esz > (126 << 20)
                               else "input fits L2: steps re-read a warm L2 (small config)")},

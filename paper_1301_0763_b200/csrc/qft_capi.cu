@@ -249,12 +249,22 @@ struct DevGuard {
     if (_dg.err != cudaSuccess)                                                          \
         return fail(QFT_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(_dg.err))
 
-// stream-order one call on the plan: wait for the previous call before, mark after
+// stream-order one call on the plan: wait for the previous call before, mark after.
+// While the stream is being captured into a CUDA graph the call is recorded as
+// plain graph nodes (an event recorded outside the capture cannot be waited on
+// inside it): ordering a replayed graph against other streams' calls on the same
+// plan is then the caller's, as for any captured work.
+static bool capturing(cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive;
+}
 static int use_begin(qft_plan *p, cudaStream_t st) {
+    if (capturing(st)) return 0;
     CUDA_TRY(cudaStreamWaitEvent(st, p->ev_use, 0));
     return 0;
 }
 static int use_end(qft_plan *p, cudaStream_t st) {
+    if (capturing(st)) return 0;
     CUDA_TRY(cudaEventRecord(p->ev_use, st));
     return 0;
 }
