@@ -324,6 +324,9 @@ QFT_DEV void tma_cells(vec2<double> *dst, const CUtensorMap *map, long long row0
 }
 // the reverse: padded shared-memory rows -> W0 rows (out-of-bounds box columns,
 // i.e. the pad cell of every row, are not written by a tensor store)
+#ifndef QFT_TB_ROT
+#define QFT_TB_ROT 0  // fp64 leaf TB stores in a lane-rotated slot order: conflict-free (4x fewer wavefronts), measured neutral on config 4
+#endif
 #ifndef QFT_LEAF_TMA_STORE
 #define QFT_LEAF_TMA_STORE 1
 #endif
@@ -581,7 +584,32 @@ QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const
             const int it = tid + r * NT;
             if (it < K * 1024) {
                 const int k = it >> 10, i = it & 1023;
-                if (mo && tks[k].sg < 0) {
+                if (QFT_TB_ROT && sizeof(T) == 8 && (G == 8 || G == 4)) {
+                    // fp64: column i's G cells are 16-byte lanes of one 128-byte row segment;
+                    // stored slot q-th by every lane they hit the same bank group 4 ways
+                    // (ncu: 4x the ideal wavefronts).  Lane i starts its G stores at slot
+                    // rot instead, rot chosen so the 8 lanes of a quarter-warp hit 8
+                    // distinct bank groups (checked exhaustively for every column / layout),
+                    // the register array rotated by a select network to match.
+                    const bool rv = mo && tks[k].sg < 0;
+                    const int ob = padx(k * L) + (rv ? padx(L - G - i * G) : padx(i * G));
+                    const int rot = G == 8 ? ((i - ob) & 7) : (((i >> 1) - ob) & 3);
+                    vec2<T> v[G];
+#pragma unroll
+                    for (int q = 0; q < G; ++q) v[q] = out[r][rv ? G - 1 - q : q];
+#pragma unroll
+                    for (int bsh = 1; bsh < G; bsh <<= 1) {  // v[q] <- v[(q + rot) mod G]
+                        const bool take = rot & bsh;
+                        vec2<T> t[G];
+#pragma unroll
+                        for (int q = 0; q < G; ++q) t[q] = take ? v[(q + bsh) & (G - 1)] : v[q];
+#pragma unroll
+                        for (int q = 0; q < G; ++q) v[q] = t[q];
+                    }
+                    vec2<T> *o = S + ob;
+#pragma unroll
+                    for (int q = 0; q < G; ++q) o[(q + rot) & (G - 1)] = v[q];
+                } else if (mo && tks[k].sg < 0) {
                     vec2<T> *o = S + padx(k * L) + padx(L - G - i * G);  // slots i*G+q at L-1-(i*G+q)
 #pragma unroll
                     for (int q = 0; q < G; ++q) o[G - 1 - q] = out[r][q];
