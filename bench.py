@@ -63,7 +63,8 @@ def read_traffic(config):
     (profiles/r*_summary.json, the newest that has this config), or None."""
     import glob
     best = None
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_summary.json")), key=os.path.getmtime)
+    # newest = last by name (r1 < r1b < r1c < r2m ...): file mtimes do not survive a checkout
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_summary.json")), key=os.path.basename)
     for f in files:
         try:
             with open(f) as fh:
