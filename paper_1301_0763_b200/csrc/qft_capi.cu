@@ -24,6 +24,12 @@
 // classical QFT (qft_classical.cu, one translation unit per precision)
 long long qft_classical_arena_cells_f32(int N);
 long long qft_classical_arena_cells_f64(int N);
+long long qft_classical_lv_arena_bytes_f32(int log2n, long long units);
+long long qft_classical_lv_arena_bytes_f64(int log2n, long long units);
+int qft_classical_lv_exec_f32(int mode, const void *in, void *out, long long units, long long nreal, int log2n,
+                              const void *T, void *arena, size_t arena_bytes, int num_sms, cudaStream_t st);
+int qft_classical_lv_exec_f64(int mode, const void *in, void *out, long long units, long long nreal, int log2n,
+                              const void *T, void *arena, size_t arena_bytes, int num_sms, cudaStream_t st);
 int qft_classical_exec_f32(int mode, const void *in, void *out, long long units, long long nreal, int N, const void *T,
                            void *arena, size_t arena_cells, int warps, cudaStream_t st);
 int qft_classical_exec_f64(int mode, const void *in, void *out, long long units, long long nreal, int N, const void *T,
@@ -364,6 +370,33 @@ static int launch_large(qft_plan *p, int mode, const void *in, void *out, long l
 static int launch_classical(qft_plan *p, int mode, const void *in, void *out, long long units, long long nreal,
                             cudaStream_t st) {
     const bool f32 = p->prec == QFT_PREC_F32;
+    if (p->d_T == nullptr) return fail(QFT_EINVAL, "plan was not created for the classical algorithm");
+    static const bool recursive = [] {  // QFT_CLASSICAL_RECURSIVE=1: the warp-recursive kernel at every N (A/B, tests)
+        const char *v = getenv("QFT_CLASSICAL_RECURSIVE");
+        return v && v[0] == '1';
+    }();
+    if (p->log2n >= 5 && !recursive) {
+        // level-synchronous schedule (qft_classical_lv.cuh): whole tree in shared
+        // memory, or global levels + shared-memory sub-trees with W0/W1 in the arena
+        const size_t need = (size_t)(f32 ? qft_classical_lv_arena_bytes_f32(p->log2n, units)
+                                         : qft_classical_lv_arena_bytes_f64(p->log2n, units));
+        if (p->arena_bytes < need) {
+            if (p->d_arena) {  // grown: earlier calls may still use the old buffer
+                cudaEventSynchronize(p->ev_use);
+                cudaFree(p->d_arena);
+            }
+            p->d_arena = nullptr;
+            p->arena_bytes = 0;
+            CUDA_TRY(cudaMalloc(&p->d_arena, need));
+            p->arena_bytes = need;
+        }
+        int e = f32 ? qft_classical_lv_exec_f32(mode, in, out, units, nreal, p->log2n, p->d_T, p->d_arena,
+                                                need, p->num_sms, st)
+                    : qft_classical_lv_exec_f64(mode, in, out, units, nreal, p->log2n, p->d_T, p->d_arena,
+                                                need, p->num_sms, st);
+        if (e) return fail(QFT_ECUDA, std::string("classical launch: ") + cudaGetErrorString((cudaError_t)e));
+        return 0;
+    }
     const long long cells = f32 ? qft_classical_arena_cells_f32(p->N) : qft_classical_arena_cells_f64(p->N);
     const size_t vb = f32 ? 8 : 16;
     long long warps = units < (long long)p->num_sms * 16 ? units : (long long)p->num_sms * 16;
@@ -382,7 +415,6 @@ static int launch_classical(qft_plan *p, int mode, const void *in, void *out, lo
         CUDA_TRY(cudaMalloc(&p->d_arena, need));
         p->arena_bytes = need;
     }
-    if (p->d_T == nullptr) return fail(QFT_EINVAL, "plan was not created for the classical algorithm");
     // the recursion is ~2 lg N calls deep with ~128-byte frames: raise the
     // per-thread stack once (the default 1 KB overflows from N = 64)
     {

@@ -11,6 +11,9 @@
 // op in the reference's operand order, no FMA (explicit .rn intrinsics).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
+#include "qft_classical_lv.cuh"
 #include "qft_common.cuh"
 
 #if !defined(QFT_CL_PREC)
@@ -346,4 +349,207 @@ int QFT_CL(qft_classical_exec)(int mode, const void *in, void *out, long long un
         default: return (int)cudaErrorInvalidValue;
     }
     return (int)cudaGetLastError();
+}
+
+// ===========================================================================
+// Level-synchronous classical QFT (qft_classical_lv.cuh): N >= 32.
+//   whole-signal kernel   the tree of one signal (or pair of real rows) in two
+//                         shared-memory buffers; one CTA per signal, persistent
+//   large N               the top d0 levels as global passes over W0/W1, the
+//                         sub-trees of periodization 2^sublog in shared memory
+//                         (in place in the global buffer), the d0 backward
+//                         levels as global passes
+// ===========================================================================
+namespace {
+
+constexpr int kLvMaxSmem = 227 * 1024;
+
+QFT_HD int lv_smem_bytes(int lognn) { return 2 * cl::buf_cells(lognn) * (int)sizeof(V); }
+
+// forward levels, register-level bases and backward levels of one tree held in P0 / P1
+__device__ __forceinline__ void lv_run_tree(const cl::Tree<Real> &t, V *P0, V *P1, int tid, int NT) {
+    const int D = t.depth();
+    V *cen = P0 + cl::cen_off(t.lognn);
+    for (int d = 0; d < D; ++d) {
+        const V *s = (d & 1) ? P1 : P0;
+        V *o = (d & 1) ? P0 : P1;
+        for (int it = tid; it < t.fwd_items(); it += NT) t.fwd_item(s, o, cen, d, it);
+        __syncthreads();
+    }
+    {
+        V *b = (D & 1) ? P1 : P0;
+        for (int it = tid; it < t.base_items(); it += NT) t.base_item(b, it);
+        __syncthreads();
+    }
+    for (int d = D - 1; d >= 0; --d) {
+        const V *chi = ((d + 1) & 1) ? P1 : P0;
+        V *o = (d & 1) ? P1 : P0;
+        for (int it = tid; it < t.bwd_items(); it += NT) t.bwd_item(chi, o, cen, d, it);
+        __syncthreads();
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(512) cl_tree_kernel(const void *in, void *out, long long units, long long nreal,
+                                                      int log2n, const Real *__restrict__ Tt) {
+    extern __shared__ __align__(16) unsigned char cl_smem[];
+    V *P0 = reinterpret_cast<V *>(cl_smem), *P1 = P0 + cl::buf_cells(log2n);
+    const cl::Tree<Real> t{log2n, log2n, cl::cos_cells(log2n), false, MODE != 3, MODE != 2, Tt};
+    const int N = 1 << log2n, m = N / 2, tid = threadIdx.x, NT = blockDim.x;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+        for (int n = tid; n < m; n += NT) cl::ingest_item<MODE, Real>(in, u, nreal, N, P0, t.CB, n);
+        __syncthreads();
+        lv_run_tree(t, P0, P1, tid, NT);
+        for (int k = tid; k <= m; k += NT) cl::emit_item<MODE, Real>(out, u, nreal, N, P0, t.CB, k);
+        __syncthreads();
+    }
+}
+
+// large N: fold (ingest) of every signal into the roots of W0
+template <int MODE>
+__global__ void __launch_bounds__(256) cl_gingest_kernel(const void *in, V *W0, long long Ws, long long units,
+                                                         long long nreal, int log2n) {
+    const int N = 1 << log2n, m = N / 2, CB = cl::cos_cells(log2n);
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= m) return;
+    for (long long u = blockIdx.y; u < units; u += gridDim.y)
+        cl::ingest_item<MODE, Real>(in, u, nreal, N, W0 + u * Ws, CB, n);
+}
+template <int MODE>
+__global__ void __launch_bounds__(256) cl_gemit_kernel(void *out, const V *W0, long long Ws, long long units,
+                                                       long long nreal, int log2n) {
+    const int N = 1 << log2n, m = N / 2, CB = cl::cos_cells(log2n);
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k > m) return;
+    for (long long u = blockIdx.y; u < units; u += gridDim.y)
+        cl::emit_item<MODE, Real>(out, u, nreal, N, W0 + u * Ws, CB, k);
+}
+// one global forward (BWD = false: src = level d, dst = level d+1) or backward
+// (BWD = true: src = level d+1 spectra, dst = level d) level of every signal
+template <bool BWD>
+__global__ void __launch_bounds__(256) cl_glevel_kernel(const V *src, V *dst, V *W0, long long Ws, long long units, int log2n,
+                                                        int d, bool do_cos, bool do_sin,
+                                                        const Real *__restrict__ Tt) {
+    const cl::Tree<Real> t{log2n, log2n, cl::cos_cells(log2n), false, do_cos, do_sin, Tt};
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= (BWD ? t.bwd_items() : t.fwd_items())) return;
+    for (long long u = blockIdx.y; u < units; u += gridDim.y) {
+        V *cen = W0 + u * Ws + cl::cen_off(log2n);  // the centres live in buffer 0
+        if (BWD) t.bwd_item(src + u * Ws, dst + u * Ws, cen, d, it);
+        else t.fwd_item(src + u * Ws, dst + u * Ws, cen, d, it);
+    }
+}
+// the sub-trees rooted at depth d0 (periodization 2^(log2n - d0)), in place in Wd
+__global__ void __launch_bounds__(512) cl_subtree_kernel(V *Wd, long long Ws, long long units, int log2n, int d0,
+                                                         bool do_cos, bool do_sin, const Real *__restrict__ Tt) {
+    extern __shared__ __align__(16) unsigned char cl_smem[];
+    const int sublog = log2n - d0, S0 = 1 << (sublog - 1), CBtop = cl::cos_cells(log2n);
+    V *P0 = reinterpret_cast<V *>(cl_smem), *P1 = P0 + cl::buf_cells(sublog);
+    const int tid = threadIdx.x, NT = blockDim.x;
+    for (long long g = blockIdx.x; g < (units << d0); g += gridDim.x) {
+        const long long u = g >> d0;
+        const int b = (int)(g & ((1LL << d0) - 1));
+        const cl::Tree<Real> t{sublog, log2n, cl::cos_cells(sublog), (b & 1) != 0, do_cos, do_sin, Tt};
+        V *wc = Wd + u * Ws + cl::cos_off(S0, b), *ws = Wd + u * Ws + CBtop + (long long)b * S0;
+        const int nc = S0 + ((b & 1) ? 0 : 1);
+        if (do_cos)
+            for (int i = tid; i < nc; i += NT) P0[i] = wc[i];
+        if (do_sin)
+            for (int i = tid; i < S0 - 1; i += NT) P0[t.CB + i] = ws[i];
+        __syncthreads();
+        lv_run_tree(t, P0, P1, tid, NT);
+        if (do_cos)
+            for (int i = tid; i < nc; i += NT) wc[i] = P0[i];
+        if (do_sin)
+            for (int i = tid; i < S0 - 1; i += NT) ws[i] = P0[t.CB + i];
+        __syncthreads();
+    }
+}
+
+template <int MODE>
+cudaError_t lv_launch_mode(const void *in, void *out, long long units, long long nreal, int log2n, const Real *Tt,
+                           V *arena, size_t arena_bytes, int num_sms, cudaStream_t st) {
+    const int smem = lv_smem_bytes(log2n);
+    if (smem <= kLvMaxSmem) {
+        auto kern = cl_tree_kernel<MODE>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        const int per_sm = kLvMaxSmem / (smem + 1024) > 0 ? kLvMaxSmem / (smem + 1024) : 1;
+        const int NT = per_sm >= 3 ? 256 : 512;
+        long long grid = (long long)num_sms * (per_sm > 4 ? 4 : per_sm);
+        if (grid > units) grid = units;
+        if (grid < 1) grid = 1;
+        kern<<<(unsigned)grid, NT, smem, st>>>(in, out, units, nreal, log2n, Tt);
+        return cudaGetLastError();
+    }
+    // large N: global levels down to sub-trees of 2^sublog
+    const int sublog = sizeof(Real) == 4 ? 12 : 11, d0 = log2n - sublog;
+    const long long Ws = cl::buf_cells(log2n);
+    const int N = 1 << log2n, m = N / 2;
+    const bool do_cos = MODE != 3, do_sin = MODE != 2;
+    long long chunk = (long long)(arena_bytes / (2 * (size_t)Ws * sizeof(V)));
+    if (chunk < 1) return cudaErrorMemoryAllocation;
+    const int ssm = lv_smem_bytes(sublog);
+    cudaError_t e = cudaFuncSetAttribute(cl_subtree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm);
+    if (e != cudaSuccess) return e;
+    const size_t in_row = MODE == 0 ? (size_t)N * sizeof(V) : 2 * (size_t)(MODE == 1 ? N : (MODE == 2 ? m + 1 : m - 1)) * sizeof(Real);
+    const size_t out_row = MODE == 0 ? (size_t)N * sizeof(V) : (MODE == 1 ? 2 * (size_t)(m + 1) * sizeof(V) : 2 * (size_t)(MODE == 2 ? m + 1 : m - 1) * sizeof(Real));
+    for (long long u0 = 0; u0 < units; u0 += chunk) {
+        const long long nu = units - u0 < chunk ? units - u0 : chunk;
+        V *W[2] = {arena, arena + nu * Ws};
+        const unsigned gy = (unsigned)(nu < 65535 ? nu : 65535);
+        const char *cin = (const char *)in + (size_t)u0 * in_row;
+        char *cout = (char *)out + (size_t)u0 * out_row;
+        const long long nr = nreal - 2 * u0;  // real rows left (real modes)
+        cl_gingest_kernel<MODE><<<dim3((m + 255) / 256, gy), 256, 0, st>>>(cin, W[0], Ws, nu, nr, log2n);
+        for (int d = 0; d < d0; ++d)
+            cl_glevel_kernel<false><<<dim3(((N / 4) + 255) / 256, gy), 256, 0, st>>>(W[d & 1], W[(d + 1) & 1], W[0], Ws, nu,
+                                                                                   log2n, d, do_cos, do_sin, Tt);
+        {
+            long long grid = (long long)num_sms * (kLvMaxSmem / (ssm + 1024));
+            if (grid > (nu << d0)) grid = nu << d0;
+            cl_subtree_kernel<<<(unsigned)grid, 256, ssm, st>>>(W[d0 & 1], Ws, nu, log2n, d0, do_cos, do_sin, Tt);
+        }
+        for (int d = d0 - 1; d >= 0; --d)
+            cl_glevel_kernel<true><<<dim3(((N / 2) + 255) / 256, gy), 256, 0, st>>>(W[(d + 1) & 1], W[d & 1], W[0], Ws, nu,
+                                                                                  log2n, d, do_cos, do_sin, Tt);
+        cl_gemit_kernel<MODE><<<dim3((m + 1 + 255) / 256, gy), 256, 0, st>>>(cout, W[0], Ws, nu, nr, log2n);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace
+
+// bytes of global scratch the level-synchronous path wants for `units` signals
+// (0: the whole tree fits shared memory); any amount >= one signal's works (chunked)
+long long QFT_CL(qft_classical_lv_arena_bytes)(int log2n, long long units) {
+    if (log2n < cl::kBaseLog || lv_smem_bytes(log2n) <= kLvMaxSmem) return 0;
+    const long long per = 2 * (long long)cl::buf_cells(log2n) * (long long)sizeof(V);
+    // QFT_CL_ARENA_MB: scratch budget (tests use a small one to exercise the chunking)
+    long long budget = 4LL << 30;
+    if (const char *v = getenv("QFT_CL_ARENA_MB")) {
+        const long long mb = atoll(v);
+        if (mb > 0) budget = mb << 20;
+    }
+    const long long cap = budget / per > 0 ? budget / per : 1;
+    return per * (units < cap ? units : cap);
+}
+
+// mode 0: complex rows; 1/2/3: rdft / dct0 / dst0 on real row pairs.  N >= 32.
+int QFT_CL(qft_classical_lv_exec)(int mode, const void *in, void *out, long long units, long long nreal, int log2n,
+                                  const void *T, void *arena, size_t arena_bytes, int num_sms, cudaStream_t st) {
+    if (log2n < cl::kBaseLog) return (int)cudaErrorInvalidValue;
+    const Real *t = (const Real *)T;
+    V *ar = (V *)arena;
+    cudaError_t e;
+    switch (mode) {
+        case 0: e = lv_launch_mode<0>(in, out, units, nreal, log2n, t, ar, arena_bytes, num_sms, st); break;
+        case 1: e = lv_launch_mode<1>(in, out, units, nreal, log2n, t, ar, arena_bytes, num_sms, st); break;
+        case 2: e = lv_launch_mode<2>(in, out, units, nreal, log2n, t, ar, arena_bytes, num_sms, st); break;
+        case 3: e = lv_launch_mode<3>(in, out, units, nreal, log2n, t, ar, arena_bytes, num_sms, st); break;
+        default: return (int)cudaErrorInvalidValue;
+    }
+    return (int)e;
 }

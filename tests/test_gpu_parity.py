@@ -401,3 +401,46 @@ def test_cuda_graph_capture_replay(torch_cuda, oracle_mod, lg, dt):
         g.replay()
         torch.cuda.synchronize()
         assert bit_equal(y.cpu().numpy(), oracle_mod.cdft_rows(z))
+
+
+@pytest.mark.parametrize("dt,lg,B", [(np.complex64, 12, 16384), (np.complex64, 10, 1000), (np.complex128, 12, 700),
+                                     (np.complex64, 13, 300), (np.complex128, 13, 40), (np.complex64, 14, 150),
+                                     (np.complex64, 5, 333), (np.complex128, 6, 149), (np.complex64, 17, 5)])
+def test_classical_level_schedule_full_batches(torch_cuda, dt, lg, B):
+    """The level-synchronous classical kernels (qft_classical_lv.cuh): every row of
+    whole batches -- more signals than resident CTAs, a ragged last wave, the
+    whole-tree kernel (fp32 <= 2^13, fp64 <= 2^12) and the global-level + sub-tree
+    schedule above -- bit-identical to the oracle's classical.py restatement."""
+    torch = torch_cuda
+    from oracle import parity
+    from paper_1301_0763_b200 import classical
+    N = 1 << lg
+    rt = torch.float32 if dt == np.complex64 else torch.float64
+    g = torch.Generator(device="cuda").manual_seed(lg * 1000 + B)
+    x = torch.view_as_complex(torch.randn((B, N, 2), dtype=rt, device="cuda", generator=g))
+    y = classical.cdft_rows(x)
+    torch.cuda.synchronize()
+    rep = parity.check_rows(x, y, algo="classical")
+    assert rep["rows_checked"] == B and rep["mismatches"] == 0, rep
+
+
+def test_classical_large_schedule_chunked_scratch(torch_cuda, oracle_mod, monkeypatch):
+    """A scratch budget smaller than the batch's W0/W1 (QFT_CL_ARENA_MB): the large-N
+    schedule runs the batch in chunks, complex and real entry points alike."""
+    from paper_1301_0763_b200 import classical
+    monkeypatch.setenv("QFT_CL_ARENA_MB", "3")   # 2^15 fp32: ~0.5 MB per signal -> 5 signals per chunk
+    N = 1 << 15
+    rng = np.random.default_rng(77)
+    z = (rng.standard_normal((N, 13)) + 1j * rng.standard_normal((N, 13))).astype(np.complex64)
+    assert bit_equal(classical.cdft(z), oracle_mod.cdft(z, algo="classical"))
+    for kind, n_vals in (("rdft", N), ("dct0", N // 2 + 1), ("dst0", N // 2 - 1)):
+        x = rng.standard_normal((n_vals, 27)).astype(np.float32)
+        assert bit_equal(getattr(classical, kind)(x), getattr(oracle_mod, kind)(x, algo="classical")), kind
+
+
+def test_classical_recursive_kernel_still_matches(torch_cuda, oracle_mod):
+    """N < 32 is served by the warp-recursive kernel (qft_classical.cu, first half)."""
+    from paper_1301_0763_b200 import classical
+    for lg in (1, 2, 3, 4):
+        z = (np.random.default_rng(lg).standard_normal((1 << lg, 70)) + 0j).astype(np.complex128)
+        assert bit_equal(classical.cdft(z), oracle_mod.cdft(z, algo="classical"))
