@@ -389,9 +389,11 @@ __device__ __forceinline__ void lv_run_tree(const cl::Tree<Real> &t, V *P0, V *P
     }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(512) cl_tree_kernel(const void *in, void *out, long long units, long long nreal,
-                                                      int log2n, const Real *__restrict__ Tt) {
+// MINB: resident CTAs per SM the register budget is set for (1: 512 threads, else 256)
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(MINB == 1 ? 512 : 256, MINB)
+    cl_tree_kernel(const void *in, void *out, long long units, long long nreal, int log2n,
+                   const Real *__restrict__ Tt) {
     extern __shared__ __align__(16) unsigned char cl_smem[];
     V *P0 = reinterpret_cast<V *>(cl_smem), *P1 = P0 + cl::buf_cells(log2n);
     const cl::Tree<Real> t{log2n, log2n, cl::cos_cells(log2n), false, MODE != 3, MODE != 2, Tt};
@@ -403,6 +405,24 @@ __global__ void __launch_bounds__(512) cl_tree_kernel(const void *in, void *out,
         for (int k = tid; k <= m; k += NT) cl::emit_item<MODE, Real>(out, u, nreal, N, P0, t.CB, k);
         __syncthreads();
     }
+}
+
+template <int MODE, int MINB>
+cudaError_t lv_launch_tree(const void *in, void *out, long long units, long long nreal, int log2n, const Real *Tt,
+                           int smem, int num_sms, cudaStream_t st) {
+    auto kern = cl_tree_kernel<MODE, MINB>;
+    constexpr int NT = MINB == 1 ? 512 : 256;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;  // what the registers and the shared memory really allow
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    long long grid = (long long)num_sms * per_sm;
+    if (grid > units) grid = units;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, NT, smem, st>>>(in, out, units, nreal, log2n, Tt);
+    return cudaGetLastError();
 }
 
 // large N: fold (ingest) of every signal into the roots of W0
@@ -440,7 +460,7 @@ __global__ void __launch_bounds__(256) cl_glevel_kernel(const V *src, V *dst, V 
     }
 }
 // the sub-trees rooted at depth d0 (periodization 2^(log2n - d0)), in place in Wd
-__global__ void __launch_bounds__(512) cl_subtree_kernel(V *Wd, long long Ws, long long units, int log2n, int d0,
+__global__ void __launch_bounds__(256, 3) cl_subtree_kernel(V *Wd, long long Ws, long long units, int log2n, int d0,
                                                          bool do_cos, bool do_sin, const Real *__restrict__ Tt) {
     extern __shared__ __align__(16) unsigned char cl_smem[];
     const int sublog = log2n - d0, S0 = 1 << (sublog - 1), CBtop = cl::cos_cells(log2n);
@@ -450,7 +470,7 @@ __global__ void __launch_bounds__(512) cl_subtree_kernel(V *Wd, long long Ws, lo
         const long long u = g >> d0;
         const int b = (int)(g & ((1LL << d0) - 1));
         const cl::Tree<Real> t{sublog, log2n, cl::cos_cells(sublog), (b & 1) != 0, do_cos, do_sin, Tt};
-        V *wc = Wd + u * Ws + cl::cos_off(S0, b), *ws = Wd + u * Ws + CBtop + (long long)b * S0;
+        V *wc = Wd + u * Ws + cl::cos_off(S0, b), *ws = Wd + u * Ws + CBtop + (long long)b * cl::sin_stride_of(log2n, d0);
         const int nc = S0 + ((b & 1) ? 0 : 1);
         if (do_cos)
             for (int i = tid; i < nc; i += NT) P0[i] = wc[i];
@@ -471,16 +491,18 @@ cudaError_t lv_launch_mode(const void *in, void *out, long long units, long long
                            V *arena, size_t arena_bytes, int num_sms, cudaStream_t st) {
     const int smem = lv_smem_bytes(log2n);
     if (smem <= kLvMaxSmem) {
-        auto kern = cl_tree_kernel<MODE>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        const int per_sm = kLvMaxSmem / (smem + 1024) > 0 ? kLvMaxSmem / (smem + 1024) : 1;
-        const int NT = per_sm >= 3 ? 256 : 512;
-        long long grid = (long long)num_sms * (per_sm > 4 ? 4 : per_sm);
-        if (grid > units) grid = units;
-        if (grid < 1) grid = 1;
-        kern<<<(unsigned)grid, NT, smem, st>>>(in, out, units, nreal, log2n, Tt);
-        return cudaGetLastError();
+        static const int minb_env = [] {  // QFT_CL_MINB=1|2|3: force the register budget (A/B)
+            const char *v = getenv("QFT_CL_MINB");
+            return v ? atoi(v) : 0;
+        }();
+        const int fit = kLvMaxSmem / (smem + 1024);
+        int minb = fit >= 3 ? 3 : (fit >= 2 ? 2 : 1);
+        if (minb_env >= 1 && minb_env <= 3 && minb_env <= (fit > 1 ? fit : 1)) minb = minb_env;
+        switch (minb) {
+            case 1: return lv_launch_tree<MODE, 1>(in, out, units, nreal, log2n, Tt, smem, num_sms, st);
+            case 2: return lv_launch_tree<MODE, 2>(in, out, units, nreal, log2n, Tt, smem, num_sms, st);
+            default: return lv_launch_tree<MODE, 3>(in, out, units, nreal, log2n, Tt, smem, num_sms, st);
+        }
     }
     // large N: global levels down to sub-trees of 2^sublog
     const int sublog = sizeof(Real) == 4 ? 12 : 11, d0 = log2n - sublog;
@@ -506,12 +528,15 @@ cudaError_t lv_launch_mode(const void *in, void *out, long long units, long long
             cl_glevel_kernel<false><<<dim3(((N / 4) + 255) / 256, gy), 256, 0, st>>>(W[d & 1], W[(d + 1) & 1], W[0], Ws, nu,
                                                                                    log2n, d, do_cos, do_sin, Tt);
         {
-            long long grid = (long long)num_sms * (kLvMaxSmem / (ssm + 1024));
+            int per_sm = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cl_subtree_kernel, 256, ssm);
+            if (e != cudaSuccess) return e;
+            long long grid = (long long)num_sms * (per_sm > 0 ? per_sm : 1);
             if (grid > (nu << d0)) grid = nu << d0;
             cl_subtree_kernel<<<(unsigned)grid, 256, ssm, st>>>(W[d0 & 1], Ws, nu, log2n, d0, do_cos, do_sin, Tt);
         }
         for (int d = d0 - 1; d >= 0; --d)
-            cl_glevel_kernel<true><<<dim3(((N / 2) + 255) / 256, gy), 256, 0, st>>>(W[(d + 1) & 1], W[d & 1], W[0], Ws, nu,
+            cl_glevel_kernel<true><<<dim3(((N / 4) + 255) / 256, gy), 256, 0, st>>>(W[(d + 1) & 1], W[d & 1], W[0], Ws, nu,
                                                                                   log2n, d, do_cos, do_sin, Tt);
         cl_gemit_kernel<MODE><<<dim3((m + 1 + 255) / 256, gy), 256, 0, st>>>(cout, W[0], Ws, nu, nr, log2n);
         e = cudaGetLastError();

@@ -25,7 +25,8 @@
 //
 // Layout of depth d of one (sub-)tree in a buffer: cosine node b at
 // cos_off(S, b) = b S + ceil(b/2) (the D nodes carry the one extra cell of the
-// dc_t1t growth, tree.py:92-102), sine node b at CB + b S.  Depth d lives in
+// dc_t1t growth, tree.py:92-102), sine node b at CB + b S (S + 1 at the base
+// depth).  Depth d lives in
 // buffer d & 1; a node's spectrum replaces its input cells.  Nodes of
 // periodization 32 (S = 16) are finished by one thread each in registers with the
 // reference recursion instantiated at compile time (dct_r / dct_odd_r / dst_r /
@@ -48,8 +49,13 @@ QFT_HD int cos_cells(int lognn) {
     return (1 << (lognn - 1)) + (D >= 1 ? (1 << (D - 1)) : 1) + 1;
 }
 // cells of one buffer: cosine area, sine area, centres (used in buffer 0 only)
-QFT_HD int cen_off(int lognn) { return cos_cells(lognn) + (1 << (lognn - 1)); }
+// (the sine area holds one pad cell per base node, Tree::sin_stride)
+QFT_HD int cen_off(int lognn) { return cos_cells(lognn) + (1 << (lognn - 1)) + (1 << (lognn > kBaseLog ? lognn - kBaseLog : 0)); }
 QFT_HD int buf_cells(int lognn) { return cen_off(lognn) + (1 << (base_depth(lognn) > 0 ? base_depth(lognn) : 0)); }
+
+// stride of the sine nodes of depth d of a tree of periodization 2^lognn: S, plus
+// one pad cell at the base depth (Tree::sin_stride)
+QFT_HD int sin_stride_of(int lognn, int d) { return (1 << (lognn - 1 - d)) + (d == base_depth(lognn) ? 1 : 0); }
 
 // half-secant 1/(2cos(2 pi n / 2^lognode)) from the natural table of the top
 // periodization 2^logtop (counting.py:152-158: a constant depends only on the
@@ -218,7 +224,8 @@ struct Tree {
         }
         if (do_sin) {  // elaborations.py:117-122 + classical.py:118-119
             const vec2<T> *x = src + CB + b * S;
-            vec2<T> *ev = dst + CB + (2 * b) * q, *oc = dst + CB + (2 * b + 1) * q;
+            const int cs = sin_stride(d + 1);
+            vec2<T> *ev = dst + CB + (2 * b) * cs, *oc = dst + CB + (2 * b + 1) * cs;
             if (i < q - 1) {
                 const int sh = logtop - (lognn - d);  // node periodization 2S
                 const vec2<T> a = x[i], c = x[S - 2 - i];
@@ -230,32 +237,35 @@ struct Tree {
         }
     }
 
-    // backward level d+1 -> d, item in [0, Nn/2): (node b, harmonic slot k < S)
+    // stride of the sine nodes of depth d: S, except at the base depth, where one
+    // pad cell per node makes the per-thread base accesses (thread = node) bank-conflict free
+    QFT_HD int sin_stride(int d) const { return sin_stride_of(lognn, d); }
+
+    // backward level d+1 -> d, item in [0, Nn/4): (node b, slot pair 2i, 2i+1 with i < q)
     QFT_HD void bwd_item(const vec2<T> *chi, vec2<T> *dst, const vec2<T> *cen, int d, int item) const {
-        const int ls = lognn - 1 - d, S = 1 << ls, q = S >> 1;
-        const int b = item >> ls, k = item & (S - 1);
+        const int lq = lognn - 2 - d, q = 1 << lq, S = 2 * q;
+        const int b = item >> lq, i = item & (q - 1);
         if (do_cos) {
             const vec2<T> *se = chi + cos_off(q, 2 * b), *so = chi + cos_off(q, 2 * b + 1);
-            vec2<T> *out = dst + cos_off(S, b);
-            auto half = [&](int j) { return (j & 1) ? so[j >> 1] : se[j >> 1]; };
-            if (!odd_type(d, b)) {  // elaborations.py:137-140
-                out[k] = half(k);
-                if (k == 0) out[S] = se[q];
-            } else {  // classical.py:98-99
-                out[k] = vadd(half(k), half(k + 1));
+            vec2<T> *out = dst + cos_off(S, b) + 2 * i;
+            const vec2<T> e0 = se[i], o0 = so[i];
+            if (!odd_type(d, b)) {  // interleave (elaborations.py:137-140)
+                out[0] = e0;
+                out[1] = o0;
+                if (i == 0) out[S] = se[q];
+            } else {  // neighbour sums of the interleave (classical.py:98-99)
+                out[0] = vadd(e0, o0);
+                out[1] = vadd(o0, se[i + 1]);
             }
         }
-        if (do_sin && k < S - 1) {  // classical.py:120-128, elaborations.py:145-148
-            const vec2<T> *se = chi + CB + (2 * b) * q, *sp = chi + CB + (2 * b + 1) * q;
-            vec2<T> *out = dst + CB + b * S;
-            if (k & 1) {
-                out[k] = se[k >> 1];
-            } else {
-                const int i = k >> 1;
-                const vec2<T> center = cen[(1 << d) + b];
-                const vec2<T> partial = i == 0 ? sp[0] : (i == q - 1 ? sp[q - 2] : vadd(sp[i - 1], sp[i]));
-                out[k] = (i & 1) ? vsub(partial, center) : vadd(partial, center);
-            }
+        if (do_sin) {  // classical.py:120-128, elaborations.py:145-148
+            const int cs = sin_stride(d + 1);
+            const vec2<T> *se = chi + CB + (2 * b) * cs, *sp = chi + CB + (2 * b + 1) * cs;
+            vec2<T> *out = dst + CB + b * S + 2 * i;
+            const vec2<T> center = cen[(1 << d) + b];
+            const vec2<T> partial = i == 0 ? sp[0] : (i == q - 1 ? sp[q - 2] : vadd(sp[i - 1], sp[i]));
+            out[0] = (i & 1) ? vsub(partial, center) : vadd(partial, center);
+            if (i < q - 1) out[1] = se[i];
         }
     }
 
@@ -286,7 +296,7 @@ struct Tree {
             }
         } else {
             if (!do_sin) return;
-            vec2<T> *x = buf + CB + (item - nn) * SB;
+            vec2<T> *x = buf + CB + (item - nn) * (D ? SB + 1 : SB);
             vec2<T> v[SB - 1], o[SB - 1];
 #pragma unroll
             for (int e = 0; e < SB - 1; ++e) v[e] = x[e];
@@ -296,7 +306,7 @@ struct Tree {
         }
     }
     QFT_HD int fwd_items() const { return 1 << (lognn - 2); }
-    QFT_HD int bwd_items() const { return 1 << (lognn - 1); }
+    QFT_HD int bwd_items() const { return 1 << (lognn - 2); }
     QFT_HD int base_items() const { return 2 << depth(); }
 };
 

@@ -45,7 +45,7 @@ int run_mode(int lg, int sublog, const void *in, void *out, long units, long nre
             std::vector<vec2<T>> P0(cl::buf_cells(sublog)), P1(cl::buf_cells(sublog));
             for (int b = 0; b < (1 << d0); ++b) {
                 const cl::Tree<T> t{sublog, lg, cl::cos_cells(sublog), (b & 1) != 0, do_cos, do_sin, Tt};
-                vec2<T> *wc = W[d0 & 1] + cl::cos_off(S0, b), *ws = W[d0 & 1] + CB + b * S0;
+                vec2<T> *wc = W[d0 & 1] + cl::cos_off(S0, b), *ws = W[d0 & 1] + CB + b * cl::sin_stride_of(lg, d0);
                 const int nc = S0 + ((b & 1) ? 0 : 1);
                 std::memset(P0.data(), 0x7f, sizeof(vec2<T>) * P0.size());
                 std::memset(P1.data(), 0x7f, sizeof(vec2<T>) * P1.size());
