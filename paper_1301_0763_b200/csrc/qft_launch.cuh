@@ -573,6 +573,74 @@ QFT_DEV void fused_units(vec2<T> *W, const T *U, const T *kcu, int ntr, int warp
     }
 }
 
+// ---- phased units (N <= 2048): below 1024-cell blocks a fused warp unit leaves
+// most lanes idle in its Lee-32 step (block 0 of N = 1024 has 8 sub-blocks: 8 of
+// 32 lanes; N = 128 has one chunk per side), and that step is most of the
+// unit's instructions.  Here the three steps are CTA phases instead: F by warp
+// units, then the Lee-32 chunks (and the L <= 16 blocks) of ALL signals of the
+// iteration flat over the CTA's threads (the chunks of a side are the cells
+// [32k, 32k+32), k < NL32, after the sub-block-major F stores), then C by warp
+// units.  Same per-cell operations, two more CTA barriers per iteration.
+#ifndef QFT_PHASED
+#define QFT_PHASED 1
+#endif
+template <int LOG2N>
+constexpr bool use_phased() {
+    return QFT_PHASED && QFT_SC && LOG2N <= 11;
+}
+template <int LOG2N, typename T, int MODE, int TT, int NW>
+QFT_DEV void phased_units(vec2<T> *W, const T *U, const T *kcu, int ntr, int tid) {
+    using P = SPlan<LOG2N>;
+    constexpr int NU = 2 * (P::NU1 + 1), NT = NW * 32, NL = P::NL32;
+    constexpr bool DOC = MODE != 3, DOS = MODE != 2;
+    const int warp = tid >> 5, lane = tid & 31;
+    auto side = [&](int tau, bool dst) { return W + tau * P::PADDED + (dst ? padx(P::S0) : 0); };
+    if constexpr (P::JF >= 1) {
+        for (int u = warp; u < TT * NU; u += NW) {
+            const int tau = u / NU, kind = u - tau * NU;
+            const bool dst = kind & 1;
+            if (tau >= ntr || (dst ? !DOS : !DOC)) continue;
+            vec2<T> *ws = side(tau, dst);
+            if ((kind >> 1) < P::NU1) {
+                FBlockP<P::LB, P::RB, false, T> f;
+                f.load(ws, U, lane);
+                __syncwarp();
+                f.store(ws, lane);
+            } else {
+                run_f_blocks<LOG2N, T, P::JR>(ws, U, false, lane);
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+    if constexpr (NL > 0) {
+        for (int it = tid; it < TT * 2 * NL; it += NT) {
+            const int tau = it / (2 * NL), r = it - tau * (2 * NL);
+            const bool dst = r >= NL;
+            if (tau >= ntr || (dst ? !DOS : !DOC)) continue;
+            b_l32<false, T>(side(tau, dst), 32 * (r - (dst ? NL : 0)), kcu, dst);
+        }
+    }
+    // the L <= 16 blocks of every side, on the threads with the fewest chunks (the last ones)
+    for (int it = NT - 1 - tid; it < TT * 2; it += NT) {
+        const int tau = it >> 1;
+        const bool dst = it & 1;
+        if (tau >= ntr || (dst ? !DOS : !DOC)) continue;
+        b_small<LOG2N, false, T>(side(tau, dst), kcu, dst);
+    }
+    if constexpr (P::JF >= 1) {
+        __syncthreads();
+        for (int u = warp; u < TT * NU; u += NW) {
+            const int tau = u / NU, kind = u - tau * NU;
+            const bool dst = kind & 1;
+            if (tau >= ntr || (dst ? !DOS : !DOC)) continue;
+            vec2<T> *ws = side(tau, dst);
+            if ((kind >> 1) < P::NU1) run_c_blockp<P::RB, false, T>(ws, lane);
+            else run_c_blocks<LOG2N, T, P::JR>(ws, false, lane);
+        }
+    }
+}
+
 // A0 of TT complex signals from src (staging buffer or global memory): chunks
 // of 64 consecutive n per warp, UNR chunks in flight; then the multiples of 64.
 // first: chunks [0, first) of a single signal (TTn == 1) were loaded ahead (QFT_A0_PRE)
@@ -710,7 +778,8 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
         // TF: top forward levels of the huge blocks (N > 4096; ends with a barrier)
         if constexpr (P::JH > 0) top_f<LOG2N, T, MODE>(W, U, ntr, tid);
         // A+B+C fused: one warp per (signal, side, unit) -- no CTA barrier inside
-        fused_units<LOG2N, T, MODE, TT, NW>(W, U, kc.u, ntr, warp, lane);
+        if constexpr (use_phased<LOG2N>()) phased_units<LOG2N, T, MODE, TT, NW>(W, U, kc.u, ntr, tid);
+        else fused_units<LOG2N, T, MODE, TT, NW>(W, U, kc.u, ntr, warp, lane);
         QFT_WMARK();
         __syncthreads();
         QFT_MARK(3);
