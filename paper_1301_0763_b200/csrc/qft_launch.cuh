@@ -157,17 +157,49 @@ QFT_DEV void l2_prefetch(const void *src, uint32_t bytes) {
 }
 
 // ------------------------------------------------------------ configuration
+#ifndef QFT_CPS_SMALL
+// CTAs resident per SM for N <= 2048 (0: the measured per-size choice below).  The
+// phases of a small transform are short and separated by CTA barriers (ncu:
+// barrier was 36 % of the stall samples at N = 1024 with one CTA per SM); more
+// resident CTAs fill them.  Measured 1 / 2 / 3 CTAs (tools/size_sweep.py, % of HBM):
+// fp32 2^10 48.8 / 52.8 / 56.6, 2^11 50.3 / 52.4 / 50.0, 2^7 44.7 / 32.1 / 32.8;
+// fp64 2^9 48.4 / 53.7 / 54.1, 2^11 49.8 / 45.6 / 51.9
+#define QFT_CPS_SMALL 0
+#endif
+// the sizes whose working area is 67 KB (fp32 N = 8192, fp64 N = 4096): one signal
+// per CTA iteration (QFT_TT_MID) and QFT_CPS_MID resident CTAs
+#ifndef QFT_TT_MID
+#define QFT_TT_MID 1
+#endif
+#ifndef QFT_CPS_MID
+#define QFT_CPS_MID 2  // measured (TT, CTAs) = (3, 1) / (1, 1) / (1, 2): fp32 2^13 33.1 / 47.9 / 49.7 %, fp64 2^12 40.8 / 41.0 / 42.3 % of HBM
+#endif
+template <int LOG2N, typename T>
+constexpr bool mid_class() {
+    return (sizeof(T) == 4 && LOG2N == 13) || (sizeof(T) == 8 && LOG2N == 12);
+}
+template <int LOG2N, typename T>
+constexpr int cps_for() {
+    if (LOG2N <= 11) {
+        if (QFT_CPS_SMALL > 0) return QFT_CPS_SMALL;
+        if (sizeof(T) == 4 && LOG2N == 7) return 1;
+        if (sizeof(T) == 4 && LOG2N == 11) return 2;
+        return 3;
+    }
+    if (mid_class<LOG2N, T>()) return QFT_CPS_MID;
+    return (LOG2N <= 12 && QFT_CTAS_PER_SM > 1) ? QFT_CTAS_PER_SM : 1;
+}
 template <int LOG2N, typename T>
 struct KCfg {
     using P = SPlan<LOG2N>;
     static constexpr int VB = (int)sizeof(vec2<T>);
     static constexpr int UB = P::UCELLS * (int)sizeof(T);
     // CTAs per SM: the QFT_CTAS_PER_SM split applies where one signal still fits
-    static constexpr int CPS = (P::n <= 12 && QFT_CTAS_PER_SM > 1) ? QFT_CTAS_PER_SM : 1;
+    static constexpr int CPS = cps_for<LOG2N, T>();
     static constexpr int BUDGET = (226 * 1024) / CPS - UB - 64;
     static constexpr int PER_W = P::PADDED * VB;        // working area per signal
     static constexpr int PER_S = P::N * VB + PER_W;     // + TMA staging
-    static constexpr int TTC = P::n >= 12 ? QFT_TT_MAX : 64;
+    static constexpr int TTC = mid_class<LOG2N, T>() ? QFT_TT_MID : (P::n >= 12 ? QFT_TT_MAX : 64);
     static constexpr int clampt(int t) { return t < 1 ? 1 : (t > TTC ? TTC : t); }
     // stage through TMA when the staging buffer still leaves room for 2 signals
     // (fp32) / 1 signal (fp64, whose global A0 path spills)
@@ -192,7 +224,9 @@ struct KCfg {
     static constexpr int NW0 = mx(W_U, W_D);
     // warps are spread over 4 SM sub-partitions of 16K registers each: 12 warps
     // keep 168 registers (fp64), 16 keep 128; 17 (fp32, N <= 4096) drop to 96
-    static constexpr int NWMAX = sizeof(T) == 8 ? 12 : (P::n >= 13 ? 16 : 17);
+    static constexpr int NWMAX1 = sizeof(T) == 8 ? 12 : (P::n >= 13 ? 16 : 17);
+    // several resident CTAs share the register file: 24 warps per SM keep 85 registers (fp32)
+    static constexpr int NWMAX = CPS == 1 ? NWMAX1 : (sizeof(T) == 8 ? 12 : 24) / CPS;
     static constexpr int NWLO = QFT_NW_MIN > NWMAX ? NWMAX : QFT_NW_MIN;
     static constexpr int NW = NW0 < NWLO ? NWLO : (NW0 > NWMAX ? NWMAX : NW0);
     static constexpr int NT = NW * 32;
@@ -209,7 +243,7 @@ struct KCfg {
 template <int LOG2N, typename T>
 constexpr bool smem_fits() {
     using P = SPlan<LOG2N>;
-    return (P::PADDED * (int)sizeof(vec2<T>) + P::UCELLS * (int)sizeof(T) + 64) <= (226 * 1024) / ((LOG2N <= 12 && QFT_CTAS_PER_SM > 1) ? QFT_CTAS_PER_SM : 1);
+    return (P::PADDED * (int)sizeof(vec2<T>) + P::UCELLS * (int)sizeof(T) + 64) <= (226 * 1024) / cps_for<LOG2N, T>();
 }
 
 // ------------------------------------------------------------ small N
@@ -614,11 +648,16 @@ QFT_DEV void phased_units(vec2<T> *W, const T *U, const T *kcu, int ntr, int tid
         __syncthreads();
     }
     if constexpr (NL > 0) {
-        for (int it = tid; it < TT * 2 * NL; it += NT) {
-            const int tau = it / (2 * NL), r = it - tau * (2 * NL);
-            const bool dst = r >= NL;
-            if (tau >= ntr || (dst ? !DOS : !DOC)) continue;
-            b_l32<false, T>(side(tau, dst), 32 * (r - (dst ? NL : 0)), kcu, dst);
+        // NL + 1 = m/32 slots per side (the last one idle): a side's chunks sit 33 cells
+        // apart and the sine side starts padx(m) = m/32 (mod 16) cells after the cosine
+        // side, so the 16 lanes of a half-warp -- one side, or 16 / (NL + 1) sides -- hit
+        // 16 distinct bank pairs (ncu: 2-way conflicts with NL slots per side)
+        constexpr int NLP = NL + 1;
+        for (int it = tid; it < TT * 2 * NLP; it += NT) {
+            const int tau = it / (2 * NLP), r = it & (2 * NLP - 1), k = r & (NLP - 1);
+            const bool dst = r >= NLP;
+            if (k == NL || tau >= ntr || (dst ? !DOS : !DOC)) continue;
+            b_l32<false, T>(side(tau, dst), 32 * k, kcu, dst);
         }
     }
     // the L <= 16 blocks of every side, on the threads with the fewest chunks (the last ones)

@@ -46,7 +46,8 @@ def test_no_fused_multiply_add_in_transform_kernels():
     feeding an FFMA2 addend must be written only by loads/moves (never by
     arithmetic), so no product is ever fused into a sum."""
     funcs, _ = sass_by_function()
-    kernels = {k: v for k, v in funcs.items() if "qft_cdft" in k or "lg_" in k}
+    kernels = {k: v for k, v in funcs.items() if "qft_cdft" in k or "lg_" in k or "cl_" in k or "classical_kernel" in k}
+    assert any("cl_tree_kernel" in k for k in kernels) and any("cl_glevel_kernel" in k for k in kernels)
     assert len(kernels) >= 20, "expected the per-size transform kernels"
     for name, ops in kernels.items():
         fused = [o for o, _, _ in ops if re.match(r"(FFMA(?!2)|DFMA|HFMA)", o)]

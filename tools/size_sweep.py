@@ -18,7 +18,8 @@ def main():
         peak = 6650.0
     rows = []
     for dt in (torch.complex64, torch.complex128):
-        for lg in range(5, 21):
+        lo, hi = (int(sys.argv[sys.argv.index("--lg") + 1]), int(sys.argv[sys.argv.index("--lg") + 2])) if "--lg" in sys.argv else (5, 20)
+        for lg in range(lo, hi + 1):
             N = 1 << lg
             es = 8 if dt == torch.complex64 else 16
             B = max(1, (1 << 30) // (N * es))
