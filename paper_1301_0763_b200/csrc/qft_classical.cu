@@ -366,25 +366,38 @@ constexpr int kLvMaxSmem = 227 * 1024;
 
 QFT_HD int lv_smem_bytes(int lognn) { return 2 * cl::buf_cells(lognn) * (int)sizeof(V); }
 
-// forward levels, register-level bases and backward levels of one tree held in P0 / P1
-__device__ __forceinline__ void lv_run_tree(const cl::Tree<Real> &t, V *P0, V *P1, int tid, int NT) {
-    const int D = t.depth();
-    V *cen = P0 + cl::cen_off(t.lognn);
+// the opaque (-0, -0) addend of the packed fp32 multiplies, once per kernel
+__device__ __forceinline__ void lv_load_mz(cl::Mul<float> &m) { m.z = __ldg(&::qft_mzero_pair); }
+__device__ __forceinline__ void lv_load_mz(cl::Mul<double> &) {}
+
+// shared memory of the whole-signal kernel (one signal per iteration): two buffers + the natural table
+QFT_HD int lv_tree_smem_bytes(int lognn) { return lv_smem_bytes(lognn) + (1 << (lognn - 2)) * (int)sizeof(Real); }
+
+// forward levels, register-level bases and backward levels of nt trees (signal s in the
+// buffer pair at P + s * 2 * buf): the items of all trees flat over the CTA's threads
+// (ONE: nt == 1, the tree index drops out of the item loops)
+template <bool ONE>
+__device__ __forceinline__ void lv_run_trees(const cl::Tree<Real> &t, V *P, int buf, int nt_arg, int tid, int NT) {
+    const int nt = ONE ? 1 : nt_arg;
+    const int D = t.depth(), coff = cl::cen_off(t.lognn);
+    const int lf = t.lognn - 2, lb = D + 1;  // log2 of the level / base items per tree
     for (int d = 0; d < D; ++d) {
-        const V *s = (d & 1) ? P1 : P0;
-        V *o = (d & 1) ? P0 : P1;
-        for (int it = tid; it < t.fwd_items(); it += NT) t.fwd_item(s, o, cen, d, it);
+        for (int it = tid; it < (nt << lf); it += NT) {
+            V *P0 = ONE ? P : P + (it >> lf) * 2 * buf, *P1 = P0 + buf;
+            t.fwd_item((d & 1) ? P1 : P0, (d & 1) ? P0 : P1, P0 + coff, d, it & ((1 << lf) - 1));
+        }
         __syncthreads();
     }
-    {
-        V *b = (D & 1) ? P1 : P0;
-        for (int it = tid; it < t.base_items(); it += NT) t.base_item(b, it);
-        __syncthreads();
+    for (int it = tid; it < (nt << lb); it += NT) {
+        V *P0 = ONE ? P : P + (it >> lb) * 2 * buf;
+        t.base_item((D & 1) ? P0 + buf : P0, it & ((1 << lb) - 1));
     }
+    __syncthreads();
     for (int d = D - 1; d >= 0; --d) {
-        const V *chi = ((d + 1) & 1) ? P1 : P0;
-        V *o = (d & 1) ? P1 : P0;
-        for (int it = tid; it < t.bwd_items(); it += NT) t.bwd_item(chi, o, cen, d, it);
+        for (int it = tid; it < (nt << lf); it += NT) {
+            V *P0 = ONE ? P : P + (it >> lf) * 2 * buf, *P1 = P0 + buf;
+            t.bwd_item(((d + 1) & 1) ? P1 : P0, (d & 1) ? P1 : P0, P0 + coff, d, it & ((1 << lf) - 1));
+        }
         __syncthreads();
     }
 }
@@ -392,24 +405,36 @@ __device__ __forceinline__ void lv_run_tree(const cl::Tree<Real> &t, V *P0, V *P
 // MINB: resident CTAs per SM the register budget is set for (1: 512 threads, else 256)
 template <int MODE, int MINB>
 __global__ void __launch_bounds__(MINB == 1 ? 512 : 256, MINB)
-    cl_tree_kernel(const void *in, void *out, long long units, long long nreal, int log2n,
+    cl_tree_kernel(const void *in, void *out, long long units, long long nreal, int log2n, int tt,
                    const Real *__restrict__ Tt) {
+    // tt signals (or pairs of real rows) per CTA iteration: small trees have few items
+    // per level, so several share the CTA's threads
     extern __shared__ __align__(16) unsigned char cl_smem[];
-    V *P0 = reinterpret_cast<V *>(cl_smem), *P1 = P0 + cl::buf_cells(log2n);
-    const cl::Tree<Real> t{log2n, log2n, cl::cos_cells(log2n), false, MODE != 3, MODE != 2, Tt};
-    const int N = 1 << log2n, m = N / 2, tid = threadIdx.x, NT = blockDim.x;
-    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-        for (int n = tid; n < m; n += NT) cl::ingest_item<MODE, Real>(in, u, nreal, N, P0, t.CB, n);
+    const int buf = cl::buf_cells(log2n);
+    V *P = reinterpret_cast<V *>(cl_smem);
+    Real *Ts = reinterpret_cast<Real *>(P + 2 * buf * tt);  // the natural table, N/4 entries
+    cl::Tree<Real> t{log2n, log2n, cl::cos_cells(log2n), false, MODE != 3, MODE != 2, Ts};
+    lv_load_mz(t.mul);
+    const int N = 1 << log2n, m = N / 2, lm = log2n - 1, tid = threadIdx.x, NT = blockDim.x;
+    for (int i = tid; i < N / 4; i += NT) Ts[i] = Tt[i];  // published by the first barrier below
+    for (long long u0 = (long long)blockIdx.x * tt; u0 < units; u0 += (long long)gridDim.x * tt) {
+        const int nt = (int)(units - u0 < tt ? units - u0 : tt);
+        for (int it = tid; it < (nt << lm); it += NT)
+            cl::ingest_item<MODE, Real>(in, u0 + (it >> lm), nreal, N, P + (it >> lm) * 2 * buf, t.CB, it & (m - 1));
         __syncthreads();
-        lv_run_tree(t, P0, P1, tid, NT);
-        for (int k = tid; k <= m; k += NT) cl::emit_item<MODE, Real>(out, u, nreal, N, P0, t.CB, k);
+        if (tt == 1) lv_run_trees<true>(t, P, buf, 1, tid, NT);
+        else lv_run_trees<false>(t, P, buf, nt, tid, NT);
+        for (int it = tid; it < nt * (m + 1); it += NT) {
+            const int sidx = it / (m + 1), k = it - sidx * (m + 1);
+            cl::emit_item<MODE, Real>(out, u0 + sidx, nreal, N, P + sidx * 2 * buf, t.CB, k);
+        }
         __syncthreads();
     }
 }
 
 template <int MODE, int MINB>
 cudaError_t lv_launch_tree(const void *in, void *out, long long units, long long nreal, int log2n, const Real *Tt,
-                           int smem, int num_sms, cudaStream_t st) {
+                           int tt, int smem, int num_sms, cudaStream_t st) {
     auto kern = cl_tree_kernel<MODE, MINB>;
     constexpr int NT = MINB == 1 ? 512 : 256;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -418,10 +443,14 @@ cudaError_t lv_launch_tree(const void *in, void *out, long long units, long long
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
-    long long grid = (long long)num_sms * per_sm;
-    if (grid > units) grid = units;
+    const long long ctas = (long long)num_sms * per_sm;
+    // small batches: fewer signals per CTA iteration so that every SM gets work
+    if (units < ctas * tt) tt = (int)((units + ctas - 1) / ctas);
+    if (tt < 1) tt = 1;
+    long long grid = (units + tt - 1) / tt;
+    if (grid > ctas) grid = ctas;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, NT, smem, st>>>(in, out, units, nreal, log2n, Tt);
+    kern<<<(unsigned)grid, NT, smem, st>>>(in, out, units, nreal, log2n, tt, Tt);
     return cudaGetLastError();
 }
 
@@ -450,7 +479,8 @@ template <bool BWD>
 __global__ void __launch_bounds__(256) cl_glevel_kernel(const V *src, V *dst, V *W0, long long Ws, long long units, int log2n,
                                                         int d, bool do_cos, bool do_sin,
                                                         const Real *__restrict__ Tt) {
-    const cl::Tree<Real> t{log2n, log2n, cl::cos_cells(log2n), false, do_cos, do_sin, Tt};
+    cl::Tree<Real> t{log2n, log2n, cl::cos_cells(log2n), false, do_cos, do_sin, Tt};
+    lv_load_mz(t.mul);
     const int it = blockIdx.x * blockDim.x + threadIdx.x;
     if (it >= (BWD ? t.bwd_items() : t.fwd_items())) return;
     for (long long u = blockIdx.y; u < units; u += gridDim.y) {
@@ -469,7 +499,8 @@ __global__ void __launch_bounds__(256, 3) cl_subtree_kernel(V *Wd, long long Ws,
     for (long long g = blockIdx.x; g < (units << d0); g += gridDim.x) {
         const long long u = g >> d0;
         const int b = (int)(g & ((1LL << d0) - 1));
-        const cl::Tree<Real> t{sublog, log2n, cl::cos_cells(sublog), (b & 1) != 0, do_cos, do_sin, Tt};
+        cl::Tree<Real> t{sublog, log2n, cl::cos_cells(sublog), (b & 1) != 0, do_cos, do_sin, Tt};
+        lv_load_mz(t.mul);
         V *wc = Wd + u * Ws + cl::cos_off(S0, b), *ws = Wd + u * Ws + CBtop + (long long)b * cl::sin_stride_of(log2n, d0);
         const int nc = S0 + ((b & 1) ? 0 : 1);
         if (do_cos)
@@ -477,7 +508,7 @@ __global__ void __launch_bounds__(256, 3) cl_subtree_kernel(V *Wd, long long Ws,
         if (do_sin)
             for (int i = tid; i < S0 - 1; i += NT) P0[t.CB + i] = ws[i];
         __syncthreads();
-        lv_run_tree(t, P0, P1, tid, NT);
+        lv_run_trees<true>(t, P0, cl::buf_cells(sublog), 1, tid, NT);
         if (do_cos)
             for (int i = tid; i < nc; i += NT) wc[i] = P0[i];
         if (do_sin)
@@ -489,19 +520,25 @@ __global__ void __launch_bounds__(256, 3) cl_subtree_kernel(V *Wd, long long Ws,
 template <int MODE>
 cudaError_t lv_launch_mode(const void *in, void *out, long long units, long long nreal, int log2n, const Real *Tt,
                            V *arena, size_t arena_bytes, int num_sms, cudaStream_t st) {
-    const int smem = lv_smem_bytes(log2n);
-    if (smem <= kLvMaxSmem) {
+    if (lv_tree_smem_bytes(log2n) <= kLvMaxSmem) {
         static const int minb_env = [] {  // QFT_CL_MINB=1|2|3: force the register budget (A/B)
             const char *v = getenv("QFT_CL_MINB");
             return v ? atoi(v) : 0;
         }();
+        // signals per CTA iteration: enough trees that the register-level bases
+        // (N/16 per tree) cover the CTA's 256 threads, within a third of the shared memory
+        const int pair = lv_smem_bytes(log2n), tab = (1 << (log2n - 2)) * (int)sizeof(Real);
+        int tt = 256 / (1 << (log2n - 4));
+        if (tt < 1) tt = 1;
+        while (tt > 1 && tt * pair + tab > 72 * 1024) tt >>= 1;
+        const int smem = tt * pair + tab;
         const int fit = kLvMaxSmem / (smem + 1024);
         int minb = fit >= 3 ? 3 : (fit >= 2 ? 2 : 1);
         if (minb_env >= 1 && minb_env <= 3 && minb_env <= (fit > 1 ? fit : 1)) minb = minb_env;
         switch (minb) {
-            case 1: return lv_launch_tree<MODE, 1>(in, out, units, nreal, log2n, Tt, smem, num_sms, st);
-            case 2: return lv_launch_tree<MODE, 2>(in, out, units, nreal, log2n, Tt, smem, num_sms, st);
-            default: return lv_launch_tree<MODE, 3>(in, out, units, nreal, log2n, Tt, smem, num_sms, st);
+            case 1: return lv_launch_tree<MODE, 1>(in, out, units, nreal, log2n, Tt, tt, smem, num_sms, st);
+            case 2: return lv_launch_tree<MODE, 2>(in, out, units, nreal, log2n, Tt, tt, smem, num_sms, st);
+            default: return lv_launch_tree<MODE, 3>(in, out, units, nreal, log2n, Tt, tt, smem, num_sms, st);
         }
     }
     // large N: global levels down to sub-trees of 2^sublog
@@ -550,7 +587,7 @@ cudaError_t lv_launch_mode(const void *in, void *out, long long units, long long
 // bytes of global scratch the level-synchronous path wants for `units` signals
 // (0: the whole tree fits shared memory); any amount >= one signal's works (chunked)
 long long QFT_CL(qft_classical_lv_arena_bytes)(int log2n, long long units) {
-    if (log2n < cl::kBaseLog || lv_smem_bytes(log2n) <= kLvMaxSmem) return 0;
+    if (log2n < cl::kBaseLog || lv_tree_smem_bytes(log2n) <= kLvMaxSmem) return 0;
     const long long per = 2 * (long long)cl::buf_cells(log2n) * (long long)sizeof(V);
     // QFT_CL_ARENA_MB: scratch budget (tests use a small one to exercise the chunking)
     long long budget = 4LL << 30;

@@ -57,6 +57,27 @@ QFT_HD int buf_cells(int lognn) { return cen_off(lognn) + (1 << (base_depth(logn
 // one pad cell at the base depth (Tree::sin_stride)
 QFT_HD int sin_stride_of(int lognn, int d) { return (1 << (lognn - 1 - d)) + (d == base_depth(lognn) ? 1 : 0); }
 
+// vec2 * constant.  fp32 on the device: the packed multiply x*c + z with the opaque
+// (-0, -0) addend of vmul<float> (qft_common.cuh), z loaded once per kernel instead
+// of once per multiply
+template <typename T>
+struct Mul {
+    QFT_HD vec2<T> operator()(vec2<T> a, T c) const { return vmul(a, c); }
+};
+template <>
+struct Mul<float> {
+    unsigned long long z = 0x8000000080000000ull;  // the kernels overwrite it with the global's value
+    QFT_HD vec2<float> operator()(vec2<float> a, float c) const {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000 && !defined(QFT_NO_F32X2) && !defined(QFT_SCALAR_MUL)
+        unsigned long long r;
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a)), "l"(pk(vec2<float>{c, c})), "l"(z));
+        return upk(r);
+#else
+        return vmul(a, c);
+#endif
+    }
+};
+
 // half-secant 1/(2cos(2 pi n / 2^lognode)) from the natural table of the top
 // periodization 2^logtop (counting.py:152-158: a constant depends only on the
 // reduced fraction)
@@ -64,7 +85,7 @@ template <typename T>
 struct HS {
     const T *Tt;
     int logtop;
-    QFT_HD T operator()(int n, int lognode) const { return Tt[(long long)n << (logtop - lognode)]; }
+    QFT_HD T operator()(int n, int lognode) const { return Tt[n << (logtop - lognode)]; }
 };
 
 // ---------------------------------------------------------------- register-level bases
@@ -191,6 +212,7 @@ struct Tree {
     int lognn, logtop, CB;
     bool root_odd, do_cos, do_sin;
     const T *Tt;
+    Mul<T> mul = {};
     QFT_HD int depth() const { return base_depth(lognn); }
     QFT_HD bool odd_type(int d, int b) const { return d ? (b & 1) : root_odd; }
 
@@ -210,13 +232,13 @@ struct Tree {
             } else {  // classical.py:86-92, elaborations.py:102-112
                 const int sh = logtop - (lognn + 1 - d);  // node periodization 4S
                 if (i == 0) {
-                    ev[q] = vmul(x[q], Tt[(long long)q << sh]);
-                    const vec2<T> c0 = vmul(x[0], (T)0.5), zero = {(T)0, (T)0};
+                    ev[q] = mul(x[q], Tt[q << sh]);
+                    const vec2<T> c0 = mul(x[0], (T)0.5), zero = {(T)0, (T)0};
                     ev[0] = vadd(c0, zero);
                     od[0] = vsub(c0, zero);
                 } else {
-                    const vec2<T> a = vmul(x[i], Tt[(long long)i << sh]);
-                    const vec2<T> c = vmul(x[S - i], Tt[(long long)(S - i) << sh]);
+                    const vec2<T> a = mul(x[i], Tt[i << sh]);
+                    const vec2<T> c = mul(x[S - i], Tt[(S - i) << sh]);
                     ev[i] = vadd(a, c);
                     od[i] = vsub(a, c);
                 }
@@ -230,7 +252,7 @@ struct Tree {
                 const int sh = logtop - (lognn - d);  // node periodization 2S
                 const vec2<T> a = x[i], c = x[S - 2 - i];
                 ev[i] = vsub(a, c);
-                oc[i] = vmul(vadd(a, c), Tt[(long long)(i + 1) << sh]);
+                oc[i] = mul(vadd(a, c), Tt[(i + 1) << sh]);
             } else {
                 cen[(1 << d) + b] = x[q - 1];  // the centre s(N/4)
             }

@@ -38,6 +38,9 @@ namespace {
 
 // largest single-pass sub-signal / leaf: 2^14 cells fp32, 2^13 fp64 (128 KiB)
 constexpr int kSubLogMax = QFT_LARGE_PREC == 32 ? 14 : 13;
+#ifndef QFT_FOLD64
+#define QFT_FOLD64 0  // fp64 plans with J0 <= 2 (N = 2^14, 2^15) fold on load like the fp32 ones
+#endif
 constexpr int kRG = 5;  // fold levels per F/B pass (fp64 R = 5: lane pairs, lg_f_pair5 / lg_b_pair5_out)
 constexpr int kRC = 4;                                    // chain levels unfolded per thread
 constexpr int kChunk = 256;
@@ -82,7 +85,9 @@ struct QFT_LG(LargePlan) {
     // (sub_item).  Those gathers read every sector of x several times from L2, so
     // this only pays where the fold pass is a large share of the step: measured
     // +3.7 % at fp32 N = 2^16 (config 3), -4 % at fp64 N = 2^20 (config 4).
-    static bool fold_on_load(int log2n) { return QFT_LARGE_PREC == 32 && log2n - sublog_for(log2n) <= 2; }
+    static bool fold_on_load(int log2n) {
+        return (QFT_LARGE_PREC == 32 || QFT_FOLD64) && log2n - sublog_for(log2n) <= 2;
+    }
 };
 
 template <typename TT>

@@ -24,4 +24,12 @@ for c in 2 3 4 5; do
   python tools/prof_stalls.py $out/prof_c$c.ncu-rep >> $out/prof_c$c.txt 2>&1
 done
 rm -f $out/prof_c3.ncu-rep $out/prof_c4.ncu-rep
+timeout 300 python tools/size_sweep.py --json $out/size_sweep.json > $out/size_sweep.txt 2>&1
+timeout 300 python tools/size_sweep.py --algo classical --json $out/size_sweep_classical.json > $out/size_sweep_classical.txt 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  -k regex:"cl_" -c 60 --csv --log-file $out/launches_classical_c4.csv python tools/classical_prof.py 20 64 f64 > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:cl_tree -s 2 -c 1 -o $out/prof_classical_c2 python tools/classical_prof.py 12 16384 > /dev/null 2>&1
+python tools/prof_summary.py $out/prof_classical_c2.ncu-rep 16384 > $out/prof_classical_c2.txt 2>&1
+python tools/prof_stalls.py $out/prof_classical_c2.ncu-rep >> $out/prof_classical_c2.txt 2>&1
+rm -f $out/prof_classical_c2.ncu-rep $out/prof_c2.ncu-rep $out/prof_c5.ncu-rep
 echo done > $out/status
