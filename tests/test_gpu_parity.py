@@ -444,3 +444,38 @@ def test_classical_recursive_kernel_still_matches(torch_cuda, oracle_mod):
     for lg in (1, 2, 3, 4):
         z = (np.random.default_rng(lg).standard_normal((1 << lg, 70)) + 0j).astype(np.complex128)
         assert bit_equal(classical.cdft(z), oracle_mod.cdft(z, algo="classical"))
+
+
+@pytest.mark.parametrize("dt", [np.complex64, np.complex128])
+@pytest.mark.parametrize("lg", [6, 7, 8, 9, 10, 11, 13])
+def test_small_sizes_full_batches_bitwise(torch_cuda, dt, lg):
+    """The phased-unit schedule of N <= 2048 (Lee-32 chunks of all signals of a CTA
+    iteration flat over the threads, several resident CTAs) and the one-signal-per-
+    iteration 2^13 / fp64 2^12 configurations: every row of batches that leave the last
+    iteration ragged, that are smaller than the resident CTAs (signals per iteration
+    lowered at launch), and that give every CTA several iterations."""
+    torch = torch_cuda
+    from oracle import parity
+    from paper_1301_0763_b200 import improved
+    N = 1 << lg
+    rt = torch.float32 if dt == np.complex64 else torch.float64
+    g = torch.Generator(device="cuda").manual_seed(lg)
+    for B in (1, 2, 7, 147, 449, 1501, 20011 if lg <= 9 else 5003):
+        x = torch.view_as_complex(torch.randn((B, N, 2), dtype=rt, device="cuda", generator=g))
+        y = improved.cdft_rows(x)
+        torch.cuda.synchronize()
+        rep = parity.check_rows(x, y)
+        assert rep["rows_checked"] == B and rep["mismatches"] == 0, (lg, B, rep)
+
+
+@pytest.mark.parametrize("kind", ["rdft", "dct0", "dst0"])
+@pytest.mark.parametrize("lg", [6, 8, 10, 11])
+def test_small_sizes_real_modes_many_rows(torch_cuda, oracle_mod, kind, lg):
+    """Real entry points through the phased units: odd row counts (the last vec2 lane
+    half unused) over several CTA iterations."""
+    from paper_1301_0763_b200 import improved
+    N = 1 << lg
+    n_vals = {"rdft": N, "dct0": N // 2 + 1, "dst0": N // 2 - 1}[kind]
+    for dt in (np.float32, np.float64):
+        x = np.random.default_rng(lg).standard_normal((n_vals, 1237)).astype(dt)
+        assert bit_equal(getattr(improved, kind)(x), getattr(oracle_mod, kind)(x))
