@@ -315,7 +315,8 @@ def accuracy_config4(x, y, stream, steps=2):
             "exact": "numpy.fft.fft of the same fp64 rows",
             "rows": int(xs.shape[0]),
             "classical_gpu": {"ms_per_step": cms, "value": xs.shape[0] / (cms / 1000.0), "unit": UNIT,
-                              "kernel": "qft_classical (warp-cooperative recursion, csrc/qft_classical.cu)"}}
+                              "kernel": "classical QFT, level-synchronous schedule (global levels + "
+                                        "shared-memory sub-trees, csrc/qft_classical_lv.cuh)"}}
 
 
 def main():
