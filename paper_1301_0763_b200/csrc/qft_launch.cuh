@@ -405,7 +405,7 @@ QFT_DEV void unit_big(vec2<T> *wb, const T *U, const T *kcu, int lane, int ub = 
     f.store(wb, lane);
     __syncwarp();
     QFT_UMARK(2);
-    if (lane < (1 << R)) b_l32p<DST, T>(wb + 33 * lane, kcu, ub);
+    if (lane < (1 << R)) b_l32p<DST, T>(wb + 33 * lane, kcu, ub, lane & 1);
     __syncwarp();
     QFT_UMARK(3);
     run_c_blockp<R, DST, T>(wb, lane);
@@ -477,7 +477,7 @@ QFT_DEV void unit_rest(vec2<T> *w, const T *U, const T *kcu, int lane, int ub = 
     run_f_blocks<LOG2N, T, P::JR>(w, U, DST, lane);
 #endif
     __syncwarp();
-    if (lane < CNT) b_l32<DST, T>(w, sb + 32 * (P::K0 + lane), kcu, ub);
+    if (lane < CNT) b_l32<DST, T>(w, sb + 32 * (P::K0 + lane), kcu, ub, (P::K0 + lane) & 1);
     else if (SMALL && lane == CNT) b_small<LOG2N, DST, T>(w, kcu, ub);
     __syncwarp();
 #if QFT_REST_FUSED
@@ -660,7 +660,7 @@ QFT_DEV void phased_units(vec2<T> *W, const T *U, const T *kcu, int ntr, int tid
             const int tau = it / (2 * NLP), r = it & (2 * NLP - 1), k = r & (NLP - 1);
             const bool dst = r >= NLP;
             if (k == NL || tau >= ntr || (dst ? !DOS : !DOC)) continue;
-            b_l32<false, T>(side(tau, dst), 32 * k, kcu, dst);
+            b_l32<false, T>(side(tau, dst), 32 * k, kcu, dst, k & 1);
         }
     }
     // the L <= 16 blocks of every side, on the threads with the fewest chunks (the last ones)

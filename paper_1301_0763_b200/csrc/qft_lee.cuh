@@ -102,15 +102,23 @@ QFT_HD void lee_fwd(vec2<T> *v, int t, const T *U) {
 // (DST) column, where the reference copies instead of adding.
 // Out: block spectrum slots [i*2^R, (i+1)*2^R).
 // ---------------------------------------------------------------------------
-template <int R, bool DST, typename T, class Halo>
+// PRE: the odd sub-blocks (odd p) arrive with their deepest neighbour sum already
+// formed -- Z_p[i] + Z_p[i+1] (DCT; Z_p[i-1] + Z_p[i] for the DST; the edge column
+// a copy) -- by the Lee-32 step that produced them (b_l32p, qft_smem.cuh), which
+// held both operands in one lane: the deepest level is then a pure interleave and
+// reads no halo (16 of the 31 halo reads of a 32-sub-block column).
+template <int R, bool DST, typename T, class Halo, bool PRE = false>
 QFT_HD void lee_bwd_fn(const vec2<T> *v, int pofs, Halo &halo, bool edge, vec2<T> *out) {
     if constexpr (R == 0) {
         out[0] = v[0];
+    } else if constexpr (PRE && R == 1) {
+        out[DST ? 1 : 0] = v[0];
+        out[DST ? 0 : 1] = v[1];
     } else {
         constexpr int H = 1 << (R - 1);
         vec2<T> e[H], o[H];
-        lee_bwd_fn<R - 1, DST, T>(v, pofs, halo, edge, e);
-        lee_bwd_fn<R - 1, DST, T>(v + H, pofs + H, halo, edge, o);
+        lee_bwd_fn<R - 1, DST, T, Halo, PRE>(v, pofs, halo, edge, e);
+        lee_bwd_fn<R - 1, DST, T, Halo, PRE>(v + H, pofs + H, halo, edge, o);
         const vec2<T> hv = halo(pofs + H);  // leftmost leaf of the odd child
         if constexpr (!DST) {
 #pragma unroll

@@ -348,18 +348,37 @@ struct Top {
 #else
 #define QFT_L32_ATTR QFT_HD
 #endif
+#ifndef QFT_PRESUM
+// The Lee-32 step of an odd sub-block (odd chunk index: every block cut into
+// sub-blocks starts at an even chunk and has an even number of them, and the
+// uncut L = 32 block sits at an even chunk) also forms the first backward level's
+// neighbour sums Z[i] + Z[i+1] -- the same operation on the same operands the C
+// step would do with a halo read of the next column -- so phase C reads 15 halo
+// cells per column instead of 31 (lee_bwd_fn PRE, qft_lee.cuh).
+#define QFT_PRESUM 1
+#endif
+// pre: this chunk is an odd sub-block of a cut block (QFT_PRESUM)
 template <bool DST, typename T>
-QFT_L32_ATTR void b_l32p(vec2<T> *c, const T *U, int ub = DST ? 1 : 0) {
+QFT_L32_ATTR void b_l32p(vec2<T> *c, const T *U, int ub = DST ? 1 : 0, bool pre = false) {
     vec2<T> v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = c[e];
     lee_full<32, DST, T>(v, U, ub);
+    if (QFT_PRESUM && pre) {
+        if constexpr (!DST) {
+#pragma unroll
+            for (int e = 0; e < 31; ++e) v[e] = vadd(v[e], v[e + 1]);  // column 31: the edge copy
+        } else {
+#pragma unroll
+            for (int e = 31; e > 0; --e) v[e] = vadd(v[e - 1], v[e]);  // column 0: the edge copy
+        }
+    }
 #pragma unroll
     for (int e = 0; e < 32; ++e) c[e] = v[e];
 }
 template <bool DST, typename T>
-QFT_HD void b_l32(vec2<T> *w, int chunk_base, const T *U, int ub = DST ? 1 : 0) {
-    b_l32p<DST, T>(w + padx(chunk_base), U, ub);
+QFT_HD void b_l32(vec2<T> *w, int chunk_base, const T *U, int ub = DST ? 1 : 0, bool pre = false) {
+    b_l32p<DST, T>(w + padx(chunk_base), U, ub, pre);
 }
 
 template <int LOG2N, bool DST, typename T, int J>
@@ -407,7 +426,7 @@ struct CBlockP {
     template <class Halo>
     QFT_HD void compute(int i, Halo &&halo, vec2<T> *out) const {
         const bool edge = DST ? (i == 0) : (i == 31);
-        lee_bwd_fn<R, DST, T>(own, 0, halo, edge, out);
+        lee_bwd_fn<R, DST, T, Halo, QFT_PRESUM != 0>(own, 0, halo, edge, out);
     }
     QFT_HD static void storep(vec2<T> *wb, int i, const vec2<T> *out) {
         // slots i*G .. i*G+G-1 lie inside one 32-cell chunk: contiguous when padded

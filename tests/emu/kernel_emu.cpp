@@ -31,7 +31,7 @@ static void emu_unit_big(vec2<T> *wb, const T *U, int ub = DST ? 1 : 0) {
     std::vector<FBlockP<L, R, DST, T>> f(32);
     for (int t = 0; t < 32; ++t) f[t].template load<REV>(wb, U, t);   // all lanes load ...
     for (int t = 0; t < 32; ++t) f[t].store(wb, t);     // ... __syncwarp ... store
-    for (int p = 0; p < (1 << R); ++p) b_l32p<DST, T>(wb + 33 * p, U, ub);
+    for (int p = 0; p < (1 << R); ++p) b_l32p<DST, T>(wb + 33 * p, U, ub, p & 1);
     using CB = CBlockP<R, DST, T>;
     std::vector<CB> c(32);
     std::vector<std::vector<vec2<T>>> outs(32, std::vector<vec2<T>>(CB::G));
@@ -84,7 +84,7 @@ template <int LOG2N, typename T, bool DST>
 static void emu_unit_rest(vec2<T> *w, const T *U, int ub = DST ? 1 : 0) {
     using P = SPlan<LOG2N>;
     emu_rest_f<LOG2N, T, P::JR, DST>(w, U);
-    for (int k = P::K0; k < P::NL32; ++k) b_l32<DST, T>(w, (DST ? P::S0 : 0) + 32 * k, U, ub);
+    for (int k = P::K0; k < P::NL32; ++k) b_l32<DST, T>(w, (DST ? P::S0 : 0) + 32 * k, U, ub, k & 1);
     b_small<LOG2N, DST, T>(w, U, ub);
     emu_rest_c<LOG2N, T, P::JR, DST>(w);
 }
