@@ -38,6 +38,9 @@ namespace {
 
 // largest single-pass sub-signal / leaf: 2^14 cells fp32, 2^13 fp64 (128 KiB)
 constexpr int kSubLogMax = QFT_LARGE_PREC == 32 ? 14 : 13;
+#ifndef QFT_LEAF_PAIR_GATHER
+#define QFT_LEAF_PAIR_GATHER 1  // the two fold-on-load leaves of a block share one gather of x
+#endif
 #ifndef QFT_FOLD64
 #define QFT_FOLD64 0  // fp64 plans with J0 <= 2 (N = 2^14, 2^15) fold on load like the fp32 ones
 #endif
@@ -471,7 +474,9 @@ QFT_DEV int item_runs(const Item &it, const LeafTask *tasks, int N, long long *l
 }
 
 // Leaf item: K leaves of 2^A cells from W0 runs -> their spectra along the runs.
-template <int A, typename T, int NT, int NW>
+// KC: the caller's K when it is a compile-time fact (2: the pair gather may apply), else 0
+// FX: the plan folds x on load (no fold pass): only then do leaves with j >= 0 occur
+template <int A, typename T, int NT, int NW, int KC = 0, bool FX = true>
 QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const T *kcu, vec2<T> *wb, int tid,
                        const vec2<T> *xb, int N, const CUtensorMap *tmap = nullptr, long long wrow = 0,
                        uint64_t *bar = nullptr, uint32_t *phase = nullptr) {
@@ -528,14 +533,30 @@ QFT_DEV void leaf_item(const LeafTask *tks, int K, vec2<T> *S, const T *U, const
     constexpr int G = LeafTop<A, false, T>::G, IT = (2 * 1024 + NT - 1) / NT;
     {
         vec2<T> v[IT][G];
+        // two fold-on-load leaves of one block (its cosine and its sine side): thread tid
+        // holds reflection group t of the first leaf in round r and of the second in
+        // round r + IT/2 -- one gather of x feeds both (QFT_LEAF_PAIR_GATHER)
+        constexpr bool HALVES = (IT % 2 == 0) && (NT * (IT / 2) == 1024);
+        constexpr bool PAIR_OK = QFT_LEAF_PAIR_GATHER && HALVES && KC == 2 && FX;
+        const bool pair = PAIR_OK && K == 2 && tks[0].j >= 0 && tks[1].j == tks[0].j && tks[0].dst != tks[1].dst;
+        if constexpr (PAIR_OK) if (pair) {
+            constexpr int H2 = HALVES ? IT / 2 : 0;  // rounds [0, H2): first leaf, [H2, IT): second leaf
+            if (!tks[0].dst) {
+#pragma unroll
+                for (int r = 0; r < H2; ++r) tf_load_x_pair<A, T>(xb, N, tks[0].j, U, tid + r * NT, v[r], v[H2 + r]);
+            } else {
+#pragma unroll
+                for (int r = 0; r < H2; ++r) tf_load_x_pair<A, T>(xb, N, tks[0].j, U, tid + r * NT, v[H2 + r], v[r]);
+            }
+        }
 #pragma unroll
         for (int r = 0; r < IT; ++r) {
             const int it = tid + r * NT;
-            if (it < K * 1024) {
+            if (!pair && it < K * 1024) {
                 const int k = it >> 10, t = it & 1023;
                 const vec2<T> *s = S + padx(k * L);
                 const int j = tks[k].j;
-                if (j >= 0) {
+                if (FX && j >= 0) {
                     if (tks[k].dst) LeafTop<A, true, T>::tf_load_x(xb, N, j, U, t, v[r]);
                     else LeafTop<A, false, T>::tf_load_x(xb, N, j, U, t, v[r]);
                 } else {
@@ -750,12 +771,17 @@ QFT_DEV void sub_item(const vec2<T> *w0b, int m, vec2<T> *W, const T *U, const T
     for (int t = tid; t < P::DT; t += NT) Chain<SUBLOG, T>::unit_e(W, emit, t);
 }
 
-template <int SUBLOG, typename T>
+// FX: the instance for plans that fold x on load (fold_x != 0); the other instance
+// serves the plans with a fold pass -- each drops the other's paths (the pair gather
+// of the fold-on-load leaves cost the shared instance 800 bytes of spills)
+template <int SUBLOG, typename T, bool FX>
 __global__ void __launch_bounds__(ItemCfg<SUBLOG, T>::NT, 1)
     lg_item_kernel(vec2<T> *W0, long long Ws, int log2n, const Item *__restrict__ items, int ni,
                    const LeafTask *__restrict__ tasks, long long batch, const T *__restrict__ Ug,
-                   const __grid_constant__ LeeConstL<T> kc, const vec2<T> *__restrict__ x, int fold_x,
+                   const __grid_constant__ LeeConstL<T> kc, const vec2<T> *__restrict__ x, int fold_x_arg,
                    const __grid_constant__ CUtensorMap tmap, int use_tma) {
+    constexpr int fold_x = FX ? 1 : 0;
+    (void)fold_x_arg;
     using C = ItemCfg<SUBLOG, T>;
     constexpr int NT = C::NT, NW = C::NW;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -794,9 +820,10 @@ __global__ void __launch_bounds__(ItemCfg<SUBLOG, T>::NT, 1)
             sub_item<SUBLOG, T>(wb, N / 2, S, U, kc.u, cbuf, cbuf + SPlan<SUBLOG>::m + 1, tid,
                                 fold_x ? x + b * N : nullptr, tm, wrow, bar, &phase);
         } else if (it.kind == 1) {
-            leaf_item<SUBLOG, T, NT, NW>(tasks + it.k0, 1, S, U, kc.u, wb, tid, x + b * N, N, tm, wrow, bar, &phase);
+            leaf_item<SUBLOG, T, NT, NW, 1, FX>(tasks + it.k0, 1, S, U, kc.u, wb, tid, x + b * N, N, tm, wrow, bar,
+                                                &phase);
         } else {
-            leaf_item<SUBLOG - 1, T, NT, NW>(tasks + it.k0, 2, S, U, kc.u, wb, tid, x + b * N, N, tm, wrow, bar,
+            leaf_item<SUBLOG - 1, T, NT, NW, 2, FX>(tasks + it.k0, 2, S, U, kc.u, wb, tid, x + b * N, N, tm, wrow, bar,
                                              &phase);
         }
         __syncthreads();
@@ -1104,8 +1131,16 @@ int QFT_LG(qft_large_exec)(void *pp, int mode, const void *d_in, void *d_out, lo
                           (int)!S.fold, tmap, use_tma);
         };
         switch (p->sublog) {
+#if QFT_LARGE_PREC == 32 || QFT_FOLD64
+#define QFT_IT(SL)                                                                                       \
+    case SL:                                                                                             \
+        e = S.fold ? run(lg_item_kernel<SL, T, false>, ItemCfg<SL, T>::NT, ItemCfg<SL, T>::SMEM)         \
+                   : run(lg_item_kernel<SL, T, true>, ItemCfg<SL, T>::NT, ItemCfg<SL, T>::SMEM);         \
+        break;
+#else
 #define QFT_IT(SL) \
-    case SL: e = run(lg_item_kernel<SL, T>, ItemCfg<SL, T>::NT, ItemCfg<SL, T>::SMEM); break;
+    case SL: e = run(lg_item_kernel<SL, T, false>, ItemCfg<SL, T>::NT, ItemCfg<SL, T>::SMEM); break;
+#endif
             QFT_IT(12) QFT_IT(13)
 #if QFT_LARGE_PREC == 32
             QFT_IT(14)

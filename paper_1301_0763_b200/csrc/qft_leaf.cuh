@@ -63,4 +63,23 @@ struct LeafTop {
     }
 };
 
+// The cosine and the sine leaf of one Lee block read straight from x: one gather
+// of x[n], x[N-n] feeds both folds (dc = a + b, ds = a - b, shared.py:28-35), then
+// each side runs its own RT levels -- the operations of two tf_load_x calls.
+template <int A, typename T>
+QFT_HD void tf_load_x_pair(const vec2<T> *x, int N, int j, const T *U, int t, vec2<T> *vc, vec2<T> *vs) {
+    using LC = LeafTop<A, false, T>;
+#pragma unroll
+    for (int q = 0; q < LC::G; ++q) {
+        int c, sg;
+        run_of(LC::RT, LC::L, q, c, sg);
+        const int n = (2 * (c + sg * t) + 1) << j;
+        const vec2<T> a = x[n], b = x[N - n];
+        vc[q] = vadd(a, b);
+        vs[q] = vsub(a, b);
+    }
+    lee_fwd<LC::RT, LC::L, false, T>(vc, t, U);
+    lee_fwd<LC::RT, LC::L, true, T>(vs, t, U);
+}
+
 }  // namespace qft
