@@ -250,6 +250,12 @@ constexpr bool smem_fits() {
 }
 
 // ------------------------------------------------------------ small N
+// signals per CTA of the register kernel's complex mode (= its threads): 128, or 64
+// where 128 rows of NN + 1 cells would exceed the 48 KB of static shared memory
+template <int NN, typename T>
+struct RegCfg {
+    static constexpr int SIG = (128 * (NN + 1) * (int)sizeof(vec2<T>) + 1024 > 48 * 1024) ? 64 : 128;
+};
 template <int NN, typename T, int MODE = 0>
 __global__ void __launch_bounds__(128) qft_cdft_reg(const vec2<T> *__restrict__ in, vec2<T> *__restrict__ out,
                                                     long long batch, const T *__restrict__ U, long long nreal = 0) {
@@ -257,15 +263,35 @@ __global__ void __launch_bounds__(128) qft_cdft_reg(const vec2<T> *__restrict__ 
     for (int i = threadIdx.x; i < (NN / 4 >= 2 ? NN / 4 : 2); i += blockDim.x) sU[i] = U[i];
     __syncthreads();
     constexpr int m = NN / 2;
+    if constexpr (MODE == 0) {
+        // the CTA's signals go through shared memory (rows of NN + 1 cells): coalesced
+        // global loads / stores, conflict-free per-thread rows -- a thread reading its own
+        // signal from global memory touched 32 sectors per load instruction (27 % of HBM
+        // at N = 32 fp32; tools/size_sweep.py)
+        constexpr int SIG = RegCfg<NN, T>::SIG;
+        __shared__ vec2<T> stage[SIG * (NN + 1)];
+        for (long long b0 = (long long)blockIdx.x * SIG; b0 < batch; b0 += (long long)gridDim.x * SIG) {
+            const int cnt = (int)(batch - b0 < SIG ? batch - b0 : SIG);
+            for (int i = threadIdx.x; i < cnt * NN; i += SIG) stage[(i / NN) * (NN + 1) + (i % NN)] = in[b0 * NN + i];
+            __syncthreads();
+            if ((int)threadIdx.x < cnt) {
+                vec2<T> x[NN], y[NN];
+                vec2<T> *row = stage + threadIdx.x * (NN + 1);
+#pragma unroll
+                for (int n = 0; n < NN; ++n) x[n] = row[n];
+                cdft_reg<NN, T>(x, y, sU);
+#pragma unroll
+                for (int n = 0; n < NN; ++n) row[n] = y[n];
+            }
+            __syncthreads();
+            for (int i = threadIdx.x; i < cnt * NN; i += SIG) out[b0 * NN + i] = stage[(i / NN) * (NN + 1) + (i % NN)];
+            __syncthreads();
+        }
+        return;
+    }
     for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < batch;
          b += (long long)gridDim.x * blockDim.x) {
         if constexpr (MODE == 0) {
-            vec2<T> x[NN], y[NN];
-#pragma unroll
-            for (int n = 0; n < NN; ++n) x[n] = in[b * NN + n];
-            cdft_reg<NN, T>(x, y, sU);
-#pragma unroll
-            for (int n = 0; n < NN; ++n) out[b * NN + n] = y[n];
         } else {
             constexpr int RL = MODE == 1 ? NN : (MODE == 2 ? m + 1 : (m > 1 ? m - 1 : 1));
             const T *xr = reinterpret_cast<const T *>(in);
@@ -918,11 +944,12 @@ constexpr int smem_config_bytes() { return KCfg<LOG2N, T>::SMEM; }
 
 template <int NN, typename T, int MODE = 0>
 cudaError_t launch_reg(const LaunchArgs &a) {
-    long long blocks = (a.batch + 127) / 128;
+    constexpr int NT = MODE == 0 ? RegCfg<NN, T>::SIG : 128;
+    long long blocks = (a.batch + NT - 1) / NT;
     long long cap = (long long)a.num_sms * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    qft_cdft_reg<NN, T, MODE><<<(unsigned)blocks, 128, 0, a.stream>>>((const vec2<T> *)a.in, (vec2<T> *)a.out,
+    qft_cdft_reg<NN, T, MODE><<<(unsigned)blocks, NT, 0, a.stream>>>((const vec2<T> *)a.in, (vec2<T> *)a.out,
                                                                       a.batch, (const T *)a.U, a.nreal);
     return cudaGetLastError();
 }
