@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(256, 3) cl_subtree_kernel(V *Wd, long long Ws,
                                                          bool do_cos, bool do_sin, const Real *__restrict__ Tt) {
     extern __shared__ __align__(16) unsigned char cl_smem[];
     const int sublog = log2n - d0, S0 = 1 << (sublog - 1), CBtop = cl::cos_cells(log2n);
-    V *P0 = reinterpret_cast<V *>(cl_smem), *P1 = P0 + cl::buf_cells(sublog);
+    V *P0 = reinterpret_cast<V *>(cl_smem);
     const int tid = threadIdx.x, NT = blockDim.x;
     for (long long g = blockIdx.x; g < (units << d0); g += gridDim.x) {
         const long long u = g >> d0;
