@@ -8,6 +8,10 @@
 #error "compile with -DQFT_INST_PREC=<32|64> -DQFT_INST_LOG2N=<1..14>"
 #endif
 
+#ifndef QFT_REG64
+#define QFT_REG64 1  // complex fp32 N = 64: one thread per signal in registers behind the shared-memory staging (146 registers; fp64 would spill)
+#endif
+
 #define QFT_CAT3(a, b, c) a##_##b##_##c
 #define QFT_NAME(P, L) QFT_CAT3(qft_inst_launch, P, L)
 
@@ -51,6 +55,7 @@ int smem_launch(const qft::LaunchArgs *a, int mode) {
         switch (mode) {
             case 0:
                 if constexpr (qft::use_pipe<L, R>()) return (int)qft::launch_pipe<L, R>(*a);
+                else if constexpr (QFT_REG64 && L == 6 && sizeof(R) == 4) return (int)qft::launch_reg<64, R, 0>(*a);
                 else return (int)qft::launch_smem<L, R, 0>(*a);
             case 1: return (int)qft::launch_smem<L, R, 1>(*a);
             case 2: return (int)qft::launch_smem<L, R, 2>(*a);

@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(128) qft_cdft_reg(const vec2<T> *__restrict__ 
     }
     for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < batch;
          b += (long long)gridDim.x * blockDim.x) {
-        {
+        if constexpr (MODE != 0) {
             constexpr int RL = MODE == 1 ? NN : (MODE == 2 ? m + 1 : (m > 1 ? m - 1 : 1));
             const T *xr = reinterpret_cast<const T *>(in);
             const long long ra = 2 * b, rb = ra + 1 < nreal ? ra + 1 : ra;
