@@ -643,6 +643,9 @@ QFT_DEV void fused_units(vec2<T> *W, const T *U, const T *kcu, int ntr, int warp
 // iteration flat over the CTA's threads (the chunks of a side are the cells
 // [32k, 32k+32), k < NL32, after the sub-block-major F stores), then C by warp
 // units.  Same per-cell operations, two more CTA barriers per iteration.
+#ifndef QFT_SMEM_L2PF
+#define QFT_SMEM_L2PF 0  // L2 bulk prefetch of the batch after the next (single-pass kernel with TMA staging): measured -0.6 % (fp32 2^10), -1 % (fp64 2^10), +0.9 % (fp32 2^11)
+#endif
 #ifndef QFT_PHASED
 #define QFT_PHASED 1
 #endif
@@ -841,6 +844,12 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
         if (TMA && tid == 0 && bt + gridDim.x < nbatch) {
             const long long nb = bt + gridDim.x;
             tma_bulk_load(stage, in + nb * tt * P::N, (uint32_t)(stage_count(nb) * P::N * K::VB), bar);
+#if QFT_SMEM_L2PF
+            // and the batch after that into L2, so that its bulk copy one iteration later
+            // is served from L2 (ncu at N = 1024: 22 % of the stall samples wait for the copy)
+            const long long nb2 = nb + gridDim.x;
+            if (nb2 < nbatch) l2_prefetch(in + nb2 * tt * P::N, (uint32_t)(stage_count(nb2) * P::N * K::VB));
+#endif
         }
         // TF: top forward levels of the huge blocks (N > 4096; ends with a barrier)
         if constexpr (P::JH > 0) top_f<LOG2N, T, MODE>(W, U, ntr, tid);
