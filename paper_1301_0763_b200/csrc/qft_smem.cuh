@@ -35,7 +35,18 @@
 #define QFT_CHAIN_LIN 0  // phase-D unfold with linear addresses (Chain::up_l); measured neutral (58.3 vs 58.5M, config 2)
 #endif
 #ifndef QFT_RC_SMALL
-#define QFT_RC_SMALL 5  // phase-D unfold depth for N <= 2^12
+#define QFT_RC_SMALL 5  // phase-D unfold depth for N = 2^12
+#endif
+#ifndef QFT_RC_MID
+// N = 512 .. 2048 and N <= 256: the small CTAs of these sizes (several resident per SM,
+// qft_launch.cuh cps_for) want more, shorter phase-D items.  Measured depth 5 / 4 / 3
+// (GB/s, tools/size_sweep.py): fp32 2^7 2882 / 3436 / 3807, 2^8 2968 / 3464 / 3533,
+// 2^9 3375 / 3736 / 3680, 2^10 3646 / 3796 / 3630, 2^11 3364 / 3363 / 3241;
+// fp64 2^7 3239 / 4007 / 4135, 2^9 3447 / 3644 / 3624, 2^11 3338 / 3455 / 3410
+#define QFT_RC_MID 4
+#endif
+#ifndef QFT_RC_TINY
+#define QFT_RC_TINY 3
 #endif
 #ifndef QFT_RC_BIG
 #define QFT_RC_BIG 5  // phase-D unfold depth for N >= 2^13 (257 items at 2^14)
@@ -75,7 +86,7 @@ struct SPlan {
     static constexpr int n = LOG2N, N = 1 << LOG2N, m = N / 2, q = N / 4;
     static constexpr int JF = n > 7 ? n - 7 : 0;     // big blocks j < JF (L > 32)
     static constexpr int JS = n - 6;                 // first small block (L = 16)
-    static constexpr int RC0 = n >= 13 ? QFT_RC_BIG : QFT_RC_SMALL;
+    static constexpr int RC0 = n >= 13 ? QFT_RC_BIG : (n >= 12 ? QFT_RC_SMALL : (n >= 9 ? QFT_RC_MID : QFT_RC_TINY));
     static constexpr int RC = n - 2 < RC0 ? n - 2 : RC0;  // chain levels unfolded in phase D
     static constexpr int L(int j) { return 1 << (n - 2 - j); }
     static constexpr int off(int j) { return m - 2 * L(j); }
