@@ -162,7 +162,8 @@ QFT_DEV void l2_prefetch(const void *src, uint32_t bytes) {
 // phases of a small transform are short and separated by CTA barriers (ncu:
 // barrier was 36 % of the stall samples at N = 1024 with one CTA per SM); more
 // resident CTAs fill them.  Measured 1 / 2 / 3 CTAs (tools/size_sweep.py, % of HBM):
-// fp32 2^10 48.8 / 52.8 / 56.6, 2^11 50.3 / 52.4 / 50.0, 2^7 44.7 / 32.1 / 32.8;
+// fp32 2^10 48.8 / 52.8 / 56.6, 2^11 50.3 / 52.4 / 50.0 (4 CTAs: 58.0 after the phase-D
+// depth change, qft_smem.cuh QFT_RC_MID), 2^7 44.7 / 32.1 / 32.8;
 // fp64 2^9 48.4 / 53.7 / 54.1, 2^11 49.8 / 45.6 / 51.9
 #define QFT_CPS_SMALL 0
 #endif
@@ -183,7 +184,7 @@ constexpr int cps_for() {
     if (LOG2N <= 11) {
         if (QFT_CPS_SMALL > 0) return QFT_CPS_SMALL;
         if (sizeof(T) == 4 && LOG2N == 7) return 1;
-        if (sizeof(T) == 4 && LOG2N == 11) return 2;
+        if (sizeof(T) == 4 && LOG2N == 11) return 4;  // with QFT_RC_MID = 4: 52.0 (2 CTAs) / 58.0 % (4 CTAs, one signal each)
         // fp64 2^10 measured 49.0 / 51.7 / 51.5 %; one CTA keeps the small-batch
         // latency of BASELINE config 1 (64 signals: one 12-warp CTA per signal)
         if (sizeof(T) == 8 && LOG2N == 10) return 1;
