@@ -183,7 +183,10 @@ template <int LOG2N, typename T>
 constexpr int cps_for() {
     if (LOG2N <= 11) {
         if (QFT_CPS_SMALL > 0) return QFT_CPS_SMALL;
-        if (sizeof(T) == 4 && LOG2N == 7) return 1;
+        // N <= 256, re-measured after the phase-D depth change (4 / 6 / 8 CTAs, % of HBM):
+        // fp32 2^7 73.7 / 70.8 / 74.5, 2^8 56.6 / 55.8 / 56.6; fp64 2^6 61.9 / 59.2 / 69.0,
+        // 2^7 70.4 / 59.5 / 68.2, 2^8 60.3 / 59.4 / 62.6 (3 CTAs: fp32 2^7 59.1, fp64 2^6 53.4)
+        if (LOG2N <= 8) return (sizeof(T) == 8 && LOG2N != 7) ? 8 : 4;
         if (sizeof(T) == 4 && LOG2N == 11) return 4;  // with QFT_RC_MID = 4: 52.0 (2 CTAs) / 58.0 % (4 CTAs, one signal each)
         // fp64 2^10 measured 49.0 / 51.7 / 51.5 %; one CTA keeps the small-batch
         // latency of BASELINE config 1 (64 signals: one 12-warp CTA per signal)
