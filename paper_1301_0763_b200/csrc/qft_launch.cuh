@@ -172,6 +172,14 @@ QFT_DEV void l2_prefetch(const void *src, uint32_t bytes) {
 #ifndef QFT_TT_MID
 #define QFT_TT_MID 1
 #endif
+#ifndef QFT_U13_SPLIT
+// fp32 N = 8192: only the constants of the Lee blocks of <= 1024 cells (U[0..1024), what
+// the warp units read) live in shared memory; the top fold levels read theirs from
+// global memory (L1-resident).  The 4 KB saved let a third CTA fit (3 x 72 KB).
+// Measured slower (46.2 vs 50.1 % of HBM with 2 CTAs: 80 registers with spills, the top
+// levels' constants from global memory); off.
+#define QFT_U13_SPLIT 0
+#endif
 #ifndef QFT_CPS_MID
 #define QFT_CPS_MID 2  // measured (TT, CTAs) = (3, 1) / (1, 1) / (1, 2): fp32 2^13 33.1 / 47.9 / 49.7 %, fp64 2^12 40.8 / 41.0 / 42.3 % of HBM
 #endif
@@ -193,14 +201,21 @@ constexpr int cps_for() {
         if (sizeof(T) == 8 && LOG2N == 10) return 1;
         return 3;
     }
-    if (mid_class<LOG2N, T>()) return QFT_CPS_MID;
+    if (mid_class<LOG2N, T>()) return (QFT_U13_SPLIT && sizeof(T) == 4 && LOG2N == 13) ? 3 : QFT_CPS_MID;
     return (LOG2N <= 12 && QFT_CTAS_PER_SM > 1) ? QFT_CTAS_PER_SM : 1;
+}
+// level-table entries kept in shared memory (QFT_U13_SPLIT: the first 1024)
+template <int LOG2N, typename T>
+constexpr int ucells_smem() {
+    return (QFT_U13_SPLIT && sizeof(T) == 4 && LOG2N == 13) ? 1024 : SPlan<LOG2N>::UCELLS;
 }
 template <int LOG2N, typename T>
 struct KCfg {
     using P = SPlan<LOG2N>;
     static constexpr int VB = (int)sizeof(vec2<T>);
-    static constexpr int UB = P::UCELLS * (int)sizeof(T);
+    static constexpr int UCS = ucells_smem<LOG2N, T>();
+    static constexpr bool USPLIT = UCS < P::UCELLS;
+    static constexpr int UB = UCS * (int)sizeof(T);
     // CTAs per SM: the QFT_CTAS_PER_SM split applies where one signal still fits
     static constexpr int CPS = cps_for<LOG2N, T>();
     static constexpr int BUDGET = (226 * 1024) / CPS - UB - 64;
@@ -250,7 +265,8 @@ struct KCfg {
 template <int LOG2N, typename T>
 constexpr bool smem_fits() {
     using P = SPlan<LOG2N>;
-    return (P::PADDED * (int)sizeof(vec2<T>) + P::UCELLS * (int)sizeof(T) + 64) <= (226 * 1024) / cps_for<LOG2N, T>();
+    return (P::PADDED * (int)sizeof(vec2<T>) + ucells_smem<LOG2N, T>() * (int)sizeof(T) + 64) <=
+           (226 * 1024) / cps_for<LOG2N, T>();
 }
 
 // ------------------------------------------------------------ small N
@@ -776,7 +792,7 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
 
     const long long nbatch = (batch + tt - 1) / tt;
     const A0Lane64 a0l64 = a0_lane64<LOG2N>(lane);
-    for (int i = tid; i < P::UCELLS; i += NT) U[i] = Ug[i];
+    for (int i = tid; i < K::UCS; i += NT) U[i] = Ug[i];
     if (TMA && tid == 0) mbar_init(bar, 1);
     __syncthreads();
     long long bt = blockIdx.x;
@@ -856,7 +872,7 @@ __global__ void __launch_bounds__(KCfg<LOG2N, T>::NT, KCfg<LOG2N, T>::CPS)
 #endif
         }
         // TF: top forward levels of the huge blocks (N > 4096; ends with a barrier)
-        if constexpr (P::JH > 0) top_f<LOG2N, T, MODE>(W, U, ntr, tid);
+        if constexpr (P::JH > 0) top_f<LOG2N, T, MODE>(W, K::USPLIT ? Ug : U, ntr, tid);
         // A+B+C fused: one warp per (signal, side, unit) -- no CTA barrier inside
         if constexpr (use_phased<LOG2N>()) phased_units<LOG2N, T, MODE, TT, NW>(W, U, kc.u, ntr, tid);
         else fused_units<LOG2N, T, MODE, TT, NW>(W, U, kc.u, ntr, warp, lane);
